@@ -1,0 +1,393 @@
+// Stage 1 merge (slices / shards -> global top-k), and stages 1b-3 fused:
+// neighbour-length histogram -> ResourceBound cost law -> Gittins index, plus
+// the running-request refresh.  sm_100a.
+//
+// Reference semantics:
+//   predict         SPEC.md:182-194 (>= min_matches neighbours, else fallback)
+//   cost            cost.py:97-99 (conditional-mean cost per bin; exact at w=1)
+//   gittins         _kernels.py:110-115 in exact integer-count form
+//   conditioning    SPEC.md:335-343, outlived rule SPEC.md:373
+//   refresh cadence SPEC.md:345-353
+#include "ss_common.cuh"
+#include "ss_internal.h"
+
+namespace ss {
+
+// ---------------------------------------------------------------------------
+// merge: per query, select the top-k of nlists*k candidate composites by an
+// MSB-first 8-bit radix select, then bitonic-sort the k winners descending.
+// ---------------------------------------------------------------------------
+constexpr int MERGE_THREADS = 256;
+
+__global__ void __launch_bounds__(MERGE_THREADS)
+k_merge(const uint64_t* __restrict__ comp, const int32_t* __restrict__ len, int nlists,
+        int64_t nq, int k, int kpad, uint64_t* __restrict__ out_comp,
+        int32_t* __restrict__ out_len, const int32_t* __restrict__ bank_lens, int64_t head,
+        int64_t gcap, int64_t slot_offset) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int M = nlists * k;
+  uint64_t* cand = reinterpret_cast<uint64_t*>(smem);            // [M]
+  uint64_t* sel = cand + M;                                      // [kpad]
+  int32_t* clen = reinterpret_cast<int32_t*>(sel + kpad);        // [M] (if len)
+  int32_t* slen = clen + (len ? M : 0);                          // [kpad]
+  __shared__ int hist[256];
+  __shared__ int s_cnt, s_digit, s_need;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t q = blockIdx.x;
+
+  int nz = 0;
+  for (int i = tid; i < M; i += MERGE_THREADS) {
+    int l = i / k, j = i % k;
+    int64_t src = ((int64_t)l * nq + q) * k + j;
+    uint64_t c = comp[src];
+    cand[i] = c;
+    if (len) clen[i] = len[src];
+    nz += (c != 0ull);
+  }
+  for (int o = 16; o > 0; o >>= 1) nz += __shfl_xor_sync(0xffffffffu, nz, o);
+  if (tid == 0) s_cnt = 0;
+  __syncthreads();
+  if (lane == 0) atomicAdd(&s_cnt, nz);
+  __syncthreads();
+  const int m0 = s_cnt;
+
+  uint64_t kth = 1ull;  // select every non-zero when m0 <= k
+  if (m0 > k) {
+    uint64_t prefix = 0, mask = 0;
+    int need = k;
+    for (int shift = 56; shift >= 0; shift -= 8) {
+      hist[tid] = 0;
+      __syncthreads();
+      for (int i0 = 0; i0 < M; i0 += MERGE_THREADS) {
+        int i = i0 + tid;
+        bool act = false;
+        int d = 0;
+        if (i < M) {
+          uint64_t c = cand[i];
+          act = (c & mask) == prefix;
+          d = (int)((c >> shift) & 255ull);
+        }
+        unsigned am = __ballot_sync(0xffffffffu, act);
+        if (act) {
+          unsigned peers = __match_any_sync(am, d);
+          if ((peers & ((1u << lane) - 1u)) == 0u) atomicAdd(&hist[d], __popc(peers));
+        }
+      }
+      __syncthreads();
+      if (warp == 0) {
+        // lane l owns digits [255-8l .. 248-8l] (descending)
+        int local = 0;
+#pragma unroll
+        for (int t = 0; t < 8; ++t) local += hist[255 - 8 * lane - t];
+        int incl = warp_incl_scan_i32(local, lane);
+        int excl = incl - local;
+        if (excl < need && incl >= need) {
+          int cum = excl;
+          for (int t = 0; t < 8; ++t) {
+            int d = 255 - 8 * lane - t;
+            if (cum + hist[d] >= need) { s_digit = d; s_need = need - cum; break; }
+            cum += hist[d];
+          }
+        }
+      }
+      __syncthreads();
+      prefix |= (uint64_t)s_digit << shift;
+      mask |= 255ull << shift;
+      need = s_need;
+      __syncthreads();
+    }
+    kth = prefix;
+  }
+  // gather winners (c >= kth), unordered, then bitonic sort descending
+  for (int i = tid; i < kpad; i += MERGE_THREADS) sel[i] = 0ull;
+  if (tid == 0) s_cnt = 0;
+  __syncthreads();
+  for (int i = tid; i < M; i += MERGE_THREADS) {
+    uint64_t c = cand[i];
+    if (c != 0ull && c >= kth) {
+      int p = atomicAdd(&s_cnt, 1);
+      if (p < kpad) {
+        sel[p] = c;
+        if (len) slen[p] = clen[i];
+      }
+    }
+  }
+  __syncthreads();
+  // bitonic sort (descending) of (sel, slen) over kpad (power of two)
+  for (int size = 2; size <= kpad; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = tid; i < kpad; i += MERGE_THREADS) {
+        int j = i ^ stride;
+        if (j > i) {
+          bool desc = ((i & size) == 0);
+          uint64_t a = sel[i], b = sel[j];
+          if ((a < b) == desc) {
+            sel[i] = b;
+            sel[j] = a;
+            if (len) { int32_t t = slen[i]; slen[i] = slen[j]; slen[j] = t; }
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = tid; i < k; i += MERGE_THREADS) {
+    uint64_t c = sel[i];
+    out_comp[q * k + i] = c;
+    int32_t L = 0;
+    if (c != 0ull) {
+      if (len) {
+        L = slen[i];
+      } else {
+        int64_t g = ((int64_t)comp_rel(c) + head) % gcap;
+        L = bank_lens[g - slot_offset];
+      }
+    }
+    out_len[q * k + i] = L;
+  }
+}
+
+int launch_merge(const uint64_t* comp, const int32_t* len, int nlists, int64_t nq, int k,
+                 uint64_t* out_comp, int32_t* out_len, const int32_t* bank_lens, int64_t head,
+                 int64_t gcap, int64_t slot_offset, cudaStream_t st) {
+  if (nq <= 0) return SS_OK;
+  int kpad = 1;
+  while (kpad < k) kpad <<= 1;
+  int64_t M = (int64_t)nlists * k;
+  size_t smem = (size_t)M * 8 + (size_t)kpad * 8 + (len ? (size_t)M * 4 + (size_t)kpad * 4 : 0);
+  if (smem > 220 * 1024)
+    return set_error(SS_ERR_UNSUPPORTED, "merge of %d lists x k=%d exceeds shared memory", nlists, k);
+  SS_CUDA_TRY(cudaFuncSetAttribute(k_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  count_launch();
+  k_merge<<<(unsigned)nq, MERGE_THREADS, smem, st>>>(comp, len, nlists, nq, k, kpad, out_comp,
+                                                    out_len, bank_lens, head, gcap, slot_offset);
+  SS_LAUNCH_CHECK();
+  return SS_OK;
+}
+
+__global__ void k_decode(const uint64_t* __restrict__ comp, int64_t n, int64_t head,
+                         int64_t capacity, float* __restrict__ key, int64_t* __restrict__ seq,
+                         int64_t* __restrict__ slot) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint64_t c = comp[i];
+  if (c == 0ull) {
+    if (key) key[i] = __int_as_float(0x7fc00000);
+    if (seq) seq[i] = -1;
+    if (slot) slot[i] = -1;
+    return;
+  }
+  int64_t rel = comp_rel(c);
+  if (key) key[i] = comp_key(c);
+  if (seq) seq[i] = head - capacity + rel;
+  if (slot) slot[i] = (rel + head) % capacity;
+}
+
+int launch_decode(const uint64_t* comp, int64_t n, int64_t head, int64_t capacity, float* key,
+                  int64_t* seq, int64_t* slot, cudaStream_t st) {
+  if (n <= 0) return SS_OK;
+  count_launch();
+  k_decode<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(comp, n, head, capacity, key, seq, slot);
+  SS_LAUNCH_CHECK();
+  return SS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// exact integer-count Gittins over a sorted sparse law (one warp).
+//   D_k = sum v^2 + 2 I sum v over bin k  (so c_k s_k = D_k / 2 exactly)
+//   attained 2a = A2 = g^2 + 2 I g; survivors D_k > A2 c_k (a suffix)
+//   ratio_k = (0.5 P'_k + ((D_k - A2 c_k) 0.5 / c_k) (T' - C'_k)) / C'_k
+//   P'_k = sum_{j<=k surv} (D_j - A2 c_j), C'_k = sum c_j, T' = C'_last
+// All integer sums are exact, the fp64 ops are explicit _rn (no FMA
+// contraction) in the same order as oracle.gittins_points -> bit-identical.
+// ---------------------------------------------------------------------------
+__device__ double warp_gittins_exact(const int32_t* c, const int64_t* D, int np, long long A2,
+                                     int I, int g, int bucket, int lane) {
+  int first = np;
+  for (int b = 0; b < np; b += 32) {
+    int k = b + lane;
+    bool s = (k < np) && (D[k] > A2 * (long long)c[k]);
+    unsigned ball = __ballot_sync(0xffffffffu, s);
+    if (ball) { first = b + __ffs(ball) - 1; break; }
+  }
+  if (first >= np) {  // outlived every predicted length
+    long long gb = (long long)g + bucket;
+    return __dadd_rn(__dmul_rn((double)(gb * gb - (long long)g * g), 0.5),
+                     __dmul_rn((double)I, (double)bucket));
+  }
+  long long T = 0;
+  for (int k = first + lane; k < np; k += 32) T += c[k];
+  for (int o = 16; o > 0; o >>= 1) T += __shfl_xor_sync(0xffffffffu, T, o);
+  long long Cc = 0, Pc = 0;
+  double best = INFINITY;
+  for (int b = first; b < np; b += 32) {
+    int k = b + lane;
+    long long ck = 0, dk = 0;
+    if (k < np) {
+      ck = c[k];
+      dk = D[k] - A2 * ck;
+    }
+    long long C = warp_incl_scan_i64(ck, lane) + Cc;
+    long long P = warp_incl_scan_i64(dk, lane) + Pc;
+    if (k < np) {
+      double sk = __ddiv_rn(__dmul_rn((double)dk, 0.5), (double)ck);
+      double num = __dadd_rn(__dmul_rn((double)P, 0.5), __dmul_rn(sk, (double)(T - C)));
+      double r = __ddiv_rn(num, (double)C);
+      best = fmin(best, r);
+    }
+    Cc = __shfl_sync(0xffffffffu, C, 31);
+    Pc = __shfl_sync(0xffffffffu, P, 31);
+  }
+  return warp_min_f64(best);
+}
+
+// ---------------------------------------------------------------------------
+// finish: one CTA per request.  Histogram with shared-memory atomics, ascending
+// ballot-scan compaction into the sparse law, then warp-0 Gittins.
+// ---------------------------------------------------------------------------
+constexpr int FIN_THREADS = 128;
+
+__global__ void __launch_bounds__(FIN_THREADS)
+k_finish(const uint64_t* __restrict__ comp, const int32_t* __restrict__ len, int64_t nq, int k,
+         int min_matches, int max_len, int nbins, const int32_t* __restrict__ I,
+         const int64_t* __restrict__ fb_cnt, const int64_t* __restrict__ fb_sv,
+         const int64_t* __restrict__ fb_sv2, int P, int32_t* __restrict__ npts,
+         int32_t* __restrict__ pbin, int32_t* __restrict__ pcnt, int64_t* __restrict__ pD,
+         int64_t* __restrict__ psv, uint8_t* __restrict__ used_fb, double* __restrict__ G) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  int64_t* h_sv = reinterpret_cast<int64_t*>(smem);         // [nbins]
+  int64_t* h_sv2 = h_sv + nbins;                            // [nbins]
+  int64_t* l_D = h_sv2 + nbins;                             // [nbins]
+  int32_t* h_cnt = reinterpret_cast<int32_t*>(l_D + nbins); // [nbins]
+  int32_t* l_c = h_cnt + nbins;                             // [nbins]
+  __shared__ int s_m, s_base, s_warp[FIN_THREADS / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t q = blockIdx.x;
+  const int w = max_len / nbins;
+  const long long Iq = I[q];
+
+  int m = 0;
+  for (int i = tid; i < k; i += FIN_THREADS) m += (comp[q * k + i] != 0ull);
+  for (int o = 16; o > 0; o >>= 1) m += __shfl_xor_sync(0xffffffffu, m, o);
+  if (tid == 0) { s_m = 0; s_base = 0; }
+  __syncthreads();
+  if (lane == 0) atomicAdd(&s_m, m);
+  __syncthreads();
+  const bool fb = s_m < min_matches;
+  if (!fb) {
+    for (int b = tid; b < nbins; b += FIN_THREADS) { h_cnt[b] = 0; h_sv[b] = 0; h_sv2[b] = 0; }
+    __syncthreads();
+    for (int i = tid; i < k; i += FIN_THREADS) {
+      if (comp[q * k + i] == 0ull) continue;
+      int L = min(max(len[q * k + i], 1), max_len);
+      int b = (L - 1) / w;
+      atomicAdd(&h_cnt[b], 1);
+      atomicAdd(reinterpret_cast<unsigned long long*>(&h_sv[b]), (unsigned long long)L);
+      atomicAdd(reinterpret_cast<unsigned long long*>(&h_sv2[b]),
+                (unsigned long long)((long long)L * L));
+    }
+  } else {
+    for (int b = tid; b < nbins; b += FIN_THREADS) {
+      h_cnt[b] = (int32_t)fb_cnt[b];
+      h_sv[b] = fb_sv[b];
+      h_sv2[b] = fb_sv2[b];
+    }
+  }
+  __syncthreads();
+  // ascending compaction of non-empty bins
+  for (int b0 = 0; b0 < nbins; b0 += FIN_THREADS) {
+    int b = b0 + tid;
+    int c = (b < nbins) ? h_cnt[b] : 0;
+    unsigned ball = __ballot_sync(0xffffffffu, c > 0);
+    if (lane == 0) s_warp[warp] = __popc(ball);
+    __syncthreads();
+    int off = s_base;
+    for (int ww = 0; ww < warp; ++ww) off += s_warp[ww];
+    if (c > 0) {
+      int pos = off + __popc(ball & ((1u << lane) - 1u));
+      long long D = h_sv2[b] + 2 * Iq * h_sv[b];
+      l_c[pos] = c;
+      l_D[pos] = D;
+      if (pos < P) {
+        pbin[q * P + pos] = b;
+        pcnt[q * P + pos] = c;
+        pD[q * P + pos] = D;
+        if (psv) psv[q * P + pos] = h_sv[b];
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int add = 0;
+      for (int ww = 0; ww < FIN_THREADS / 32; ++ww) add += s_warp[ww];
+      s_base += add;
+    }
+    __syncthreads();
+  }
+  const int np = s_base;
+  if (warp == 0) {
+    double g = (np > 0) ? warp_gittins_exact(l_c, l_D, np, 0, (int)Iq, 0, 0, lane) : INFINITY;
+    if (lane == 0) {
+      G[q] = g;
+      npts[q] = np;
+      if (used_fb) used_fb[q] = fb ? 1 : 0;
+    }
+  }
+}
+
+int launch_finish(const uint64_t* comp, const int32_t* len, int64_t nq, int k, int min_matches,
+                  int max_len, int nbins, const int32_t* I, const int64_t* fb_cnt,
+                  const int64_t* fb_sv, const int64_t* fb_sv2, int P, int32_t* npts,
+                  int32_t* pbin, int32_t* pcnt, int64_t* pD, int64_t* psv, uint8_t* used_fb,
+                  double* G, cudaStream_t st) {
+  if (nq <= 0) return SS_OK;
+  size_t smem = (size_t)nbins * (8 * 3 + 4 * 2);
+  if (smem > 200 * 1024) return set_error(SS_ERR_UNSUPPORTED, "nbins %d too large", nbins);
+  if (smem > 48 * 1024)
+    SS_CUDA_TRY(cudaFuncSetAttribute(k_finish, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  count_launch();
+  k_finish<<<(unsigned)nq, FIN_THREADS, smem, st>>>(comp, len, nq, k, min_matches, max_len, nbins,
+                                                    I, fb_cnt, fb_sv, fb_sv2, P, npts, pbin, pcnt,
+                                                    pD, psv, used_fb, G);
+  SS_LAUNCH_CHECK();
+  return SS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// refresh: warp per running request (SPEC.md:345-353 cadence).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256)
+k_refresh(int64_t n, const int32_t* __restrict__ I, const int32_t* __restrict__ g_new,
+          int32_t* __restrict__ bucket_io, int bucket_size, const int32_t* __restrict__ npts,
+          const int32_t* __restrict__ pcnt, const int64_t* __restrict__ pD, int P,
+          double* __restrict__ G_io, uint8_t* __restrict__ refreshed, int force) {
+  const int lane = threadIdx.x & 31;
+  const int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (i >= n) return;
+  const int g = g_new[i];
+  const int nb = g / bucket_size;
+  const bool due = force || nb > bucket_io[i];
+  if (due) {
+    const long long Ii = I[i];
+    const long long A2 = (long long)g * g + 2 * Ii * g;
+    double v = warp_gittins_exact(pcnt + i * P, pD + i * P, npts[i], A2, (int)Ii, g, bucket_size,
+                                  lane);
+    if (lane == 0) {
+      G_io[i] = v;
+      bucket_io[i] = nb;
+    }
+  }
+  if (lane == 0 && refreshed) refreshed[i] = due ? 1 : 0;
+}
+
+int launch_refresh(int64_t n, const int32_t* I, const int32_t* g_new, int32_t* bucket_io,
+                   int bucket_size, const int32_t* npts, const int32_t* pcnt, const int64_t* pD,
+                   int P, double* G_io, uint8_t* refreshed, int force, cudaStream_t st) {
+  if (n <= 0) return SS_OK;
+  count_launch();
+  k_refresh<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(n, I, g_new, bucket_io, bucket_size, npts,
+                                                      pcnt, pD, P, G_io, refreshed, force);
+  SS_LAUNCH_CHECK();
+  return SS_OK;
+}
+
+}  // namespace ss

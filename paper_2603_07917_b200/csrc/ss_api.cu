@@ -1,0 +1,521 @@
+// C-ABI layer of libsagesched: argument validation, handle/workspace
+// management and stage orchestration.  Every function here is declared in
+// include/sagesched.h, which cites the reference interface each replaces.
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <atomic>
+#include <mutex>
+#include <new>
+
+#include "ss_common.cuh"
+#include "ss_internal.h"
+
+namespace ss {
+
+static thread_local char g_err[1024] = "";
+static std::atomic<int64_t> g_launches{0};
+
+int set_error(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+int sm_count(int device) {
+  static int cache[64] = {0};
+  if (device < 0 || device >= 64) return 148;
+  if (!cache[device]) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) != cudaSuccess || v <= 0)
+      v = 148;
+    cache[device] = v;
+  }
+  return cache[device];
+}
+
+// per-device sticky error flag for handle-less synchronous entry points
+static int* device_err_flag() {
+  static std::mutex mu;
+  static int* flags[64] = {nullptr};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  if (!flags[dev]) {
+    if (cudaMalloc(&flags[dev], sizeof(int)) != cudaSuccess) return nullptr;
+    cudaMemset(flags[dev], 0, sizeof(int));
+  }
+  return flags[dev];
+}
+
+static int read_and_clear(int* d_err, cudaStream_t st) {
+  int h = 0;
+  if (cudaMemcpyAsync(&h, d_err, sizeof(int), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return set_error(SS_ERR_CUDA, "error-flag readback failed: %s",
+                     cudaGetErrorString(cudaGetLastError()));
+  if (h) cudaMemsetAsync(d_err, 0, sizeof(int), st);
+  return h;
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+}  // namespace ss
+
+using namespace ss;
+
+struct ss_bank {
+  int device;
+  int64_t cap, gcap, slot_offset;
+  int dim;
+  int64_t head;
+  int8_t* emb = nullptr;
+  float* inv = nullptr;
+  int32_t* lens = nullptr;
+  int64_t* seq = nullptr;
+  int* d_err = nullptr;
+  void* ws = nullptr;
+  size_t ws_bytes = 0;
+};
+
+static int ws_reserve(ss_bank* h, size_t bytes) {
+  if (bytes <= h->ws_bytes) return SS_OK;
+  if (h->ws) cudaFree(h->ws);
+  h->ws = nullptr;
+  h->ws_bytes = 0;
+  size_t want = bytes + bytes / 4;
+  SS_CUDA_TRY(cudaMalloc(&h->ws, want));
+  h->ws_bytes = want;
+  return SS_OK;
+}
+
+static inline size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+extern "C" {
+
+const char* ss_last_error(void) { return g_err; }
+int ss_version(void) { return 10000; }
+int64_t ss_launch_count(void) { return g_launches.load(); }
+
+// ------------------------------------------------------------- compat -----
+int ss_match_pmfs(const float* sims, int64_t nq, int64_t nw, const int64_t* lens, float theta,
+                  int64_t max_len, double* sup, double* mas, int64_t* sizes, int64_t out_stride,
+                  void* stream) {
+  if (nq < 0 || nw < 0 || max_len < 1 || out_stride < max_len)
+    return set_error(SS_ERR_ARG, "match_pmfs: bad shape (nq=%lld nw=%lld max_len=%lld stride=%lld)",
+                     (long long)nq, (long long)nw, (long long)max_len, (long long)out_stride);
+  if (nq == 0) return SS_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  int* err = device_err_flag();
+  if (!err) return set_error(SS_ERR_CUDA, "error flag alloc failed");
+  int rc = launch_match_pmfs(sims, nq, nw, lens, theta, max_len, sup, mas, sizes, out_stride, err, st);
+  if (rc) return rc;
+  int e = read_and_clear(err, st);
+  if (e == SS_ERR_RANGE) return set_error(SS_ERR_RANGE, "match_pmfs: a matched length lies outside [0, max_len]");
+  return e;
+}
+
+int ss_gittins_min_batch(const double* support, const double* masses, const int64_t* npts,
+                         int64_t n, int64_t stride, double* out, void* stream) {
+  if (n < 0 || stride < 0) return set_error(SS_ERR_ARG, "gittins_min_batch: bad shape");
+  if (n == 0) return SS_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  int* err = device_err_flag();
+  if (!err) return set_error(SS_ERR_CUDA, "error flag alloc failed");
+  int rc = launch_gittins_dist(support, masses, npts, nullptr, nullptr, n, stride, out, err, 1, st);
+  if (rc) return rc;
+  int e = read_and_clear(err, st);
+  if (e == SS_ERR_ZERODIV) return set_error(SS_ERR_ZERODIV, "float division by zero");
+  return e;
+}
+
+int ss_gittins_dist_batch(const double* support, const double* masses, const int64_t* npts,
+                          const double* attained, const double* outlived_index, int64_t n,
+                          int64_t stride, double* out, void* stream) {
+  if (n < 0 || stride < 0) return set_error(SS_ERR_ARG, "gittins_dist_batch: bad shape");
+  int* err = device_err_flag();
+  if (!err) return set_error(SS_ERR_CUDA, "error flag alloc failed");
+  return launch_gittins_dist(support, masses, npts, attained, outlived_index, n, stride, out, err,
+                             0, (cudaStream_t)stream);
+}
+
+int ss_embed_accumulate_batch(const int64_t* tokens, const int64_t* offsets, int64_t n,
+                              uint64_t salt, int32_t dim, double* out, void* stream) {
+  if (n < 0 || dim < 1) return set_error(SS_ERR_ARG, "embed: bad shape");
+  return launch_embed(tokens, offsets, n, salt, dim, out, nullptr, nullptr, nullptr,
+                      (cudaStream_t)stream);
+}
+
+int ss_embed_quantize_batch(const int64_t* tokens, const int64_t* offsets, int64_t n,
+                            uint64_t salt, int32_t dim, int8_t* out_emb, float* out_inv_norm,
+                            void* stream) {
+  if (n < 0 || dim < 1 || !out_emb || !out_inv_norm) return set_error(SS_ERR_ARG, "embed_quantize: bad args");
+  if (n == 0) return SS_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  int* err = device_err_flag();
+  if (!err) return set_error(SS_ERR_CUDA, "error flag alloc failed");
+  int rc = launch_embed(tokens, offsets, n, salt, dim, nullptr, out_emb, out_inv_norm, err, st);
+  if (rc) return rc;
+  int e = read_and_clear(err, st);
+  if (e == SS_ERR_RANGE) return set_error(SS_ERR_RANGE, "embed_quantize: a bucket exceeds int8 range");
+  return e;
+}
+
+int ss_cost_distribution_batch(int32_t kind, double w_in, double w_out, const double* input_len,
+                               const double* len_support, const int64_t* npts, int64_t n,
+                               int64_t stride, double* out_support, void* stream) {
+  if (kind < 0 || kind > 2) return set_error(SS_ERR_ARG, "unknown cost model kind %d", kind);
+  if (kind == SS_COST_WEIGHTED_SUM && (w_in <= 0 || w_out <= 0))
+    return set_error(SS_ERR_ARG, "weighted-sum weights must be positive");
+  return launch_cost_dist(kind, w_in, w_out, input_len, len_support, npts, n, stride, out_support,
+                          (cudaStream_t)stream);
+}
+
+// ---------------------------------------------------------------- bank ----
+int ss_bank_create(ss_bank_t** out, int32_t device, int64_t capacity, int32_t dim,
+                   int64_t global_capacity, int64_t slot_offset) {
+  if (!out) return set_error(SS_ERR_ARG, "null out");
+  *out = nullptr;
+  if (capacity < 1 || dim < 16 || dim % 16 || global_capacity < capacity || slot_offset < 0 ||
+      slot_offset + capacity > global_capacity || global_capacity >= (1LL << 32))
+    return set_error(SS_ERR_ARG, "bank_create: bad shape (cap=%lld dim=%d gcap=%lld off=%lld)",
+                     (long long)capacity, dim, (long long)global_capacity, (long long)slot_offset);
+  DeviceGuard g(device);
+  ss_bank* h = new (std::nothrow) ss_bank();
+  if (!h) return set_error(SS_ERR_ARG, "oom");
+  h->device = device;
+  h->cap = capacity;
+  h->gcap = global_capacity;
+  h->slot_offset = slot_offset;
+  h->dim = dim;
+  h->head = 0;
+  int rc = SS_OK;
+  auto fail = [&](cudaError_t e) {
+    rc = set_error(SS_ERR_CUDA, "bank_create: %s", cudaGetErrorString(e));
+  };
+  cudaError_t e;
+  if ((e = cudaMalloc(&h->emb, (size_t)capacity * dim)) != cudaSuccess) fail(e);
+  else if ((e = cudaMalloc(&h->inv, (size_t)capacity * 4)) != cudaSuccess) fail(e);
+  else if ((e = cudaMalloc(&h->lens, (size_t)capacity * 4)) != cudaSuccess) fail(e);
+  else if ((e = cudaMalloc(&h->seq, (size_t)capacity * 8)) != cudaSuccess) fail(e);
+  else if ((e = cudaMalloc(&h->d_err, sizeof(int))) != cudaSuccess) fail(e);
+  if (rc == SS_OK) {
+    cudaMemset(h->emb, 0, (size_t)capacity * dim);
+    cudaMemset(h->inv, 0xff, (size_t)capacity * 4);  // NaN: never matches
+    cudaMemset(h->lens, 0, (size_t)capacity * 4);
+    cudaMemset(h->seq, 0xff, (size_t)capacity * 8);  // -1: empty slot
+    cudaMemset(h->d_err, 0, sizeof(int));
+    e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) fail(e);
+  }
+  if (rc != SS_OK) {
+    ss_bank_destroy(h);
+    return rc;
+  }
+  *out = h;
+  return SS_OK;
+}
+
+int ss_bank_destroy(ss_bank_t* h) {
+  if (!h) return SS_OK;
+  DeviceGuard g(h->device);
+  cudaFree(h->emb);
+  cudaFree(h->inv);
+  cudaFree(h->lens);
+  cudaFree(h->seq);
+  cudaFree(h->d_err);
+  cudaFree(h->ws);
+  delete h;
+  return SS_OK;
+}
+
+int ss_bank_push(ss_bank_t* h, const int8_t* emb, const float* inv_norm, const int32_t* lens,
+                 int64_t n, void* stream) {
+  if (!h || n < 0) return set_error(SS_ERR_ARG, "bank_push: bad args");
+  if (h->gcap != h->cap || h->slot_offset != 0)
+    return set_error(SS_ERR_ARG, "bank_push on a shard: use ss_bank_write with the global head");
+  if (n == 0) return SS_OK;
+  int64_t skip = n > h->cap ? n - h->cap : 0;
+  int rc = launch_bank_write(h->emb, h->inv, h->lens, h->seq, h->dim, emb, inv_norm, lens, nullptr,
+                             nullptr, n, h->head, h->cap, skip, h->d_err, (cudaStream_t)stream);
+  if (rc) return rc;
+  h->head += n;
+  return SS_OK;
+}
+
+int ss_bank_write(ss_bank_t* h, const int8_t* emb, const float* inv_norm, const int32_t* lens,
+                  const int64_t* seq, const int64_t* local_slot, int64_t n, void* stream) {
+  if (!h || n < 0 || !seq || !local_slot) return set_error(SS_ERR_ARG, "bank_write: bad args");
+  return launch_bank_write(h->emb, h->inv, h->lens, h->seq, h->dim, emb, inv_norm, lens, seq,
+                           local_slot, n, 0, h->cap, 0, h->d_err, (cudaStream_t)stream);
+}
+
+int ss_bank_set_head(ss_bank_t* h, int64_t global_head) {
+  if (!h || global_head < 0) return set_error(SS_ERR_ARG, "bank_set_head: bad args");
+  h->head = global_head;
+  return SS_OK;
+}
+
+int ss_bank_info(ss_bank_t* h, int64_t* head, int64_t* size, int64_t* capacity, int32_t* dim) {
+  if (!h) return set_error(SS_ERR_ARG, "null bank");
+  if (head) *head = h->head;
+  if (size) *size = h->head < h->gcap ? h->head : h->gcap;
+  if (capacity) *capacity = h->cap;
+  if (dim) *dim = h->dim;
+  return SS_OK;
+}
+
+int ss_bank_device_ptrs(ss_bank_t* h, int8_t** emb, float** inv_norm, int32_t** lens,
+                        int64_t** seq) {
+  if (!h) return set_error(SS_ERR_ARG, "null bank");
+  if (emb) *emb = h->emb;
+  if (inv_norm) *inv_norm = h->inv;
+  if (lens) *lens = h->lens;
+  if (seq) *seq = h->seq;
+  return SS_OK;
+}
+
+int ss_bank_sync_check(ss_bank_t* h, void* stream) {
+  if (!h) return set_error(SS_ERR_ARG, "null bank");
+  DeviceGuard g(h->device);
+  int e = read_and_clear(h->d_err, (cudaStream_t)stream);
+  if (e == SS_ERR_RANGE) return set_error(SS_ERR_RANGE, "bank: a pushed length lies outside [1, 65535]");
+  if (e == SS_ERR_ARG) return set_error(SS_ERR_ARG, "bank: a write targeted a slot outside the shard");
+  return e;
+}
+
+static int check_bins(int32_t max_len, int32_t nbins) {
+  if (max_len < 1 || nbins < 1 || max_len % nbins || nbins > 4096)
+    return set_error(SS_ERR_ARG, "max_len (%d) must be a positive multiple of nbins (%d <= 4096)",
+                     max_len, nbins);
+  return SS_OK;
+}
+
+int ss_bank_fallback_hist(ss_bank_t* h, int32_t max_len, int32_t nbins, int64_t* cnt, int64_t* sv,
+                          int64_t* sv2, void* stream) {
+  if (!h) return set_error(SS_ERR_ARG, "null bank");
+  if (int rc = check_bins(max_len, nbins)) return rc;
+  return launch_fallback_hist(h->lens, h->seq, h->cap, max_len, nbins, cnt, sv, sv2,
+                              (cudaStream_t)stream);
+}
+
+// ------------------------------------------------------------- predict ----
+static int topk_plan(ss_bank* h, const TopkArgs& a, int32_t& algo, int& slices) {
+  bool tc_ok = topk_tc_supported(a);
+  if (algo == SS_ALGO_AUTO) algo = tc_ok ? SS_ALGO_TCGEN05 : SS_ALGO_SCAN;
+  if (algo == SS_ALGO_TCGEN05 && !tc_ok)
+    return set_error(SS_ERR_UNSUPPORTED, "tcgen05 path unsupported for dim=%d k=%d", h->dim, a.k);
+  if (algo != SS_ALGO_TCGEN05 && algo != SS_ALGO_SCAN)
+    return set_error(SS_ERR_ARG, "unknown similarity algo %d", algo);
+  slices = (algo == SS_ALGO_TCGEN05) ? topk_tc_slices(a, h->device) : topk_scan_slices(a, h->device);
+  while ((int64_t)slices * a.k > 16384 && slices > 1) slices = (slices + 1) / 2;
+  return SS_OK;
+}
+
+static size_t topk_ws_need(ss_bank* h, int64_t nq, int32_t k, int32_t algo) {
+  TopkArgs a{nullptr, nullptr, nq, h->emb, h->inv, h->cap, h->dim, k, 0.f, h->head, h->gcap,
+             h->slot_offset};
+  int slices = 1;
+  if (topk_plan(h, a, algo, slices)) return 0;
+  return align_up((size_t)slices * nq * k * 8);
+}
+
+static int topk_impl(ss_bank* h, const int8_t* q, const float* q_inv, int64_t nq, int32_t k,
+                     float theta, int32_t algo, uint64_t* out_comp, int32_t* out_len,
+                     size_t ws_offset, cudaStream_t st) {
+  if (k < 1 || k > 256) return set_error(SS_ERR_ARG, "k must lie in [1, 256], got %d", k);
+  if (nq < 0) return set_error(SS_ERR_ARG, "nq < 0");
+  if (nq == 0) return SS_OK;
+  TopkArgs a{q, q_inv, nq, h->emb, h->inv, h->cap, h->dim, k, theta, h->head, h->gcap,
+             h->slot_offset};
+  int slices = 1;
+  if (int rc = topk_plan(h, a, algo, slices)) return rc;
+  size_t need = ws_offset + align_up((size_t)slices * nq * k * 8);
+  if (int rc = ws_reserve(h, need)) return rc;
+  uint64_t* partials = reinterpret_cast<uint64_t*>((char*)h->ws + ws_offset);
+  int rc = (algo == SS_ALGO_TCGEN05) ? launch_topk_tc(a, partials, slices, st)
+                                     : launch_topk_scan(a, partials, slices, st);
+  if (rc) return rc;
+  return launch_merge(partials, nullptr, slices, nq, k, out_comp, out_len, h->lens, h->head,
+                      h->gcap, h->slot_offset, st);
+}
+
+int ss_topk(ss_bank_t* h, const int8_t* q, const float* q_inv, int64_t nq, int32_t k, float theta,
+            int32_t algo, uint64_t* out_comp, int32_t* out_len, void* stream) {
+  if (!h || !out_comp || !out_len) return set_error(SS_ERR_ARG, "topk: null args");
+  return topk_impl(h, q, q_inv, nq, k, theta, algo, out_comp, out_len, 0, (cudaStream_t)stream);
+}
+
+int ss_topk_partials(ss_bank_t* h, const int8_t* q, const float* q_inv, int64_t nq, int32_t k,
+                     float theta, int32_t algo, uint64_t* partials, int32_t max_slices,
+                     int32_t* n_slices, void* stream) {
+  if (!h || !partials || !n_slices) return set_error(SS_ERR_ARG, "topk_partials: null args");
+  if (k < 1 || k > 256 || nq < 0) return set_error(SS_ERR_ARG, "topk_partials: bad k/nq");
+  TopkArgs a{q, q_inv, nq, h->emb, h->inv, h->cap, h->dim, k, theta, h->head, h->gcap,
+             h->slot_offset};
+  int slices = 1;
+  if (int rc = topk_plan(h, a, algo, slices)) return rc;
+  if (slices > max_slices) slices = max_slices;
+  if (slices < 1) return set_error(SS_ERR_ARG, "topk_partials: max_slices < 1");
+  *n_slices = slices;
+  if (nq == 0) return SS_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  return (algo == SS_ALGO_TCGEN05) ? launch_topk_tc(a, partials, slices, st)
+                                   : launch_topk_scan(a, partials, slices, st);
+}
+
+int ss_merge_topk(const uint64_t* comp, const int32_t* len, int32_t nlists, int64_t nq, int32_t k,
+                  uint64_t* out_comp, int32_t* out_len, void* stream) {
+  if (nlists < 1 || k < 1 || k > 256 || nq < 0 || !len)
+    return set_error(SS_ERR_ARG, "merge_topk: bad args");
+  return launch_merge(comp, len, nlists, nq, k, out_comp, out_len, nullptr, 0, 1, 0,
+                      (cudaStream_t)stream);
+}
+
+int ss_decode_topk(const uint64_t* comp, int64_t n, int64_t head, int64_t capacity, float* out_key,
+                   int64_t* out_seq, int64_t* out_slot, void* stream) {
+  if (n < 0 || capacity < 1) return set_error(SS_ERR_ARG, "decode: bad args");
+  return launch_decode(comp, n, head, capacity, out_key, out_seq, out_slot, (cudaStream_t)stream);
+}
+
+int ss_finish(const uint64_t* comp, const int32_t* len, int64_t nq, int32_t k,
+              int32_t min_matches, int32_t max_len, int32_t nbins, const int32_t* input_len,
+              const int64_t* fb_cnt, const int64_t* fb_sv, const int64_t* fb_sv2, int32_t P,
+              int32_t* npts, int32_t* pbin, int32_t* pcnt, int64_t* pD, int64_t* psv,
+              uint8_t* used_fb, double* G, void* stream) {
+  if (int rc = check_bins(max_len, nbins)) return rc;
+  if (P < nbins) return set_error(SS_ERR_ARG, "P (%d) must be >= nbins (%d)", P, nbins);
+  if (k < 1 || min_matches < 0 || nq < 0) return set_error(SS_ERR_ARG, "finish: bad args");
+  return launch_finish(comp, len, nq, k, min_matches, max_len, nbins, input_len, fb_cnt, fb_sv,
+                       fb_sv2, P, npts, pbin, pcnt, pD, psv, used_fb, G, (cudaStream_t)stream);
+}
+
+int ss_refresh(int64_t n, const int32_t* input_len, const int32_t* g_new, int32_t* bucket_io,
+               int32_t bucket_size, const int32_t* npts, const int32_t* pcnt, const int64_t* pD,
+               int32_t P, double* G_io, uint8_t* refreshed, int32_t force, void* stream) {
+  if (n < 0 || bucket_size < 1 || P < 1) return set_error(SS_ERR_ARG, "refresh: bad args");
+  return launch_refresh(n, input_len, g_new, bucket_io, bucket_size, npts, pcnt, pD, P, G_io,
+                        refreshed, force, (cudaStream_t)stream);
+}
+
+int64_t ss_rank_workspace_bytes(int64_t n) { return rank_workspace_bytes(n); }
+
+int ss_rank(const double* G, const int64_t* ids, int64_t n, int64_t* perm, void* workspace,
+            int64_t workspace_bytes, void* stream) {
+  if (n < 0) return set_error(SS_ERR_ARG, "rank: n < 0");
+  return launch_rank(G, ids, n, perm, workspace, workspace_bytes, (cudaStream_t)stream);
+}
+
+// ----------------------------------------------------------- fused round --
+// workspace layout: [topk partials ...][comp nq*k][len nq*k][fb 3*nbins][rank ws][host-round bufs]
+struct RoundLayout {
+  size_t comp, len, fb, rank, end;
+};
+static RoundLayout round_layout(int64_t nq, int k, int nbins) {
+  RoundLayout L;
+  size_t o = 0;
+  L.comp = o; o += align_up((size_t)nq * k * 8);
+  L.len = o; o += align_up((size_t)nq * k * 4);
+  L.fb = o; o += align_up((size_t)3 * nbins * 8);
+  L.rank = o; o += align_up((size_t)rank_workspace_bytes(nq));
+  L.end = o;
+  return L;
+}
+
+static int round_impl(ss_bank* h, const int8_t* q, const float* q_inv, const int32_t* input_len,
+                      const int64_t* ids, int64_t nq, int32_t k, float theta, int32_t min_matches,
+                      int32_t max_len, int32_t nbins, int32_t algo, int32_t P, int32_t* npts,
+                      int32_t* pbin, int32_t* pcnt, int64_t* pD, uint8_t* used_fb, double* G,
+                      int64_t* perm, size_t extra_front, cudaStream_t st) {
+  if (int rc = check_bins(max_len, nbins)) return rc;
+  if (P < nbins) return set_error(SS_ERR_ARG, "P (%d) must be >= nbins (%d)", P, nbins);
+  if (h->head <= 0) return set_error(SS_ERR_EMPTY, "cold start: the history window is empty");
+  if (nq == 0) return SS_OK;
+  RoundLayout L = round_layout(nq, k, nbins);
+  size_t base = extra_front;
+  if (int rc = ws_reserve(h, base + L.end + topk_ws_need(h, nq, k, algo))) return rc;
+  char* ws = (char*)h->ws + base;
+  uint64_t* comp = reinterpret_cast<uint64_t*>(ws + L.comp);
+  int32_t* len = reinterpret_cast<int32_t*>(ws + L.len);
+  int64_t* fb = reinterpret_cast<int64_t*>(ws + L.fb);
+  // the top-k partials live after the round buffers
+  int rc = topk_impl(h, q, q_inv, nq, k, theta, algo, comp, len, base + L.end, st);
+  if (rc) return rc;
+  rc = launch_fallback_hist(h->lens, h->seq, h->cap, max_len, nbins, fb, fb + nbins, fb + 2 * nbins, st);
+  if (rc) return rc;
+  rc = launch_finish(comp, len, nq, k, min_matches, max_len, nbins, input_len, fb, fb + nbins,
+                     fb + 2 * nbins, P, npts, pbin, pcnt, pD, nullptr, used_fb, G, st);
+  if (rc) return rc;
+  return launch_rank(G, ids, nq, perm, ws + L.rank, (int64_t)rank_workspace_bytes(nq), st);
+}
+
+int ss_schedule_round(ss_bank_t* h, const int8_t* q, const float* q_inv, const int32_t* input_len,
+                      const int64_t* ids, int64_t nq, int32_t k, float theta, int32_t min_matches,
+                      int32_t max_len, int32_t nbins, int32_t algo, int32_t P, int32_t* npts,
+                      int32_t* pbin, int32_t* pcnt, int64_t* pD, uint8_t* used_fb, double* G,
+                      int64_t* perm, void* stream) {
+  if (!h) return set_error(SS_ERR_ARG, "null bank");
+  return round_impl(h, q, q_inv, input_len, ids, nq, k, theta, min_matches, max_len, nbins, algo, P,
+                    npts, pbin, pcnt, pD, used_fb, G, perm, 0, (cudaStream_t)stream);
+}
+
+int ss_schedule_round_host(ss_bank_t* h, const int8_t* q_host, const float* q_inv_host,
+                           const int32_t* input_len_host, const int64_t* ids_host, int64_t nq,
+                           int32_t k, float theta, int32_t min_matches, int32_t max_len,
+                           int32_t nbins, int32_t algo, double* G_host, int64_t* perm_host,
+                           void* stream) {
+  if (!h || nq < 0) return set_error(SS_ERR_ARG, "round_host: bad args");
+  if (nq == 0) return SS_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int P = nbins;
+  // front region: device copies of the inputs and the per-request state
+  size_t o = 0;
+  size_t oq = o; o += align_up((size_t)nq * h->dim);
+  size_t oqi = o; o += align_up((size_t)nq * 4);
+  size_t oI = o; o += align_up((size_t)nq * 4);
+  size_t oid = o; o += align_up((size_t)nq * 8);
+  size_t onp = o; o += align_up((size_t)nq * 4);
+  size_t opb = o; o += align_up((size_t)nq * P * 4);
+  size_t opc = o; o += align_up((size_t)nq * P * 4);
+  size_t opD = o; o += align_up((size_t)nq * P * 8);
+  size_t ofb = o; o += align_up((size_t)nq);
+  size_t oG = o; o += align_up((size_t)nq * 8);
+  size_t operm = o; o += align_up((size_t)nq * 8);
+  RoundLayout L = round_layout(nq, k, nbins);
+  if (int rc = ws_reserve(h, o + L.end + topk_ws_need(h, nq, k, algo))) return rc;
+  char* w = (char*)h->ws;
+  SS_CUDA_TRY(cudaMemcpyAsync(w + oq, q_host, (size_t)nq * h->dim, cudaMemcpyHostToDevice, st));
+  SS_CUDA_TRY(cudaMemcpyAsync(w + oqi, q_inv_host, (size_t)nq * 4, cudaMemcpyHostToDevice, st));
+  SS_CUDA_TRY(cudaMemcpyAsync(w + oI, input_len_host, (size_t)nq * 4, cudaMemcpyHostToDevice, st));
+  if (ids_host)
+    SS_CUDA_TRY(cudaMemcpyAsync(w + oid, ids_host, (size_t)nq * 8, cudaMemcpyHostToDevice, st));
+  int rc = round_impl(h, (const int8_t*)(w + oq), (const float*)(w + oqi), (const int32_t*)(w + oI),
+                      ids_host ? (const int64_t*)(w + oid) : nullptr, nq, k, theta, min_matches,
+                      max_len, nbins, algo, P, (int32_t*)(w + onp), (int32_t*)(w + opb),
+                      (int32_t*)(w + opc), (int64_t*)(w + opD), (uint8_t*)(w + ofb),
+                      (double*)(w + oG), (int64_t*)(w + operm), o, st);
+  if (rc) return rc;
+  w = (char*)h->ws;
+  if (G_host) SS_CUDA_TRY(cudaMemcpyAsync(G_host, w + oG, (size_t)nq * 8, cudaMemcpyDeviceToHost, st));
+  if (perm_host)
+    SS_CUDA_TRY(cudaMemcpyAsync(perm_host, w + operm, (size_t)nq * 8, cudaMemcpyDeviceToHost, st));
+  SS_CUDA_TRY(cudaStreamSynchronize(st));
+  return SS_OK;
+}
+
+}  // extern "C"

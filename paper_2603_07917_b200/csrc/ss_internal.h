@@ -1,0 +1,75 @@
+// Internal (non-ABI) declarations shared between the kernel files and the
+// C-ABI layer in ss_api.cu.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace ss {
+
+void count_launch();
+int set_error(int code, const char* fmt, ...);
+int sm_count(int device);
+
+int launch_match_pmfs(const float* sims, int64_t nq, int64_t nw, const int64_t* lens,
+                      float theta, int64_t max_len, double* sup, double* mas,
+                      int64_t* sizes, int64_t out_stride, int* err, cudaStream_t st);
+int launch_gittins_dist(const double* support, const double* masses, const int64_t* npts,
+                        const double* attained, const double* outlived, int64_t n,
+                        int64_t stride, double* out, int* err, int ref_mode, cudaStream_t st);
+int launch_embed(const int64_t* tokens, const int64_t* offsets, int64_t n, uint64_t salt,
+                 int dim, double* out_f64, int8_t* out_i8, float* out_inv, int* err,
+                 cudaStream_t st);
+int launch_cost_dist(int kind, double w_in, double w_out, const double* I, const double* ls,
+                     const int64_t* npts, int64_t n, int64_t stride, double* out,
+                     cudaStream_t st);
+
+// bank maintenance (k_bank.cu)
+int launch_bank_write(int8_t* emb, float* inv, int32_t* lens, int64_t* seq, int dim,
+                      const int8_t* src_emb, const float* src_inv, const int32_t* src_lens,
+                      const int64_t* src_seq, const int64_t* src_slot, int64_t n,
+                      int64_t first_seq, int64_t capacity, int64_t skip, int* err,
+                      cudaStream_t st);
+int launch_fallback_hist(const int32_t* lens, const int64_t* seq, int64_t capacity,
+                         int max_len, int nbins, int64_t* cnt, int64_t* sv, int64_t* sv2,
+                         cudaStream_t st);
+
+// similarity + top-k
+struct TopkArgs {
+  const int8_t* q;
+  const float* q_inv;
+  int64_t nq;
+  const int8_t* emb;
+  const float* inv;
+  int64_t n_rows;        // local slots scanned [0, n_rows)
+  int dim;
+  int k;
+  float theta;
+  int64_t head, gcap, slot_offset;  // rel = (slot_offset + j - head) mod gcap
+};
+int launch_topk_scan(const TopkArgs& a, uint64_t* partials, int n_slices, cudaStream_t st);
+int topk_scan_slices(const TopkArgs& a, int device);
+int launch_topk_tc(const TopkArgs& a, uint64_t* partials, int n_slices, cudaStream_t st);
+int topk_tc_slices(const TopkArgs& a, int device);
+bool topk_tc_supported(const TopkArgs& a);
+
+int launch_merge(const uint64_t* comp, const int32_t* len, int nlists, int64_t nq, int k,
+                 uint64_t* out_comp, int32_t* out_len, const int32_t* bank_lens,
+                 int64_t head, int64_t gcap, int64_t slot_offset, cudaStream_t st);
+int launch_decode(const uint64_t* comp, int64_t n, int64_t head, int64_t capacity,
+                  float* key, int64_t* seq, int64_t* slot, cudaStream_t st);
+int launch_finish(const uint64_t* comp, const int32_t* len, int64_t nq, int k,
+                  int min_matches, int max_len, int nbins, const int32_t* I,
+                  const int64_t* fb_cnt, const int64_t* fb_sv, const int64_t* fb_sv2, int P,
+                  int32_t* npts, int32_t* pbin, int32_t* pcnt, int64_t* pD, int64_t* psv,
+                  uint8_t* used_fb, double* G, cudaStream_t st);
+int launch_refresh(int64_t n, const int32_t* I, const int32_t* g_new, int32_t* bucket_io,
+                   int bucket_size, const int32_t* npts, const int32_t* pcnt,
+                   const int64_t* pD, int P, double* G_io, uint8_t* refreshed, int force,
+                   cudaStream_t st);
+
+// rank
+int64_t rank_workspace_bytes(int64_t n);
+int launch_rank(const double* G, const int64_t* ids, int64_t n, int64_t* perm,
+                void* ws, int64_t ws_bytes, cudaStream_t st);
+
+}  // namespace ss

@@ -1,0 +1,333 @@
+"""GPU parity: every kernel on the hot path against the CPU oracle (which is
+itself pinned to the reference by tests/test_oracle_golden.py) and against
+the reference's golden vectors.  Bars (north star): neighbour sets, counts
+and orderings bit-exact; Gittins/cost bit-exact here (the integer form is
+deterministic), general-law Gittins within 1e-12 relative."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import sagesched_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _t(x, dtype=None):
+    t = torch.as_tensor(np.ascontiguousarray(x), device="cuda")
+    return t.to(dtype) if dtype is not None else t
+
+
+# ------------------------------------------------------- reference compat --
+def test_match_pmfs_bit_exact_vs_reference(cuda, golden):
+    from paper_2603_07917_b200 import _kernels as K
+    g = golden
+    nq = g["mp_sims"].shape[0]
+    sup = np.zeros_like(g["mp_sup"])
+    mas = np.zeros_like(g["mp_mas"])
+    sizes = np.zeros(nq, np.int64)
+    K.match_pmfs(g["mp_sims"], g["mp_lens"], g["mp_theta"], int(g["mp_max_len"]), sup, mas, sizes)
+    assert np.array_equal(sizes, g["mp_sizes"])
+    for q in range(nq):
+        k = sizes[q]
+        assert np.array_equal(sup[q, :k], g["mp_sup"][q, :k])
+        assert np.array_equal(mas[q, :k], g["mp_mas"][q, :k])
+
+
+def test_match_pmfs_out_of_range_len_raises(cuda):
+    from paper_2603_07917_b200 import _kernels as K
+    sims = np.ones((1, 3), np.float32)
+    with pytest.raises(ValueError):
+        K.match_pmfs(sims, np.array([1, 2, 99]), np.float32(0.5), 8, np.zeros((1, 9)),
+                     np.zeros((1, 9)), np.zeros(1, np.int64))
+
+
+def test_gittins_min_vs_reference(cuda, golden):
+    from paper_2603_07917_b200 import _kernels as K
+    g = golden
+    out = K.gittins_min_batch(_t(g["gm_support"]), _t(g["gm_masses"]), _t(g["gm_npts"]))
+    got = out.cpu().numpy()
+    np.testing.assert_allclose(got, g["gm_value"], rtol=1e-12, atol=0)
+    assert K.gittins_min(np.array([1.0, 9.0]), np.array([0.5, 0.5])) == 2.0
+    for c in (1.0, 5.0, 1000.0):
+        assert K.gittins_min(np.array([c]), np.array([1.0])) == c
+    with pytest.raises(ZeroDivisionError):
+        K.gittins_min(np.array([1.0, 2.0]), np.array([0.0, 1.0]))
+    assert K.gittins_min(np.zeros(0), np.zeros(0)) == np.inf
+
+
+def test_embed_vs_reference(cuda, golden):
+    from paper_2603_07917_b200 import _kernels as K
+    g = golden
+    t, offs = _t(g["em_tokens"]), _t(g["em_offsets"])
+    for d in (384, 256, 17):
+        got = K.embed_accumulate_batch(t, offs, int(g["em_salt"]), d).cpu().numpy()
+        assert np.array_equal(got, g[f"em_{d}"])
+    assert np.array_equal(K.embed_accumulate(g["em_tokens"][:5], int(g["em_salt"]), 384),
+                          O.embed_accumulate(g["em_tokens"][:5], int(g["em_salt"]), 384))
+
+
+def test_embed_quantize_and_push(cuda):
+    from paper_2603_07917_b200.history import embed_batch, DEFAULT_SALT
+    rng = np.random.default_rng(3)
+    prompts = [rng.integers(0, 50000, int(rng.integers(1, 200))) for _ in range(50)] + [[]]
+    e, inv = embed_batch(prompts, DEFAULT_SALT, 384)
+    ref = np.stack([O.embed_accumulate(p, DEFAULT_SALT, 384) for p in prompts]).astype(np.int8)
+    assert np.array_equal(e.cpu().numpy(), ref)
+    ri = O.inv_norm(ref)
+    gi = inv.cpu().numpy()
+    assert np.array_equal(np.isnan(gi), np.isnan(ri))
+    assert np.array_equal(gi[~np.isnan(ri)], ri[~np.isnan(ri)])
+
+
+def test_cost_distribution_vs_reference(cuda, golden):
+    from paper_2603_07917_b200.cost import ResourceBound, cost_distribution
+    from paper_2603_07917_b200.distribution import DiscreteDistribution
+    g = golden
+    for i in range(g["cd_n"].size):
+        k = int(g["cd_n"][i])
+        d = DiscreteDistribution(g["cd_sup"][i, :k], g["cd_mas"][i, :k])
+        out = cost_distribution(ResourceBound(), g["cd_I"][i], d)
+        assert np.array_equal(out.support, g["cd_out"][i, :k])
+    # SPEC.md:281
+    out = cost_distribution(ResourceBound(), 100, DiscreteDistribution([100, 300], [.5, .5]))
+    assert list(out.support) == [15000.0, 75000.0]
+
+
+def test_gittins_conditioning_spec_examples(cuda):
+    from paper_2603_07917_b200.distribution import DiscreteDistribution as DD
+    from paper_2603_07917_b200.gittins import condition_on_attained, gittins_index
+    d = DD([1.0, 9.0], [0.5, 0.5])
+    assert gittins_index(d) == 2.0
+    c = condition_on_attained(d, 1.0)
+    assert list(c.support) == [8.0] and gittins_index(c) == 8.0
+    c = condition_on_attained(DD([2.0, 4.0, 8.0], [0.25, 0.25, 0.5]), 3.0)
+    np.testing.assert_allclose(c.support, [1.0, 5.0])
+    np.testing.assert_allclose(c.masses, [1 / 3, 2 / 3])
+
+
+# -------------------------------------------------------------- the bank ---
+def test_ring_push_evicts_oldest(cuda):
+    from paper_2603_07917_b200.history import HistoryWindow
+    rng = np.random.default_rng(0)
+    cap, dim = 100, 128
+    w = HistoryWindow(cap, dim)
+    e = rng.integers(-127, 128, (250, dim)).astype(np.int8)
+    L = rng.integers(1, 2049, 250).astype(np.int32)
+    w.push(e[:30], L[:30])
+    w.push(e[30:], L[30:])  # wraps twice
+    assert w.head == 250 and len(w) == cap
+    emb, inv, lens, seq = w.tensors()
+    seq = seq.cpu().numpy()
+    for slot in range(cap):
+        s = 200 + ((slot - 200) % cap)  # the newest seq congruent to slot
+        assert seq[slot] == s
+        assert np.array_equal(emb[slot].cpu().numpy(), e[s])
+        assert lens[slot].item() == L[s]
+    assert np.array_equal(inv.cpu().numpy(), O.inv_norm(e[seq]))
+    with pytest.raises(ValueError):
+        w.push(e[:1], np.array([0], np.int32))  # length < 1 rejected
+
+
+# ------------------------------------------------------- top-k (stage 1) ---
+def _bank(n, dim, ncl, seed, nq, cap=None):
+    from paper_2603_07917_b200.history import HistoryWindow
+    emb, lens, cl, _ = O.make_bank(n + nq, dim, ncl, seed)
+    w = HistoryWindow(cap or n, dim)
+    w.push(emb[:n], lens[:n])
+    q = emb[n:]
+    return w, emb[:n], lens[:n], q, O.inv_norm(q)
+
+
+def _oracle_topk(w, bank_e, q, q_inv, k, theta):
+    head, cap = w.head, w.global_capacity
+    n = bank_e.shape[0]
+    seq = np.arange(n, dtype=np.int64) + max(0, head - n)
+    keys = O.scores(q, q_inv, bank_e, O.inv_norm(bank_e))
+    return keys, seq, [O.select_topk(keys[i], seq, k, theta) for i in range(q.shape[0])]
+
+
+def _check_topk(w, comp, keys, seq, ref, k):
+    key, gseq, _ = w.decode(comp)
+    key, gseq = key.cpu().numpy(), gseq.cpu().numpy()
+    for i, sel in enumerate(ref):
+        m = sel.size
+        assert np.array_equal(gseq[i, :m], seq[sel]), i
+        assert np.array_equal(key[i, :m], keys[i, sel]), i
+        assert np.all(gseq[i, m:] == -1)
+
+
+@pytest.mark.parametrize("algo", ["scan", "tcgen05"])
+@pytest.mark.parametrize("theta,k", [(0.8, 32), (-1.0, 32), (0.5, 64), (-1.0, 256)])
+def test_topk_c1_bit_exact(cuda, algo, theta, k):
+    from paper_2603_07917_b200 import _lib
+    w, be, bl, q, qi = _bank(10_000, 384, 100, 7, 64)
+    keys, seq, ref = _oracle_topk(w, be, q, qi, k, theta)
+    try:
+        comp, ln = w.topk(q, qi, k, theta, algo)
+    except NotImplementedError:
+        pytest.skip(f"{algo} not available")
+    _check_topk(w, comp, keys, seq, ref, k)
+    lens = ln.cpu().numpy()
+    for i, sel in enumerate(ref):
+        assert np.array_equal(lens[i, :sel.size], bl[sel])
+
+
+@pytest.mark.parametrize("algo", ["scan", "tcgen05"])
+def test_topk_edges(cuda, algo):
+    """ragged nq, partially filled ring, ties, degenerate query, k > rows."""
+    from paper_2603_07917_b200.history import HistoryWindow
+    rng = np.random.default_rng(11)
+    dim = 384
+    base = rng.integers(-20, 21, (300, dim)).astype(np.int8)
+    base[100:110] = base[5]  # exact duplicates -> score ties broken by larger seq
+    L = rng.integers(1, 2049, 300).astype(np.int32)
+    w = HistoryWindow(1000, dim)  # 700 empty slots
+    w.push(base, L)
+    for nq in (1, 3, 129):
+        q = rng.integers(-20, 21, (nq, dim)).astype(np.int8)
+        q[0] = base[5]
+        if nq > 1:
+            q[1] = 0  # degenerate (zero) query: no neighbours
+        qi = O.inv_norm(q)
+        for k, theta in ((16, -1.0), (256, -1.0), (8, 0.9)):
+            try:
+                comp, _ = w.topk(q, qi, k, theta, algo)
+            except NotImplementedError:
+                pytest.skip(f"{algo} not available")
+            keys = O.scores(q, qi, base, O.inv_norm(base))
+            seq = np.arange(300)
+            ref = [O.select_topk(keys[i], seq, k, theta) for i in range(nq)]
+            _check_topk(w, comp, keys, seq, ref, k)
+            if nq > 1:
+                assert int((comp[1] != 0).sum()) == 0
+
+
+# ------------------------------------------------- full round (stages 1-4) --
+@pytest.mark.parametrize("algo", ["scan", "tcgen05"])
+@pytest.mark.parametrize("nbins,theta", [(64, 0.8), (2048, 0.8), (128, -1.0)])
+def test_round_c1_bit_exact(cuda, algo, nbins, theta):
+    from paper_2603_07917_b200.scheduler import RoundConfig, SageScheduler
+    w, be, bl, q, qi = _bank(10_000, 384, 100, 7, 64)
+    rng = np.random.default_rng(2)
+    I = rng.integers(1, 4097, 64).astype(np.int32)
+    ids = np.arange(64, dtype=np.int64)
+    k = 32
+    cfg = RoundConfig(k=k, theta=theta, min_matches=20, max_len=2048, nbins=nbins, algo=algo)
+    s = SageScheduler(w, cfg)
+    try:
+        perm, G, out = s.schedule_round(_t(q), _t(qi), _t(I), _t(ids))
+    except NotImplementedError:
+        pytest.skip(f"{algo} not available")
+    keys, seq, _ = _oracle_topk(w, be, q, qi, k, theta)
+    ref = O.predict_round(keys, seq, bl, I, k, theta, 20, 2048, nbins, window_lens=bl)
+    Gr = np.array([r["G"] for r in ref])
+    assert np.array_equal(G.cpu().numpy(), Gr)
+    assert np.array_equal(perm.cpu().numpy(), O.rank(Gr, ids))
+    npts = out["npts"].cpu().numpy()
+    for i, r in enumerate(ref):
+        assert npts[i] == r["c"].size
+        assert np.array_equal(out["pcnt"][i, :npts[i]].cpu().numpy(), r["c"])
+        assert np.array_equal(out["pD"][i, :npts[i]].cpu().numpy(), r["D"])
+        assert np.array_equal(out["pbin"][i, :npts[i]].cpu().numpy(), r["bins"])
+        assert bool(out["used_fb"][i].item()) == r["used_fallback"]
+    # host (plugin) entry point gives the same answer
+    ph, Gh = s.schedule_round_host(q, qi, I, ids)
+    assert np.array_equal(Gh, Gr) and np.array_equal(ph, O.rank(Gr, ids))
+
+
+def test_round_fallback_and_cold_start(cuda):
+    from paper_2603_07917_b200 import _lib
+    from paper_2603_07917_b200.history import HistoryWindow
+    from paper_2603_07917_b200.scheduler import RoundConfig, SageScheduler
+    w = HistoryWindow(64, 128)
+    s = SageScheduler(w, RoundConfig(k=8, theta=0.99, nbins=64))
+    q = np.ones((2, 128), np.int8)
+    with pytest.raises(_lib.ColdStartError):
+        s.predict(q, O.inv_norm(q), np.array([5, 6]))
+    rng = np.random.default_rng(1)
+    e = rng.integers(-5, 6, (40, 128)).astype(np.int8)
+    L = rng.integers(1, 2049, 40).astype(np.int32)
+    w.push(e, L)
+    st = s.predict(q, O.inv_norm(q), np.array([5, 6]))
+    assert st.used_fb.cpu().tolist() == [1, 1]  # nothing is >= 0.99 similar
+    bins, c, D = O.hist_to_points(*O.bin_hist(L, 2048, 64), 5)
+    assert np.array_equal(st.pcnt[0, :c.size].cpu().numpy(), c)
+    assert st.G[0].item() == O.gittins_points(c, D)
+
+
+def test_predict_dropin_limit_equals_reference_match(cuda):
+    """predict() with k >= #matches and width-1 bins returns exactly the
+    reference's threshold-match pmf (match_pmfs)."""
+    from paper_2603_07917_b200.predictor import Request, SemanticHistory, predict
+    w, be, bl, q, qi = _bank(2000, 128, 10, 3, 4)
+    keys = O.scores(q, qi, be, O.inv_norm(be))
+    for i in range(4):
+        hits = np.flatnonzero(keys[i] >= np.float32(0.8))
+        if hits.size > 256 or hits.size < 1:
+            continue
+        req = Request(id=i, prompt_tokens=np.arange(3), input_len=10)
+        req.embedding, req.inv_norm = _t(q[i]), _t(qi[i:i + 1])[0]
+        d = predict(SemanticHistory(theta=0.8, min_matches=1, k=256), req, w)
+        sup = np.zeros((1, 2049))
+        mas = np.zeros((1, 2049))
+        sz = np.zeros(1, np.int64)
+        O.match_pmfs(keys[i:i + 1], bl.astype(np.int64), np.float32(0.8), 2048, sup, mas, sz)
+        assert np.array_equal(d.support, sup[0, :sz[0]])
+        np.testing.assert_allclose(d.masses, mas[0, :sz[0]], rtol=1e-15, atol=0)
+
+
+# ------------------------------------------------- refresh + rank (c3) -----
+def _c3_laws(n, nbins, seed, P=None):
+    rng = np.random.default_rng(seed)
+    P = P or nbins
+    I = rng.integers(1, 4097, n).astype(np.int32)
+    npts = np.zeros(n, np.int32)
+    pc = np.zeros((n, P), np.int32)
+    pD = np.zeros((n, P), np.int64)
+    for i in range(n):
+        lens = rng.integers(1, 2049, 64) if i % 3 else np.clip(
+            np.rint(np.exp(rng.normal(5, 0.7, 64))), 1, 2048).astype(np.int64)
+        _, c, D = O.hist_to_points(*O.bin_hist(lens, 2048, nbins), I[i])
+        npts[i] = c.size
+        pc[i, :c.size] = c
+        pD[i, :c.size] = D
+    g = np.where(rng.random(n) < 0.4, rng.integers(0, 2049, n), 0).astype(np.int32)
+    return I, npts, pc, pD, g
+
+
+def test_refresh_bit_exact(cuda):
+    from paper_2603_07917_b200 import _lib
+    n, nbins = 3000, 512
+    I, npts, pc, pD, g = _c3_laws(n, nbins, 4)
+    bucket = np.zeros(n, np.int32)
+    G = np.full(n, -1.0)
+    dI, dg, db, dn, dpc, dpD, dG = map(_t, (I, g, bucket, npts, pc, pD, G))
+    ref_flag = torch.zeros(n, dtype=torch.uint8, device="cuda")
+    _lib.call("ss_refresh", n, dI.data_ptr(), dg.data_ptr(), db.data_ptr(), 200, dn.data_ptr(),
+              dpc.data_ptr(), dpD.data_ptr(), nbins, dG.data_ptr(), ref_flag.data_ptr(), 1,
+              _lib.stream_ptr())
+    got = dG.cpu().numpy()
+    for i in range(n):
+        k = npts[i]
+        ref = O.gittins_points(pc[i, :k], pD[i, :k], int(I[i]), int(g[i]))
+        assert got[i] == ref, (i, got[i], ref)
+    assert np.array_equal(db.cpu().numpy(), g // 200)
+    # not due -> untouched
+    dG.fill_(-1.0)
+    _lib.call("ss_refresh", n, dI.data_ptr(), dg.data_ptr(), db.data_ptr(), 200, dn.data_ptr(),
+              dpc.data_ptr(), dpD.data_ptr(), nbins, dG.data_ptr(), ref_flag.data_ptr(), 0,
+              _lib.stream_ptr())
+    assert (dG == -1.0).all() and int(ref_flag.sum()) == 0
+
+
+@pytest.mark.parametrize("n", [1, 7, 1024, 4096, 4097, 200_000])
+def test_rank_bit_exact(cuda, n):
+    from paper_2603_07917_b200.scheduler import rank
+    rng = np.random.default_rng(n)
+    G = rng.choice(rng.uniform(1, 1e7, max(2, n // 3)), n)  # many exact ties
+    ids = rng.permutation(n).astype(np.int64)
+    perm = rank(_t(G), _t(ids)).cpu().numpy()
+    assert np.array_equal(perm, O.rank(G, ids))
+    perm = rank(_t(G)).cpu().numpy()
+    assert np.array_equal(perm, O.rank(G, np.arange(n)))
