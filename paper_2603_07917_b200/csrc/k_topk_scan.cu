@@ -16,7 +16,6 @@
 
 namespace ss {
 
-constexpr int SCAN_THREADS = 128;
 constexpr int SCAN_ROWS = 32;
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
@@ -28,7 +27,7 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-template <int D>
+template <int D, int SCAN_THREADS>
 __global__ void __launch_bounds__(SCAN_THREADS, 2)
 k_topk_scan(const int8_t* __restrict__ Q, const float* __restrict__ q_inv, int64_t nq,
             const int8_t* __restrict__ emb, const float* __restrict__ inv, int64_t n_rows,
@@ -123,23 +122,32 @@ k_topk_scan(const int8_t* __restrict__ Q, const float* __restrict__ q_inv, int64
   }
 }
 
-template <int D>
-static int launch_scan_d(const TopkArgs& a, uint64_t* partials, int n_slices, cudaStream_t st) {
+template <int D, int SCAN_THREADS>
+static int launch_scan_dt(const TopkArgs& a, uint64_t* partials, int n_slices, cudaStream_t st) {
   size_t smem = (size_t)2 * SCAN_ROWS * D + 2 * SCAN_ROWS * 4 + (size_t)a.k * SCAN_THREADS * 8;
   if (smem > 227 * 1024) return set_error(SS_ERR_UNSUPPORTED, "k=%d too large for scan", a.k);
-  SS_CUDA_TRY(cudaFuncSetAttribute(k_topk_scan<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  SS_CUDA_TRY(cudaFuncSetAttribute(k_topk_scan<D, SCAN_THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int64_t rows_per_slice = (a.n_rows + n_slices - 1) / n_slices;
   rows_per_slice = (rows_per_slice + SCAN_ROWS - 1) / SCAN_ROWS * SCAN_ROWS;
   dim3 grid((unsigned)n_slices, (unsigned)((a.nq + SCAN_THREADS - 1) / SCAN_THREADS));
   count_launch();
-  k_topk_scan<D><<<grid, SCAN_THREADS, smem, st>>>(a.q, a.q_inv, a.nq, a.emb, a.inv, a.n_rows, a.k,
+  k_topk_scan<D, SCAN_THREADS><<<grid, SCAN_THREADS, smem, st>>>(a.q, a.q_inv, a.nq, a.emb, a.inv, a.n_rows, a.k,
                                                    a.theta, a.head, a.gcap, a.slot_offset,
                                                    rows_per_slice, partials);
   SS_LAUNCH_CHECK();
   return SS_OK;
 }
 
+template <int D>
+static int launch_scan_d(const TopkArgs& a, uint64_t* partials, int n_slices, cudaStream_t st) {
+  return a.k <= 128 ? launch_scan_dt<D, 128>(a, partials, n_slices, st)
+                    : launch_scan_dt<D, 64>(a, partials, n_slices, st);
+}
+
+static inline int scan_threads(int k) { return k <= 128 ? 128 : 64; }
+
 int topk_scan_slices(const TopkArgs& a, int device) {
+  const int SCAN_THREADS = scan_threads(a.k);
   int sms = sm_count(device);
   int64_t qtiles = (a.nq + SCAN_THREADS - 1) / SCAN_THREADS;
   int64_t want = (2 * sms + qtiles - 1) / qtiles;  // ~2 CTAs per SM

@@ -120,7 +120,7 @@ def test_ring_push_evicts_oldest(cuda):
     emb, inv, lens, seq = w.tensors()
     seq = seq.cpu().numpy()
     for slot in range(cap):
-        s = 200 + ((slot - 200) % cap)  # the newest seq congruent to slot
+        s = 150 + ((slot - 150) % cap)  # the newest seq congruent to slot
         assert seq[slot] == s
         assert np.array_equal(emb[slot].cpu().numpy(), e[s])
         assert lens[slot].item() == L[s]
@@ -171,6 +171,35 @@ def test_topk_c1_bit_exact(cuda, algo, theta, k):
     lens = ln.cpu().numpy()
     for i, sel in enumerate(ref):
         assert np.array_equal(lens[i, :sel.size], bl[sel])
+
+
+@pytest.mark.parametrize("algo", ["scan", "tcgen05"])
+@pytest.mark.parametrize("theta", [-1.0, 0.8])
+def test_topk_multi_tile_ring_wrap(cuda, algo, theta):
+    """200k-row bank pushed through a wrapping ring (head > capacity), ragged
+    nq=300: many 256-row tiles per CTA, stage-ring and TMEM double-buffer wrap."""
+    from paper_2603_07917_b200.history import HistoryWindow
+    n, cap, dim, nq, k = 260_000, 200_000, 384, 300, 64
+    emb, lens, _, _ = O.make_bank(n + nq, dim, 500, 21)
+    w = HistoryWindow(cap, dim)
+    w.push(emb[:n], lens[:n])  # wraps: slots hold seqs 60000..259999
+    q = emb[n:]
+    qi = O.inv_norm(q)
+    seqs = np.arange(n - cap, n)
+    bank_e = emb[n - cap:n]
+    keys = O.scores(q, qi, bank_e, O.inv_norm(bank_e))
+    ref = [O.select_topk(keys[i], seqs, k, theta) for i in range(nq)]
+    try:
+        comp, ln = w.topk(q, qi, k, theta, algo)
+    except NotImplementedError:
+        pytest.skip(f"{algo} not available")
+    key, gseq, _ = w.decode(comp)
+    key, gseq, ln = key.cpu().numpy(), gseq.cpu().numpy(), ln.cpu().numpy()
+    for i, sel in enumerate(ref):
+        m = sel.size
+        assert np.array_equal(gseq[i, :m], seqs[sel]), i
+        assert np.array_equal(key[i, :m], keys[i, sel]), i
+        assert np.array_equal(ln[i, :m], lens[seqs[sel]]), i
 
 
 @pytest.mark.parametrize("algo", ["scan", "tcgen05"])
