@@ -132,7 +132,7 @@ static int launch_scan_dt(const TopkArgs& a, uint64_t* partials, int n_slices, c
   dim3 grid((unsigned)n_slices, (unsigned)((a.nq + SCAN_THREADS - 1) / SCAN_THREADS));
   count_launch();
   k_topk_scan<D, SCAN_THREADS><<<grid, SCAN_THREADS, smem, st>>>(a.q, a.q_inv, a.nq, a.emb, a.inv, a.n_rows, a.k,
-                                                   a.theta, a.head, a.gcap, a.slot_offset,
+                                                   a.theta, a.head % a.gcap, a.gcap, a.slot_offset,
                                                    rows_per_slice, partials);
   SS_LAUNCH_CHECK();
   return SS_OK;

@@ -7,17 +7,24 @@
 // scores exactly as DESIGN.md section 3 (int8 dot products are exact in
 // int32, so the tensor-core result is bit-identical to the CPU oracle).
 //
-// CTA = 128 queries (M, = TMEM lanes) x one slice of the bank streamed in
-// 256-row tiles (N).  6 warps:
+// A CTA owns 128 queries (M = TMEM lanes) and streams one slice of the bank
+// in 256-row tiles (N).  Two variants:
+//   CG = 1  one CTA per MMA (M=128, N=256); each CTA loads whole B tiles.
+//   CG = 2  a CTA pair (cluster of 2, tcgen05 cta_group::2, M=256, N=256):
+//           each CTA loads half of every B tile, the leader issues the MMA
+//           for both, halving the L2->SM traffic of the bank stream.
+// 6 warps per CTA:
 //   warp 0      TMA producer: A (queries, once) and B (bank K-blocks, ring)
-//   warp 1      TMEM allocator + single-thread MMA issuer
+//   warp 1      TMEM allocator + single-thread MMA issuer (leader CTA)
 //   warps 2..5  epilogue: tcgen05.ld 32 columns at a time, s = dot*inv_w,
-//               one compare against the per-query heap threshold, rare
-//               exact insert into the per-query shared-memory min-heap
+//               one max-tree compare per 32 columns against the per-query
+//               heap threshold; rare exact inserts into the per-query
+//               shared-memory min-heap
 // Two TMEM accumulator buffers (2 x 256 columns) let the MMA of tile t+1
 // overlap the epilogue of tile t.
 #include <cuda.h>
 #include <cudaTypedefs.h>
+#include <stdlib.h>
 
 #include "ss_common.cuh"
 #include "ss_internal.h"
@@ -34,11 +41,20 @@ constexpr int THREADS = 192;
 constexpr int EPI_WARP0 = 2;
 constexpr int KMAX = 64;         // heap capacity (k <= 64 on this path)
 constexpr int A_BLK = BM * BK;   // 16 KB per K-block of A
-constexpr int B_STAGE = BN * BK; // 32 KB per K-block of B
+constexpr uint32_t PEER_MASK = 0xFEFFFFFFu;  // shared::cluster address -> pair leader
 }  // namespace tc
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::
+                   : "memory");
 }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
@@ -51,6 +67,12 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
+// arrive on the same barrier in the pair leader's shared memory
+__device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(
+                   smem_u32(bar) & tc::PEER_MASK)
+               : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n"
@@ -62,13 +84,38 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+template <int CG>
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar,
                                             int c0, int c1) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4}], [%2];\n" ::"r"(smem_u32(dst)),
-      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
-      : "memory");
+  if constexpr (CG == 1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];\n" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+  } else {  // completion is signalled on the pair leader's barrier
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];\n" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(smem_u32(bar) & tc::PEER_MASK), "r"(c0), "r"(c1)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void tma_prefetch_l2_2d(const CUtensorMap* map, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];\n" ::"l"(map),
+               "r"(c0), "r"(c1)
+               : "memory");
 }
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -76,21 +123,58 @@ __device__ __forceinline__ void tc_fence_before() {
 __device__ __forceinline__ void tc_fence_after() {
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
 }
+template <int CG>
 __device__ __forceinline__ void tc_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
-                   smem_u32(bar))
-               : "memory");
+  if constexpr (CG == 1) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                     smem_u32(bar))
+                 : "memory");
+  } else {  // arrive on this barrier in both CTAs of the pair
+    asm volatile(
+        "{\n"
+        ".reg .b16 m;\n"
+        "mov.b16 m, 3;\n"
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+        " [%0], m;\n"
+        "}\n" ::"r"(smem_u32(bar))
+        : "memory");
+  }
 }
+template <int CG>
 __device__ __forceinline__ void tc_mma_i8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
                                           uint32_t idesc, uint32_t accum) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "setp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n"
-      "}\n" ::"r"(d_tmem),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
-      : "memory");
+  if constexpr (CG == 1) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
+        : "memory");
+  }
+}
+template <int CG>
+__device__ __forceinline__ void tmem_alloc512(uint32_t* dst) {
+  if constexpr (CG == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
+        smem_u32(dst)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  } else {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
+        smem_u32(dst)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
+  }
+}
+template <int CG>
+__device__ __forceinline__ void tmem_dealloc512(uint32_t taddr) {
+  if constexpr (CG == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(taddr));
+  else
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;\n" ::"r"(taddr));
 }
 // 32 lanes x 32 consecutive 32-bit columns -> 32 registers per thread
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, int (&v)[32]) {
@@ -107,6 +191,32 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, int (&v)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 }
 
+// Asynchronous variant: the registers are only valid after tmem_wait_regs(v),
+// which names them as in/out operands so no consumer can be hoisted above it.
+__device__ __forceinline__ void tmem_ld32_async(uint32_t taddr, int (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+      "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];\n"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+        "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+        "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_regs(int (&v)[32]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n"
+               : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]),
+                 "+r"(v[6]), "+r"(v[7]), "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]),
+                 "+r"(v[12]), "+r"(v[13]), "+r"(v[14]), "+r"(v[15]), "+r"(v[16]), "+r"(v[17]),
+                 "+r"(v[18]), "+r"(v[19]), "+r"(v[20]), "+r"(v[21]), "+r"(v[22]), "+r"(v[23]),
+                 "+r"(v[24]), "+r"(v[25]), "+r"(v[26]), "+r"(v[27]), "+r"(v[28]), "+r"(v[29]),
+                 "+r"(v[30]), "+r"(v[31])
+               :
+               : "memory");
+}
+
 // UMMA shared-memory descriptor, K-major, 128B swizzle: rows of 128 B, 8-row
 // atoms 1024 B apart (SBO), LBO unused for swizzled K-major, version 1.
 __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
@@ -119,29 +229,40 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
   return d;
 }
 
-// instruction descriptor: D=S32, A=B=signed int8, K-major both, N=256, M=128
-constexpr uint32_t IDESC_I8 = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(tc::BN >> 3) << 17) |
-                              ((uint32_t)(tc::BM >> 4) << 24);
-
-__device__ __noinline__ void tc_consider(uint64_t* heap, int k, HeapState* st, int dot, float iw,
-                                         float iq, float theta, int64_t gslot, int64_t head,
-                                         int64_t gcap) {
-  heap_consider<tc::BM>(heap, k, *st, dot, iw, iq, theta, gslot, head, gcap);
+// instruction descriptor: D=S32, A=B=signed int8, K-major both, N=256, M=128*CG
+template <int CG>
+__device__ __forceinline__ constexpr uint32_t idesc_i8() {
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(tc::BN >> 3) << 17) |
+         ((uint32_t)((tc::BM * CG) >> 4) << 24);
 }
 
+// out-of-line heap maintenance for the epilogue (rare): returns the new root
+__device__ __noinline__ uint64_t tc_heapify(uint64_t* heap, int k) {
+  for (int i = k / 2 - 1; i >= 0; --i) heap_sift_down<tc::BM>(heap, k, i, heap[i * tc::BM]);
+  return heap[0];
+}
+__device__ __noinline__ uint64_t tc_heap_replace(uint64_t* heap, int k, uint64_t x) {
+  heap_sift_down<tc::BM>(heap, k, 0, x);
+  return heap[0];
+}
+
+template <int CG>
 __global__ void __launch_bounds__(tc::THREADS, 1)
 k_topk_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmB,
           const float* __restrict__ q_inv, int64_t nq, const float* __restrict__ inv,
-          int64_t n_rows, int nkb, int stages, int k, float theta, int64_t head, int64_t gcap,
-          int64_t slot_offset, int64_t tiles_per_slice, uint64_t* __restrict__ partials) {
+          int64_t n_rows, int nkb, int stages, int k, float theta, int64_t hmod, int64_t gcap,
+          int64_t slot_offset, int64_t tiles_per_slice, uint64_t* __restrict__ partials, int dbg) {
+  constexpr int BN_CTA = tc::BN / CG;          // B rows this CTA loads per tile
+  constexpr int B_STAGE = BN_CTA * tc::BK;     // bytes per K-block stage per CTA
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~(uintptr_t)1023);
+  // 1024-B alignment for the 128B-swizzle atoms; index the __shared__ array
+  // (not an integer round trip) so every access stays LDS/STS, not generic.
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;                                        // nkb x 16 KB
-  uint8_t* sB = sA + nkb * tc::A_BLK;                        // stages x 32 KB
-  uint64_t* s_heap = reinterpret_cast<uint64_t*>(sB + stages * tc::B_STAGE);  // [k][128]
-  float* s_iw = reinterpret_cast<float*>(s_heap + (size_t)k * tc::BM);      // [4][256]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(s_iw + 4 * tc::BN);
+  uint8_t* sB = sA + nkb * tc::A_BLK;                        // stages x B_STAGE
+  uint64_t* s_heap = reinterpret_cast<uint64_t*>(sB + stages * B_STAGE);  // [k][128]
+  float* s_iw = reinterpret_cast<float*>(s_heap + (size_t)k * tc::BM);  // [4 warps][2][256]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(s_iw + 8 * tc::BN);
   uint64_t* a_full = bars;
   uint64_t* full = bars + 1;
   uint64_t* empty = full + stages;
@@ -150,7 +271,9 @@ k_topk_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUten
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int qt = blockIdx.x, slice = blockIdx.y;
+  const uint32_t rank = (CG == 2) ? cluster_rank() : 0u;
+  const bool leader = (rank == 0);
+  const int qt = blockIdx.x, slice = blockIdx.y;  // qt: 128-query tile of this CTA
   const int64_t tile0 = (int64_t)slice * tiles_per_slice;
   const int64_t total_tiles = (n_rows + tc::BN - 1) / tc::BN;
   const int64_t tile1 = min(total_tiles, tile0 + tiles_per_slice);
@@ -166,47 +289,60 @@ k_topk_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUten
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 4);  // one arrive per epilogue warp
+      mbar_init(&tempty[b], 4 * CG);  // one arrive per epilogue warp of the pair
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
-                     smem_u32(s_tmem)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
-  }
+  if (warp == 1) tmem_alloc512<CG>(s_tmem);
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *s_tmem;
 
   if (warp == 0) {
     // ------------------------------------------------------ TMA producer ---
     if (lane == 0 && ntiles > 0) {
-      mbar_expect_tx(a_full, nkb * tc::A_BLK);
+      // the leader's barriers count the bytes landing in both CTAs
+      if (leader) mbar_expect_tx(a_full, CG * nkb * tc::A_BLK);
       for (int kb = 0; kb < nkb; ++kb)
-        tma_load_2d(sA + kb * tc::A_BLK, &tmQ, a_full, kb * tc::BK, qt * tc::BM);
+        tma_load_2d<CG>(sA + kb * tc::A_BLK, &tmQ, a_full, kb * tc::BK, qt * tc::BM);
+      // optional L2 prefetch PF tiles ahead of the smem ring
+      const int PF = (dbg >> 8) & 0xff;
+      for (int t = 0; t < PF && t < ntiles; ++t)
+        for (int kb = 0; kb < nkb; ++kb)
+          tma_prefetch_l2_2d(&tmB, kb * tc::BK, (int)((tile0 + t) * tc::BN + rank * BN_CTA));
       int it = 0;
       for (int t = 0; t < ntiles; ++t) {
-        const int row0 = (int)((tile0 + t) * tc::BN);
+        const int row0 = (int)((tile0 + t) * tc::BN + rank * BN_CTA);
+        if (t + PF < ntiles && PF > 0)
+          for (int kb = 0; kb < nkb; ++kb)
+            tma_prefetch_l2_2d(&tmB, kb * tc::BK, row0 + PF * tc::BN);
         for (int kb = 0; kb < nkb; ++kb, ++it) {
           const int s = it % stages;
           mbar_wait(&empty[s], ((it / stages) & 1) ^ 1);
-          mbar_expect_tx(&full[s], tc::B_STAGE);
-          tma_load_2d(sB + s * tc::B_STAGE, &tmB, &full[s], kb * tc::BK, row0);
+          if (dbg & 8) {  // debug: no bank traffic
+            if (leader) mbar_expect_tx(&full[s], 0);
+            continue;
+          }
+          if (leader) mbar_expect_tx(&full[s], CG * B_STAGE);
+          tma_load_2d<CG>(sB + s * B_STAGE, &tmB, &full[s], kb * tc::BK, row0);
         }
       }
+      // drain: wait for the final MMA commits on every stage, so no
+      // (multicast) arrive can target this CTA's shared memory after it exits
+      for (int i = max(0, it - stages); i < it; ++i) mbar_wait(&empty[i % stages], (i / stages) & 1);
     }
   } else if (warp == 1) {
     // ------------------------------------------------------- MMA issuer ----
-    if (lane == 0 && ntiles > 0) {
+    if (leader && lane == 0 && ntiles > 0) {
       mbar_wait(a_full, 0);
       tc_fence_after();
       const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
       int it = 0;
       for (int t = 0; t < ntiles; ++t) {
         const int acc = t & 1;
-        mbar_wait(&tempty[acc], ((t >> 1) & 1) ^ 1);
+        if constexpr (CG == 2) mbar_wait_cluster(&tempty[acc], ((t >> 1) & 1) ^ 1);
+        else mbar_wait(&tempty[acc], ((t >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d = tmem + acc * tc::BN;
         for (int kb = 0; kb < nkb; ++kb, ++it) {
@@ -215,13 +351,13 @@ k_topk_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUten
           tc_fence_after();
 #pragma unroll
           for (int kk = 0; kk < tc::BK / tc::UK; ++kk) {
-            uint64_t ad = umma_desc_sw128(a_base + kb * tc::A_BLK + kk * tc::UK);
-            uint64_t bd = umma_desc_sw128(b_base + s * tc::B_STAGE + kk * tc::UK);
-            tc_mma_i8(d, ad, bd, IDESC_I8, (kb | kk) != 0);
+            const uint64_t ad = umma_desc_sw128(a_base + kb * tc::A_BLK + kk * tc::UK);
+            const uint64_t bd = umma_desc_sw128(b_base + s * B_STAGE + kk * tc::UK);
+            if (!(dbg & 2)) tc_mma_i8<CG>(d, ad, bd, idesc_i8<CG>(), (kb | kk) != 0);
           }
-          tc_commit(&empty[s]);  // frees the B stage once these MMAs retire
+          tc_commit<CG>(&empty[s]);  // frees the B stage (in both CTAs) once these MMAs retire
         }
-        tc_commit(&tfull[acc]);  // accumulator ready for the epilogue
+        tc_commit<CG>(&tfull[acc]);  // accumulator ready for the epilogue(s)
       }
     }
   } else {
@@ -231,58 +367,135 @@ k_topk_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUten
     const int qrow = quarter * 32 + lane;       // query row within the tile
     const int64_t q = (int64_t)qt * tc::BM + qrow;
     const float iq = (q < nq) ? q_inv[q] : __int_as_float(0x7fc00000);
-    HeapState st;
-    st.cnt = 0;
-    st.root = 0;
-    st.thr_s = (iq == iq) ? s_threshold(theta, iq) : INFINITY;
+    // per-query heap state in registers (see topk_heap.cuh for the invariant)
+    int hcnt = 0;
+    uint64_t hroot = 0;
     uint64_t* heap = s_heap + qrow;
-    float* wiw = s_iw + ew * tc::BN;
+    float* wiw = s_iw + ew * 2 * tc::BN;  // double-buffered per warp
+    const float NaNf = __int_as_float(0x7fc00000);
+    // register prefetch of a tile's inverse norms (8 per lane)
+    float pre[8];
+    auto fetch_iw = [&](int t) {
+      const int64_t r0 = (tile0 + t) * tc::BN + lane * 8;
+      if (r0 + 8 <= n_rows) {
+        const float4* p = reinterpret_cast<const float4*>(inv + r0);
+        float4 a = __ldg(p), b = __ldg(p + 1);
+        pre[0] = a.x; pre[1] = a.y; pre[2] = a.z; pre[3] = a.w;
+        pre[4] = b.x; pre[5] = b.y; pre[6] = b.z; pre[7] = b.w;
+      } else {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) pre[u] = (r0 + u < n_rows) ? inv[r0 + u] : NaNf;
+      }
+    };
+    if (ntiles > 0) fetch_iw(0);
+    // conservative s-domain filter: admits every row whose exact key can reach
+    // the current k-th best (or theta while the heap fills)
+    float thr = (iq == iq) ? s_threshold(theta, iq) : INFINITY;
     for (int t = 0; t < ntiles; ++t) {
       const int acc = t & 1;
       const int64_t row0 = (tile0 + t) * tc::BN;
-      // this tile's inverse norms -> warp-private smem (8 per lane)
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        int64_t r = row0 + lane * 8 + u;
-        wiw[lane * 8 + u] = (r < n_rows) ? inv[r] : __int_as_float(0x7fc00000);
+      float* ciw = wiw + (t & 1) * tc::BN;
+      {
+        float4* d = reinterpret_cast<float4*>(ciw + lane * 8);
+        d[0] = make_float4(pre[0], pre[1], pre[2], pre[3]);
+        d[1] = make_float4(pre[4], pre[5], pre[6], pre[7]);
       }
       __syncwarp();
+      if (t + 1 < ntiles) fetch_iw(t + 1);  // overlaps this tile's epilogue
       mbar_wait(&tfull[acc], (t >> 1) & 1);
       tc_fence_after();
       const uint32_t tbase = tmem + ((uint32_t)(quarter * 32) << 16) + acc * tc::BN;
-#pragma unroll 1
-      for (int c = 0; c < tc::BN / 32; ++c) {
-        int v[32];
-        tmem_ld32(tbase + c * 32, v);
-        if (c == tc::BN / 32 - 1) {
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty[acc]);
-        }
-        float thr = st.thr_s;
+      auto chunk = [&](const int (&v)[32], const int c) {
+        if (dbg & 4) return;  // debug: TMEM drain only
+        // hot path: 32 independent s = fl(dot * inv_w), one max tree, one branch
+        float s[32];
+        const float4* iw4 = reinterpret_cast<const float4*>(ciw + c * 32);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const float iw = wiw[c * 32 + j];
-          const float s = __fmul_rn(__int2float_rn(v[j]), iw);
-          if (s >= thr) {
-            tc_consider(heap, k, &st, v[j], iw, iq, theta, slot_offset + row0 + c * 32 + j, head,
-                        gcap);
-            thr = st.thr_s;
+        for (int j4 = 0; j4 < 8; ++j4) {
+          const float4 w = iw4[j4];  // broadcast LDS.128
+          s[4 * j4 + 0] = __fmul_rn(__int2float_rn(v[4 * j4 + 0]), w.x);
+          s[4 * j4 + 1] = __fmul_rn(__int2float_rn(v[4 * j4 + 1]), w.y);
+          s[4 * j4 + 2] = __fmul_rn(__int2float_rn(v[4 * j4 + 2]), w.z);
+          s[4 * j4 + 3] = __fmul_rn(__int2float_rn(v[4 * j4 + 3]), w.w);
+        }
+        float m[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) m[j] = fmaxf(s[j], s[j + 16]);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) m[j] = fmaxf(m[j], m[j + 8]);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) m[j] = fmaxf(m[j], m[j + 4]);
+        const float mx = fmaxf(fmaxf(m[0], m[1]), fmaxf(m[2], m[3]));
+        if (!(dbg & 1) && mx >= thr) {  // rare: exact keys and heap inserts for this chunk
+          // key = fl(s * iq) is exactly the oracle's fl(fl(dot*iw)*iq); the
+          // common case is an append while the heap fills, inlined here; only
+          // heapify / root replacement leave the hot code (noinline helpers)
+          const int64_t gbase = slot_offset + row0 + c * 32 - hmod;
+          uint32_t mask = 0;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) mask |= (s[j] >= thr ? 1u : 0u) << j;
+          float sl[32];  // dynamic indexing below: the compiler stages these in local memory
+#pragma unroll
+          for (int j = 0; j < 32; ++j) sl[j] = s[j];
+          while (mask) {
+            const int j = __ffs(mask) - 1;
+            mask &= mask - 1;
+            {
+              const float key = __fmul_rn(sl[j], iq);
+              if (key >= theta) {
+                int64_t rel = gbase + j;
+                if (rel < 0) rel += gcap;
+                const uint64_t comp = make_comp(key, (uint32_t)rel);
+                if (hcnt < k) {
+                  heap[hcnt * tc::BM] = comp;
+                  if (++hcnt == k) {
+                    hroot = tc_heapify(heap, k);
+                    thr = fmaxf(thr, s_threshold(comp_key(hroot), iq));
+                  }
+                } else if (comp > hroot) {
+                  hroot = tc_heap_replace(heap, k, comp);
+                  thr = fmaxf(thr, s_threshold(comp_key(hroot), iq));
+                }
+              }
+            }
           }
         }
+      };
+      // software pipeline: the TMEM load of chunk c+1 is in flight while
+      // chunk c is scanned
+      int va[32], vb[32];
+      tmem_ld32_async(tbase, va);
+      tmem_wait_regs(va);
+#pragma unroll 1
+      for (int c = 0; c < tc::BN / 32; c += 2) {
+        tmem_ld32_async(tbase + (c + 1) * 32, vb);
+        chunk(va, c);
+        tmem_wait_regs(vb);
+        if (c + 2 < tc::BN / 32) {
+          tmem_ld32_async(tbase + (c + 2) * 32, va);
+        } else {  // accumulator drained: hand it back to the MMA warp
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            if constexpr (CG == 2) mbar_arrive_leader(&tempty[acc]);
+            else mbar_arrive(&tempty[acc]);
+          }
+        }
+        chunk(vb, c + 1);
+        if (c + 2 < tc::BN / 32) tmem_wait_regs(va);
       }
       __syncwarp();
     }
     if (q < nq) {
       uint64_t* out = partials + ((int64_t)slice * nq + q) * k;
-      for (int i = 0; i < k; ++i) out[i] = (i < st.cnt) ? heap[i * tc::BM] : 0ull;
+      for (int i = 0; i < k; ++i) out[i] = (i < hcnt) ? heap[i * tc::BM] : 0ull;
     }
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync(); else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
+    tmem_dealloc512<CG>(tmem);
   }
 }
 
@@ -313,16 +526,36 @@ static int make_map(CUtensorMap* m, const void* base, int64_t rows, int dim, int
   return SS_OK;
 }
 
-static int tc_stages(int dim, int k) {
-  const int fixed = (dim / tc::BK) * tc::A_BLK + k * tc::BM * 8 + 4 * tc::BN * 4 + 256 + 1024;
-  for (int s = 4; s >= 2; --s)
-    if (fixed + s * tc::B_STAGE <= 227 * 1024) return s;
-  return 0;
+static int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
 }
 
-static size_t tc_smem(int dim, int k, int stages) {
-  return (size_t)(dim / tc::BK) * tc::A_BLK + (size_t)stages * tc::B_STAGE +
-         (size_t)k * tc::BM * 8 + 4 * tc::BN * 4 + 256 + 1024;
+// CTA-pair (cta_group::2) variant: correct and available (SS_TC_CG=2), but
+// measured slower than single-CTA MMA here because the bound is the TMEM
+// drain + epilogue, not L2->SM traffic (profiles/ROUND1.md), so off by default.
+static int tc_cg(int64_t nq) {
+  int v = env_int("SS_TC_CG", 0);
+  if ((v == 1 || v == 2) && (v == 1 || nq > tc::BM)) return v;
+  return 1;
+}
+
+// L2 prefetch distance (tiles), off by default (measured: no gain)
+static int tc_prefetch() { return env_int("SS_TC_PREFETCH", 0) & 0xff; }
+
+static size_t tc_fixed_smem(int dim, int k) {
+  return (size_t)(dim / tc::BK) * tc::A_BLK + (size_t)k * tc::BM * 8 + 8 * tc::BN * 4 + 512 + 1024;
+}
+
+static int tc_stages(int dim, int k, int cg) {
+  const int forced = env_int("SS_TC_STAGES", 0);
+  const size_t stage = (size_t)(tc::BN / cg) * tc::BK;
+  const size_t fixed = tc_fixed_smem(dim, k);
+  int s = 0;
+  for (int c = 8; c >= 2; --c)
+    if (fixed + c * stage <= 227 * 1024) { s = c; break; }
+  if (forced >= 2 && forced <= s) s = forced;
+  return s;
 }
 
 bool topk_tc_supported(const TopkArgs& a) {
@@ -333,12 +566,14 @@ bool topk_tc_supported(const TopkArgs& a) {
   cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
   cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
   if (major != 10 || minor != 0) return false;  // built for sm_100a only
-  return tc_stages(a.dim, a.k) >= 2;
+  return tc_stages(a.dim, a.k, 1) >= 2;
 }
 
 int topk_tc_slices(const TopkArgs& a, int device) {
   int sms = sm_count(device);
+  const int cg = tc_cg(a.nq);
   int64_t qtiles = (a.nq + tc::BM - 1) / tc::BM;
+  qtiles = (qtiles + cg - 1) / cg * cg;
   int64_t tiles = (a.n_rows + tc::BN - 1) / tc::BN;
   int64_t want = sms / qtiles;
   if (want < 1) want = 1;
@@ -346,23 +581,44 @@ int topk_tc_slices(const TopkArgs& a, int device) {
   return (int)want;
 }
 
-int launch_topk_tc(const TopkArgs& a, uint64_t* partials, int n_slices, cudaStream_t st) {
-  if (!topk_tc_supported(a)) return set_error(SS_ERR_UNSUPPORTED, "tcgen05 path unsupported");
-  const int stages = tc_stages(a.dim, a.k);
-  const size_t smem = tc_smem(a.dim, a.k, stages);
+template <int CG>
+static int launch_cg(const TopkArgs& a, uint64_t* partials, int n_slices, cudaStream_t st) {
+  const int stages = tc_stages(a.dim, a.k, CG);
+  if (stages < 2) return set_error(SS_ERR_UNSUPPORTED, "tcgen05: not enough shared memory");
+  const size_t smem = tc_fixed_smem(a.dim, a.k) + (size_t)stages * (tc::BN / CG) * tc::BK;
   CUtensorMap mq, mb;
   if (int rc = make_map(&mq, a.q, a.nq, a.dim, tc::BM)) return rc;
-  if (int rc = make_map(&mb, a.emb, a.n_rows, a.dim, tc::BN)) return rc;
-  SS_CUDA_TRY(cudaFuncSetAttribute(k_topk_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (int rc = make_map(&mb, a.emb, a.n_rows, a.dim, tc::BN / CG)) return rc;
+  SS_CUDA_TRY(cudaFuncSetAttribute(k_topk_tc<CG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem));
   const int64_t tiles = (a.n_rows + tc::BN - 1) / tc::BN;
   const int64_t tps = (tiles + n_slices - 1) / n_slices;
-  dim3 grid((unsigned)((a.nq + tc::BM - 1) / tc::BM), (unsigned)n_slices);
+  int64_t qtiles = (a.nq + tc::BM - 1) / tc::BM;
+  qtiles = (qtiles + CG - 1) / CG * CG;  // a pair always has two CTAs
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)qtiles, (unsigned)n_slices);
+  cfg.blockDim = dim3(tc::THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const int dbg = env_int("SS_TC_DEBUG", 0) | (tc_prefetch() << 8);
   count_launch();
-  k_topk_tc<<<grid, tc::THREADS, smem, st>>>(mq, mb, a.q_inv, a.nq, a.inv, a.n_rows, a.dim / tc::BK,
-                                             stages, a.k, a.theta, a.head, a.gcap, a.slot_offset,
-                                             tps, partials);
-  SS_LAUNCH_CHECK();
+  SS_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_topk_tc<CG>, mq, mb, a.q_inv, a.nq, a.inv, a.n_rows,
+                                 a.dim / tc::BK, stages, a.k, a.theta, a.head % a.gcap, a.gcap,
+                                 a.slot_offset, tps, partials, dbg));
   return SS_OK;
+}
+
+int launch_topk_tc(const TopkArgs& a, uint64_t* partials, int n_slices, cudaStream_t st) {
+  if (!topk_tc_supported(a)) return set_error(SS_ERR_UNSUPPORTED, "tcgen05 path unsupported");
+  return tc_cg(a.nq) == 2 ? launch_cg<2>(a, partials, n_slices, st)
+                          : launch_cg<1>(a, partials, n_slices, st);
 }
 
 }  // namespace ss

@@ -61,7 +61,8 @@ __device__ __forceinline__ void heap_consider(uint64_t* heap, int k, HeapState& 
                                               int64_t head, int64_t gcap) {
   float key = score_key(dot, iw, iq);
   if (!(key >= theta)) return;
-  int64_t rel = (gslot - head) % gcap;
+  // `head` is passed pre-reduced mod gcap by the launcher, so no 64-bit modulo
+  int64_t rel = gslot - head;
   if (rel < 0) rel += gcap;
   heap_offer<STRIDE>(heap, k, st, make_comp(key, (uint32_t)rel), iq);
 }
