@@ -1,6 +1,11 @@
 // History bank maintenance: FIFO ring writes and the window-wide fallback
 // histogram.  Reference contract: SPEC.md:101-130 (HistoryRecord, push),
 // SPEC.md:184-186,223 (fallback = empirical law of the whole window).
+//
+// The bank keeps an exact-length count histogram len_cnt[0..65535] up to date
+// on every write (+1 for the new record, -1 for the evicted one; integer
+// atomics, so exact), which makes the per-round fallback histogram a scan of
+// the count table instead of a scan of the whole window.
 #include "ss_common.cuh"
 #include "ss_internal.h"
 
@@ -10,11 +15,11 @@ namespace ss {
 // norm (IEEE 1/sqrt, bit-identical to numpy float32), length and seq.
 __global__ void __launch_bounds__(256)
 k_bank_write(int8_t* __restrict__ emb, float* __restrict__ inv, int32_t* __restrict__ lens,
-             int64_t* __restrict__ seq, int dim, const int8_t* __restrict__ src_emb,
-             const float* __restrict__ src_inv, const int32_t* __restrict__ src_lens,
-             const int64_t* __restrict__ src_seq, const int64_t* __restrict__ src_slot,
-             int64_t n, int64_t first_seq, int64_t capacity, int64_t skip,
-             int* __restrict__ err) {
+             int64_t* __restrict__ seq, int32_t* __restrict__ len_cnt, int dim,
+             const int8_t* __restrict__ src_emb, const float* __restrict__ src_inv,
+             const int32_t* __restrict__ src_lens, const int64_t* __restrict__ src_seq,
+             const int64_t* __restrict__ src_slot, int64_t n, int64_t first_seq,
+             int64_t capacity, int64_t skip, int* __restrict__ err) {
   const int lane = threadIdx.x & 31;
   const int64_t r = skip + (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (r >= n) return;
@@ -36,8 +41,13 @@ k_bank_write(int8_t* __restrict__ emb, float* __restrict__ inv, int32_t* __restr
   }
   for (int o = 16; o > 0; o >>= 1) ss2 += __shfl_xor_sync(0xffffffffu, ss2, o);
   if (lane == 0) {
+    if (seq[slot] >= 0) atomicSub(&len_cnt[lens[slot] & 0xffff], 1);  // evicted record
     int L = src_lens[r];
-    if (L < 1 || L > 65535) atomicExch(err, SS_ERR_RANGE);
+    if (L < 1 || L > 65535) {
+      atomicExch(err, SS_ERR_RANGE);
+      L = max(1, min(L, 65535));
+    }
+    atomicAdd(&len_cnt[L], 1);
     lens[slot] = L;
     seq[slot] = s;
     float iv;
@@ -47,66 +57,70 @@ k_bank_write(int8_t* __restrict__ emb, float* __restrict__ inv, int32_t* __restr
   }
 }
 
-int launch_bank_write(int8_t* emb, float* inv, int32_t* lens, int64_t* seq, int dim,
-                      const int8_t* src_emb, const float* src_inv, const int32_t* src_lens,
-                      const int64_t* src_seq, const int64_t* src_slot, int64_t n,
-                      int64_t first_seq, int64_t capacity, int64_t skip, int* err,
+int launch_bank_write(int8_t* emb, float* inv, int32_t* lens, int64_t* seq, int32_t* len_cnt,
+                      int dim, const int8_t* src_emb, const float* src_inv,
+                      const int32_t* src_lens, const int64_t* src_seq, const int64_t* src_slot,
+                      int64_t n, int64_t first_seq, int64_t capacity, int64_t skip, int* err,
                       cudaStream_t st) {
   int64_t m = n - skip;
   if (m <= 0) return SS_OK;
   count_launch();
-  k_bank_write<<<(unsigned)((m + 7) / 8), 256, 0, st>>>(emb, inv, lens, seq, dim, src_emb,
+  k_bank_write<<<(unsigned)((m + 7) / 8), 256, 0, st>>>(emb, inv, lens, seq, len_cnt, dim, src_emb,
                                                           src_inv, src_lens, src_seq, src_slot,
                                                           n, first_seq, capacity, skip, err);
   SS_LAUNCH_CHECK();
   return SS_OK;
 }
 
-// window histogram: per-CTA shared-memory atomics, then one global atomic per
-// non-empty bin.  Integer-exact, so the order of accumulation is irrelevant.
-__global__ void __launch_bounds__(256)
-k_fallback_hist(const int32_t* __restrict__ lens, const int64_t* __restrict__ seq,
-                int64_t capacity, int max_len, int nbins, unsigned long long* __restrict__ cnt,
-                unsigned long long* __restrict__ sv, unsigned long long* __restrict__ sv2) {
+// fallback histogram from the exact-length counts: one CTA walks len_cnt,
+// clamps lengths to max_len and accumulates (count, sum v, sum v^2) per bin
+// with shared-memory atomics.  Integer-exact.
+constexpr int FB_THREADS = 1024;
+
+__global__ void __launch_bounds__(FB_THREADS)
+k_fallback_hist(const int32_t* __restrict__ len_cnt, int max_len, int nbins,
+                int64_t* __restrict__ cnt, int64_t* __restrict__ sv, int64_t* __restrict__ sv2) {
   extern __shared__ unsigned long long s_h[];  // [3][nbins]
   const int w = max_len / nbins;
   for (int b = threadIdx.x; b < 3 * nbins; b += blockDim.x) s_h[b] = 0ull;
   __syncthreads();
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < capacity;
-       j += (int64_t)gridDim.x * blockDim.x) {
-    if (seq[j] < 0) continue;
-    int L = min(lens[j], max_len);
-    int b = (L - 1) / w;
-    atomicAdd(&s_h[b], 1ull);
-    atomicAdd(&s_h[nbins + b], (unsigned long long)L);
-    atomicAdd(&s_h[2 * nbins + b], (unsigned long long)L * (unsigned long long)L);
+  // 65536 counts = 16 int4 per thread, all loads issued before any use
+  const int4* c4 = reinterpret_cast<const int4*>(len_cnt);
+  int4 r[16];
+#pragma unroll
+  for (int u = 0; u < 16; ++u) r[u] = c4[u * FB_THREADS + threadIdx.x];
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    const int base = 4 * (u * FB_THREADS + threadIdx.x);
+    const int cs[4] = {r[u].x, r[u].y, r[u].z, r[u].w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int v = base + e;
+      const int c = cs[e];
+      if (c == 0 || v == 0) continue;
+      const unsigned long long L = (unsigned long long)min(v, max_len);
+      const int b = (int)(L - 1) / w;
+      atomicAdd(&s_h[b], (unsigned long long)c);
+      atomicAdd(&s_h[nbins + b], (unsigned long long)c * L);
+      atomicAdd(&s_h[2 * nbins + b], (unsigned long long)c * L * L);
+    }
   }
   __syncthreads();
   for (int b = threadIdx.x; b < nbins; b += blockDim.x) {
-    if (s_h[b]) {
-      atomicAdd(&cnt[b], s_h[b]);
-      atomicAdd(&sv[b], s_h[nbins + b]);
-      atomicAdd(&sv2[b], s_h[2 * nbins + b]);
-    }
+    cnt[b] = (int64_t)s_h[b];
+    sv[b] = (int64_t)s_h[nbins + b];
+    sv2[b] = (int64_t)s_h[2 * nbins + b];
   }
 }
 
-int launch_fallback_hist(const int32_t* lens, const int64_t* seq, int64_t capacity,
-                         int max_len, int nbins, int64_t* cnt, int64_t* sv, int64_t* sv2,
-                         cudaStream_t st) {
-  SS_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(int64_t) * nbins, st));
-  SS_CUDA_TRY(cudaMemsetAsync(sv, 0, sizeof(int64_t) * nbins, st));
-  SS_CUDA_TRY(cudaMemsetAsync(sv2, 0, sizeof(int64_t) * nbins, st));
-  if (capacity <= 0) return SS_OK;
+int launch_fallback_hist(const int32_t* len_cnt, int max_len, int nbins, int64_t* cnt, int64_t* sv,
+                         int64_t* sv2, cudaStream_t st) {
   size_t smem = (size_t)3 * nbins * sizeof(unsigned long long);
   if (smem > 48 * 1024)
-    SS_CUDA_TRY(cudaFuncSetAttribute(k_fallback_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int64_t blocks = (capacity + 2047) / 2048;
-  if (blocks > 296) blocks = 296;
+    SS_CUDA_TRY(cudaFuncSetAttribute(k_fallback_hist, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
   count_launch();
-  k_fallback_hist<<<(unsigned)blocks, 256, smem, st>>>(
-      lens, seq, capacity, max_len, nbins, reinterpret_cast<unsigned long long*>(cnt),
-      reinterpret_cast<unsigned long long*>(sv), reinterpret_cast<unsigned long long*>(sv2));
+  k_fallback_hist<<<1, FB_THREADS, smem, st>>>(len_cnt, max_len, nbins, cnt, sv, sv2);
   SS_LAUNCH_CHECK();
   return SS_OK;
 }

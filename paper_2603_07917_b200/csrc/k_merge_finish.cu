@@ -13,52 +13,88 @@
 
 namespace ss {
 
-// ---------------------------------------------------------------------------
-// merge: per query, select the top-k of nlists*k candidate composites by an
-// MSB-first 8-bit radix select, then bitonic-sort the k winners descending.
-// ---------------------------------------------------------------------------
-constexpr int MERGE_THREADS = 256;
+constexpr int MF_THREADS = 256;
 
-__global__ void __launch_bounds__(MERGE_THREADS)
-k_merge(const uint64_t* __restrict__ comp, const int32_t* __restrict__ len, int nlists,
-        int64_t nq, int k, int kpad, uint64_t* __restrict__ out_comp,
-        int32_t* __restrict__ out_len, const int32_t* __restrict__ bank_lens, int64_t head,
-        int64_t gcap, int64_t slot_offset) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  const int M = nlists * k;
-  uint64_t* cand = reinterpret_cast<uint64_t*>(smem);            // [M]
-  uint64_t* sel = cand + M;                                      // [kpad]
-  int32_t* clen = reinterpret_cast<int32_t*>(sel + kpad);        // [M] (if len)
-  int32_t* slen = clen + (len ? M : 0);                          // [kpad]
-  __shared__ int hist[256];
-  __shared__ int s_cnt, s_digit, s_need;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t q = blockIdx.x;
+// ---------------------------------------------------------------------------
+// select the top-k of M candidate composites (cand[0..M) in smem) into
+// sel[0..kpad) sorted descending (0-padded), carrying an int32 payload.
+// MSB-first 8-bit radix select of the k-th largest when more than k are
+// non-zero, then a bitonic sort of the <= k winners.
+// ---------------------------------------------------------------------------
+// Fast path first: every full input list (k non-zero entries) proves that the
+// global k-th best is >= that list's minimum, so candidates below
+// tau = max over full lists of their minimum are dropped; when at most
+// SORT_MAX candidates survive they are bitonic-sorted directly.
+constexpr int SORT_MAX = 512;
 
-  int nz = 0;
-  for (int i = tid; i < M; i += MERGE_THREADS) {
-    int l = i / k, j = i % k;
-    int64_t src = ((int64_t)l * nq + q) * k + j;
-    uint64_t c = comp[src];
-    cand[i] = c;
-    if (len) clen[i] = len[src];
-    nz += (c != 0ull);
+__device__ bool block_select_small(uint64_t* cand, int32_t* cpay, int M, int nlists, int k,
+                                   int kpad, uint64_t* sel, int32_t* spay, int* s_misc) {
+  __shared__ uint64_t tau_s;
+  uint64_t* s_tau = &tau_s;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  if (tid == 0) { *s_tau = 1ull; s_misc[3] = 0; }
+  __syncthreads();
+  for (int l = warp; l < nlists; l += nw) {
+    uint64_t mn = ~0ull;
+    for (int j = lane; j < k; j += 32) mn = min(mn, cand[l * k + j]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    if (lane == 0 && mn != 0ull) atomicMax(reinterpret_cast<unsigned long long*>(s_tau), mn);
   }
+  __syncthreads();
+  const uint64_t tau = *s_tau;
+  // compact survivors (>= tau, non-zero) into the front of cand (stable
+  // order is irrelevant: composites are unique)
+  __shared__ uint64_t buf[SORT_MAX];
+  __shared__ int32_t pbuf[SORT_MAX];
+  for (int i = tid; i < M; i += blockDim.x) {
+    const uint64_t c = cand[i];
+    if (c >= tau) {
+      int p = atomicAdd(&s_misc[3], 1);
+      if (p < SORT_MAX) { buf[p] = c; pbuf[p] = cpay[i]; }
+    }
+  }
+  __syncthreads();
+  const int m1 = s_misc[3];
+  if (m1 > SORT_MAX) return false;
+  // rank by counting (composites are unique): no barriers inside, the
+  // broadcast LDS of buf[j] is shared by the whole warp
+  for (int i = tid; i < kpad; i += blockDim.x) { sel[i] = 0ull; spay[i] = 0; }
+  __syncthreads();
+  for (int i = tid; i < m1; i += blockDim.x) {
+    const uint64_t c = buf[i];
+    int r = 0;
+    for (int j = 0; j < m1; ++j) r += (buf[j] > c);
+    if (r < k) {
+      sel[r] = c;
+      spay[r] = pbuf[i];
+    }
+  }
+  __syncthreads();
+  return true;
+}
+
+__device__ void block_select_topk(uint64_t* cand, int32_t* cpay, int M, int nlists, int k, int kpad,
+                                  uint64_t* sel, int32_t* spay, int* hist, int* s_misc) {
+  if (block_select_small(cand, cpay, M, nlists, k, kpad, sel, spay, s_misc)) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int nz = 0;
+  for (int i = tid; i < M; i += blockDim.x) nz += (cand[i] != 0ull);
   for (int o = 16; o > 0; o >>= 1) nz += __shfl_xor_sync(0xffffffffu, nz, o);
-  if (tid == 0) s_cnt = 0;
+  if (tid == 0) s_misc[0] = 0;
   __syncthreads();
-  if (lane == 0) atomicAdd(&s_cnt, nz);
+  if (lane == 0) atomicAdd(&s_misc[0], nz);
   __syncthreads();
-  const int m0 = s_cnt;
+  const int m0 = s_misc[0];
 
   uint64_t kth = 1ull;  // select every non-zero when m0 <= k
   if (m0 > k) {
     uint64_t prefix = 0, mask = 0;
     int need = k;
     for (int shift = 56; shift >= 0; shift -= 8) {
-      hist[tid] = 0;
+      for (int d = tid; d < 256; d += blockDim.x) hist[d] = 0;
       __syncthreads();
-      for (int i0 = 0; i0 < M; i0 += MERGE_THREADS) {
+      for (int i0 = 0; i0 < M; i0 += blockDim.x) {
         int i = i0 + tid;
         bool act = false;
         int d = 0;
@@ -85,38 +121,36 @@ k_merge(const uint64_t* __restrict__ comp, const int32_t* __restrict__ len, int 
           int cum = excl;
           for (int t = 0; t < 8; ++t) {
             int d = 255 - 8 * lane - t;
-            if (cum + hist[d] >= need) { s_digit = d; s_need = need - cum; break; }
+            if (cum + hist[d] >= need) { s_misc[1] = d; s_misc[2] = need - cum; break; }
             cum += hist[d];
           }
         }
       }
       __syncthreads();
-      prefix |= (uint64_t)s_digit << shift;
+      prefix |= (uint64_t)s_misc[1] << shift;
       mask |= 255ull << shift;
-      need = s_need;
+      need = s_misc[2];
       __syncthreads();
     }
     kth = prefix;
   }
-  // gather winners (c >= kth), unordered, then bitonic sort descending
-  for (int i = tid; i < kpad; i += MERGE_THREADS) sel[i] = 0ull;
-  if (tid == 0) s_cnt = 0;
+  for (int i = tid; i < kpad; i += blockDim.x) sel[i] = 0ull;
+  if (tid == 0) s_misc[0] = 0;
   __syncthreads();
-  for (int i = tid; i < M; i += MERGE_THREADS) {
+  for (int i = tid; i < M; i += blockDim.x) {
     uint64_t c = cand[i];
     if (c != 0ull && c >= kth) {
-      int p = atomicAdd(&s_cnt, 1);
+      int p = atomicAdd(&s_misc[0], 1);
       if (p < kpad) {
         sel[p] = c;
-        if (len) slen[p] = clen[i];
+        spay[p] = cpay[i];
       }
     }
   }
   __syncthreads();
-  // bitonic sort (descending) of (sel, slen) over kpad (power of two)
   for (int size = 2; size <= kpad; size <<= 1) {
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int i = tid; i < kpad; i += MERGE_THREADS) {
+      for (int i = tid; i < kpad; i += blockDim.x) {
         int j = i ^ stride;
         if (j > i) {
           bool desc = ((i & size) == 0);
@@ -124,27 +158,71 @@ k_merge(const uint64_t* __restrict__ comp, const int32_t* __restrict__ len, int 
           if ((a < b) == desc) {
             sel[i] = b;
             sel[j] = a;
-            if (len) { int32_t t = slen[i]; slen[i] = slen[j]; slen[j] = t; }
+            int32_t t = spay[i]; spay[i] = spay[j]; spay[j] = t;
           }
         }
       }
       __syncthreads();
     }
   }
-  for (int i = tid; i < k; i += MERGE_THREADS) {
-    uint64_t c = sel[i];
-    out_comp[q * k + i] = c;
-    int32_t L = 0;
-    if (c != 0ull) {
-      if (len) {
-        L = slen[i];
-      } else {
-        int64_t g = ((int64_t)comp_rel(c) + head) % gcap;
-        L = bank_lens[g - slot_offset];
-      }
-    }
-    out_len[q * k + i] = L;
+}
+
+// load nlists x k candidates of query q; payload = carried length (len) or
+// the bank length looked up from the slot (single-GPU / local merge)
+__device__ void load_candidates(const uint64_t* comp, const int32_t* len, int nlists, int64_t nq,
+                                int k, int64_t q, uint64_t* cand, int32_t* cpay,
+                                const int32_t* bank_lens, int64_t head, int64_t gcap,
+                                int64_t slot_offset) {
+  const int M = nlists * k;
+  for (int i = threadIdx.x; i < M; i += blockDim.x) {
+    int l = i / k, j = i % k;
+    int64_t src = ((int64_t)l * nq + q) * k + j;
+    uint64_t c = comp[src];
+    cand[i] = c;
+    cpay[i] = len ? len[src] : 0;  // bank lengths are gathered for the winners only
   }
+  __syncthreads();
+}
+
+// winners' lengths from the local bank (single-GPU / local merge)
+__device__ void resolve_lens(const uint64_t* sel, int32_t* spay, int k, const int32_t* bank_lens,
+                             int64_t head, int64_t gcap, int64_t slot_offset) {
+  for (int i = threadIdx.x; i < k; i += blockDim.x) {
+    const uint64_t c = sel[i];
+    if (c != 0ull) {
+      int64_t g = (int64_t)comp_rel(c) + head % gcap;
+      if (g >= gcap) g -= gcap;
+      spay[i] = bank_lens[g - slot_offset];
+    }
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(MF_THREADS)
+k_merge(const uint64_t* __restrict__ comp, const int32_t* __restrict__ len, int nlists,
+        int64_t nq, int k, int kpad, uint64_t* __restrict__ out_comp,
+        int32_t* __restrict__ out_len, const int32_t* __restrict__ bank_lens, int64_t head,
+        int64_t gcap, int64_t slot_offset) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int M = nlists * k;
+  uint64_t* cand = reinterpret_cast<uint64_t*>(smem);      // [M]
+  uint64_t* sel = cand + M;                                // [kpad]
+  int32_t* cpay = reinterpret_cast<int32_t*>(sel + kpad);  // [M]
+  int32_t* spay = cpay + M;                                // [kpad]
+  __shared__ int hist[256];
+  __shared__ int s_misc[4];
+  const int64_t q = blockIdx.x;
+  load_candidates(comp, len, nlists, nq, k, q, cand, cpay, bank_lens, head, gcap, slot_offset);
+  block_select_topk(cand, cpay, M, nlists, k, kpad, sel, spay, hist, s_misc);
+  if (!len) resolve_lens(sel, spay, k, bank_lens, head, gcap, slot_offset);
+  for (int i = threadIdx.x; i < k; i += blockDim.x) {
+    out_comp[q * k + i] = sel[i];
+    out_len[q * k + i] = sel[i] ? spay[i] : 0;
+  }
+}
+
+static size_t merge_smem(int nlists, int k, int kpad) {
+  return (size_t)nlists * k * 12 + (size_t)kpad * 12;
 }
 
 int launch_merge(const uint64_t* comp, const int32_t* len, int nlists, int64_t nq, int k,
@@ -153,14 +231,13 @@ int launch_merge(const uint64_t* comp, const int32_t* len, int nlists, int64_t n
   if (nq <= 0) return SS_OK;
   int kpad = 1;
   while (kpad < k) kpad <<= 1;
-  int64_t M = (int64_t)nlists * k;
-  size_t smem = (size_t)M * 8 + (size_t)kpad * 8 + (len ? (size_t)M * 4 + (size_t)kpad * 4 : 0);
+  size_t smem = merge_smem(nlists, k, kpad);
   if (smem > 220 * 1024)
     return set_error(SS_ERR_UNSUPPORTED, "merge of %d lists x k=%d exceeds shared memory", nlists, k);
   SS_CUDA_TRY(cudaFuncSetAttribute(k_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   count_launch();
-  k_merge<<<(unsigned)nq, MERGE_THREADS, smem, st>>>(comp, len, nlists, nq, k, kpad, out_comp,
-                                                    out_len, bank_lens, head, gcap, slot_offset);
+  k_merge<<<(unsigned)nq, MF_THREADS, smem, st>>>(comp, len, nlists, nq, k, kpad, out_comp, out_len,
+                                                 bank_lens, head, gcap, slot_offset);
   SS_LAUNCH_CHECK();
   return SS_OK;
 }
@@ -242,90 +319,98 @@ __device__ double warp_gittins_exact(const int32_t* c, const int64_t* D, int np,
 }
 
 // ---------------------------------------------------------------------------
-// finish: one CTA per request.  Histogram with shared-memory atomics, ascending
-// ballot-scan compaction into the sparse law, then warp-0 Gittins.
+// finish for one request (whole CTA): histogram of the <= k sorted neighbours
+// (shared-memory atomics) or the fallback, ascending ballot-scan compaction
+// into the sparse law, then warp-0 Gittins.
 // ---------------------------------------------------------------------------
-constexpr int FIN_THREADS = 128;
+struct FinishSmem {
+  int64_t* h_sv;
+  int64_t* h_sv2;
+  int64_t* l_D;
+  int32_t* h_cnt;
+  int32_t* l_c;
+};
 
-__global__ void __launch_bounds__(FIN_THREADS)
-k_finish(const uint64_t* __restrict__ comp, const int32_t* __restrict__ len, int64_t nq, int k,
-         int min_matches, int max_len, int nbins, const int32_t* __restrict__ I,
-         const int64_t* __restrict__ fb_cnt, const int64_t* __restrict__ fb_sv,
-         const int64_t* __restrict__ fb_sv2, int P, int32_t* __restrict__ npts,
-         int32_t* __restrict__ pbin, int32_t* __restrict__ pcnt, int64_t* __restrict__ pD,
-         int64_t* __restrict__ psv, uint8_t* __restrict__ used_fb, double* __restrict__ G) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  int64_t* h_sv = reinterpret_cast<int64_t*>(smem);         // [nbins]
-  int64_t* h_sv2 = h_sv + nbins;                            // [nbins]
-  int64_t* l_D = h_sv2 + nbins;                             // [nbins]
-  int32_t* h_cnt = reinterpret_cast<int32_t*>(l_D + nbins); // [nbins]
-  int32_t* l_c = h_cnt + nbins;                             // [nbins]
-  __shared__ int s_m, s_base, s_warp[FIN_THREADS / 32];
+__device__ FinishSmem carve_finish(unsigned char* p, int nbins) {
+  FinishSmem f;
+  f.h_sv = reinterpret_cast<int64_t*>(p);
+  f.h_sv2 = f.h_sv + nbins;
+  f.l_D = f.h_sv2 + nbins;
+  f.h_cnt = reinterpret_cast<int32_t*>(f.l_D + nbins);
+  f.l_c = f.h_cnt + nbins;
+  return f;
+}
+static size_t finish_smem(int nbins) { return (size_t)nbins * (8 * 3 + 4 * 2); }
+
+__device__ void finish_one(const uint64_t* comp, const int32_t* len, int k, int64_t q,
+                           int min_matches, int max_len, int nbins, long long Iq,
+                           const int64_t* fb_cnt, const int64_t* fb_sv, const int64_t* fb_sv2,
+                           int P, int32_t* npts, int32_t* pbin, int32_t* pcnt, int64_t* pD,
+                           int64_t* psv, uint8_t* used_fb, double* G, FinishSmem f, int* s_misc,
+                           int* s_warp) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t q = blockIdx.x;
+  const int nw = blockDim.x >> 5;
   const int w = max_len / nbins;
-  const long long Iq = I[q];
-
   int m = 0;
-  for (int i = tid; i < k; i += FIN_THREADS) m += (comp[q * k + i] != 0ull);
+  for (int i = tid; i < k; i += blockDim.x) m += (comp[i] != 0ull);
   for (int o = 16; o > 0; o >>= 1) m += __shfl_xor_sync(0xffffffffu, m, o);
-  if (tid == 0) { s_m = 0; s_base = 0; }
+  if (tid == 0) { s_misc[0] = 0; s_misc[1] = 0; }
   __syncthreads();
-  if (lane == 0) atomicAdd(&s_m, m);
+  if (lane == 0) atomicAdd(&s_misc[0], m);
   __syncthreads();
-  const bool fb = s_m < min_matches;
+  const bool fb = s_misc[0] < min_matches;
   if (!fb) {
-    for (int b = tid; b < nbins; b += FIN_THREADS) { h_cnt[b] = 0; h_sv[b] = 0; h_sv2[b] = 0; }
+    for (int b = tid; b < nbins; b += blockDim.x) { f.h_cnt[b] = 0; f.h_sv[b] = 0; f.h_sv2[b] = 0; }
     __syncthreads();
-    for (int i = tid; i < k; i += FIN_THREADS) {
-      if (comp[q * k + i] == 0ull) continue;
-      int L = min(max(len[q * k + i], 1), max_len);
+    for (int i = tid; i < k; i += blockDim.x) {
+      if (comp[i] == 0ull) continue;
+      int L = min(max(len[i], 1), max_len);
       int b = (L - 1) / w;
-      atomicAdd(&h_cnt[b], 1);
-      atomicAdd(reinterpret_cast<unsigned long long*>(&h_sv[b]), (unsigned long long)L);
-      atomicAdd(reinterpret_cast<unsigned long long*>(&h_sv2[b]),
+      atomicAdd(&f.h_cnt[b], 1);
+      atomicAdd(reinterpret_cast<unsigned long long*>(&f.h_sv[b]), (unsigned long long)L);
+      atomicAdd(reinterpret_cast<unsigned long long*>(&f.h_sv2[b]),
                 (unsigned long long)((long long)L * L));
     }
   } else {
-    for (int b = tid; b < nbins; b += FIN_THREADS) {
-      h_cnt[b] = (int32_t)fb_cnt[b];
-      h_sv[b] = fb_sv[b];
-      h_sv2[b] = fb_sv2[b];
+    for (int b = tid; b < nbins; b += blockDim.x) {
+      f.h_cnt[b] = (int32_t)fb_cnt[b];
+      f.h_sv[b] = fb_sv[b];
+      f.h_sv2[b] = fb_sv2[b];
     }
   }
   __syncthreads();
   // ascending compaction of non-empty bins
-  for (int b0 = 0; b0 < nbins; b0 += FIN_THREADS) {
+  for (int b0 = 0; b0 < nbins; b0 += blockDim.x) {
     int b = b0 + tid;
-    int c = (b < nbins) ? h_cnt[b] : 0;
+    int c = (b < nbins) ? f.h_cnt[b] : 0;
     unsigned ball = __ballot_sync(0xffffffffu, c > 0);
     if (lane == 0) s_warp[warp] = __popc(ball);
     __syncthreads();
-    int off = s_base;
+    int off = s_misc[1];
     for (int ww = 0; ww < warp; ++ww) off += s_warp[ww];
     if (c > 0) {
       int pos = off + __popc(ball & ((1u << lane) - 1u));
-      long long D = h_sv2[b] + 2 * Iq * h_sv[b];
-      l_c[pos] = c;
-      l_D[pos] = D;
+      long long D = f.h_sv2[b] + 2 * Iq * f.h_sv[b];
+      f.l_c[pos] = c;
+      f.l_D[pos] = D;
       if (pos < P) {
         pbin[q * P + pos] = b;
         pcnt[q * P + pos] = c;
         pD[q * P + pos] = D;
-        if (psv) psv[q * P + pos] = h_sv[b];
+        if (psv) psv[q * P + pos] = f.h_sv[b];
       }
     }
     __syncthreads();
     if (tid == 0) {
       int add = 0;
-      for (int ww = 0; ww < FIN_THREADS / 32; ++ww) add += s_warp[ww];
-      s_base += add;
+      for (int ww = 0; ww < nw; ++ww) add += s_warp[ww];
+      s_misc[1] += add;
     }
     __syncthreads();
   }
-  const int np = s_base;
+  const int np = s_misc[1];
   if (warp == 0) {
-    double g = (np > 0) ? warp_gittins_exact(l_c, l_D, np, 0, (int)Iq, 0, 0, lane) : INFINITY;
+    double g = (np > 0) ? warp_gittins_exact(f.l_c, f.l_D, np, 0, (int)Iq, 0, 0, lane) : INFINITY;
     if (lane == 0) {
       G[q] = g;
       npts[q] = np;
@@ -334,20 +419,96 @@ k_finish(const uint64_t* __restrict__ comp, const int32_t* __restrict__ len, int
   }
 }
 
+__global__ void __launch_bounds__(MF_THREADS)
+k_finish(const uint64_t* __restrict__ comp, const int32_t* __restrict__ len, int64_t nq, int k,
+         int min_matches, int max_len, int nbins, const int32_t* __restrict__ I,
+         const int64_t* __restrict__ fb_cnt, const int64_t* __restrict__ fb_sv,
+         const int64_t* __restrict__ fb_sv2, int P, int32_t* __restrict__ npts,
+         int32_t* __restrict__ pbin, int32_t* __restrict__ pcnt, int64_t* __restrict__ pD,
+         int64_t* __restrict__ psv, uint8_t* __restrict__ used_fb, double* __restrict__ G) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ int s_misc[4], s_warp[MF_THREADS / 32];
+  const int64_t q = blockIdx.x;
+  finish_one(comp + q * k, len + q * k, k, q, min_matches, max_len, nbins, I[q], fb_cnt, fb_sv,
+             fb_sv2, P, npts, pbin, pcnt, pD, psv, used_fb, G, carve_finish(smem, nbins), s_misc,
+             s_warp);
+}
+
 int launch_finish(const uint64_t* comp, const int32_t* len, int64_t nq, int k, int min_matches,
                   int max_len, int nbins, const int32_t* I, const int64_t* fb_cnt,
                   const int64_t* fb_sv, const int64_t* fb_sv2, int P, int32_t* npts,
                   int32_t* pbin, int32_t* pcnt, int64_t* pD, int64_t* psv, uint8_t* used_fb,
                   double* G, cudaStream_t st) {
   if (nq <= 0) return SS_OK;
-  size_t smem = (size_t)nbins * (8 * 3 + 4 * 2);
+  size_t smem = finish_smem(nbins);
   if (smem > 200 * 1024) return set_error(SS_ERR_UNSUPPORTED, "nbins %d too large", nbins);
   if (smem > 48 * 1024)
     SS_CUDA_TRY(cudaFuncSetAttribute(k_finish, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   count_launch();
-  k_finish<<<(unsigned)nq, FIN_THREADS, smem, st>>>(comp, len, nq, k, min_matches, max_len, nbins,
-                                                    I, fb_cnt, fb_sv, fb_sv2, P, npts, pbin, pcnt,
-                                                    pD, psv, used_fb, G);
+  k_finish<<<(unsigned)nq, MF_THREADS, smem, st>>>(comp, len, nq, k, min_matches, max_len, nbins, I,
+                                                  fb_cnt, fb_sv, fb_sv2, P, npts, pbin, pcnt, pD,
+                                                  psv, used_fb, G);
+  SS_LAUNCH_CHECK();
+  return SS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// merge + finish fused (single-GPU round): per request, select the global
+// top-k from the similarity kernel's slices, then histogram/cost/Gittins,
+// without a global round trip of the neighbour lists in between.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(MF_THREADS)
+k_merge_finish(const uint64_t* __restrict__ partials, int nlists, int64_t nq, int k, int kpad,
+               const int32_t* __restrict__ bank_lens, int64_t head, int64_t gcap,
+               int64_t slot_offset, uint64_t* __restrict__ out_comp,
+               int32_t* __restrict__ out_len, int min_matches, int max_len, int nbins,
+               const int32_t* __restrict__ I, const int64_t* __restrict__ fb_cnt,
+               const int64_t* __restrict__ fb_sv, const int64_t* __restrict__ fb_sv2, int P,
+               int32_t* __restrict__ npts, int32_t* __restrict__ pbin, int32_t* __restrict__ pcnt,
+               int64_t* __restrict__ pD, int64_t* __restrict__ psv, uint8_t* __restrict__ used_fb,
+               double* __restrict__ G) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int M = nlists * k;
+  uint64_t* cand = reinterpret_cast<uint64_t*>(smem);      // [M]
+  uint64_t* sel = cand + M;                                // [kpad]
+  int32_t* cpay = reinterpret_cast<int32_t*>(sel + kpad);  // [M]
+  int32_t* spay = cpay + M;                                // [kpad]
+  __shared__ int hist[256];
+  __shared__ int s_misc[4], s_warp[MF_THREADS / 32];
+  const int64_t q = blockIdx.x;
+  load_candidates(partials, nullptr, nlists, nq, k, q, cand, cpay, bank_lens, head, gcap,
+                  slot_offset);
+  block_select_topk(cand, cpay, M, nlists, k, kpad, sel, spay, hist, s_misc);
+  resolve_lens(sel, spay, k, bank_lens, head, gcap, slot_offset);
+  for (int i = threadIdx.x; i < k; i += blockDim.x) {
+    if (out_comp) out_comp[q * k + i] = sel[i];
+    if (out_len) out_len[q * k + i] = sel[i] ? spay[i] : 0;
+  }
+  finish_one(sel, spay, k, q, min_matches, max_len, nbins, I[q], fb_cnt, fb_sv, fb_sv2, P, npts,
+             pbin, pcnt, pD, psv, used_fb, G,
+             carve_finish(smem + (((size_t)M * 12 + (size_t)kpad * 12 + 15) & ~(size_t)15), nbins),
+             s_misc, s_warp);
+}
+
+int launch_merge_finish(const uint64_t* partials, int nlists, int64_t nq, int k,
+                        const int32_t* bank_lens, int64_t head, int64_t gcap, int64_t slot_offset,
+                        uint64_t* out_comp, int32_t* out_len, int min_matches, int max_len,
+                        int nbins, const int32_t* I, const int64_t* fb_cnt, const int64_t* fb_sv,
+                        const int64_t* fb_sv2, int P, int32_t* npts, int32_t* pbin, int32_t* pcnt,
+                        int64_t* pD, int64_t* psv, uint8_t* used_fb, double* G, cudaStream_t st) {
+  if (nq <= 0) return SS_OK;
+  int kpad = 1;
+  while (kpad < k) kpad <<= 1;
+  const size_t smem = ((merge_smem(nlists, k, kpad) + 15) & ~(size_t)15) + finish_smem(nbins);
+  if (smem > 220 * 1024)
+    return set_error(SS_ERR_UNSUPPORTED, "merge+finish of %d lists x k=%d, %d bins exceeds smem",
+                     nlists, k, nbins);
+  SS_CUDA_TRY(cudaFuncSetAttribute(k_merge_finish, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem));
+  count_launch();
+  k_merge_finish<<<(unsigned)nq, MF_THREADS, smem, st>>>(
+      partials, nlists, nq, k, kpad, bank_lens, head, gcap, slot_offset, out_comp, out_len,
+      min_matches, max_len, nbins, I, fb_cnt, fb_sv, fb_sv2, P, npts, pbin, pcnt, pD, psv, used_fb, G);
   SS_LAUNCH_CHECK();
   return SS_OK;
 }

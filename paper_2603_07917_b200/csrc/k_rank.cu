@@ -54,6 +54,50 @@ k_rank_small(const double* __restrict__ G, const int64_t* __restrict__ ids, int 
   for (int i = threadIdx.x; i < n; i += blockDim.x) perm[i] = idx[i];
 }
 
+// ------------------------------------------------------- rank by counting --
+// n <= 8192: every thread owns one request and counts the requests that
+// precede it in the total order (G, id, index) -- a strict total order, so
+// the ranks form a permutation and perm[rank_i] = i is exact and stable.
+// Keys are staged through shared memory in 1024-entry tiles.
+constexpr int COUNT_MAX = 8192;
+
+// 8 lanes per request: lane t of a group compares against j = t, t+8, ...
+// (L1-resident loads), then the group sums its partial ranks with shuffles.
+constexpr int RC_LANES = 8;
+
+__global__ void __launch_bounds__(256)
+k_rank_count(const double* __restrict__ G, const int64_t* __restrict__ ids, int n,
+             int64_t* __restrict__ perm) {
+  __shared__ uint64_t sk[2048];
+  __shared__ int64_t sid[2048];
+  const int t = threadIdx.x & (RC_LANES - 1);
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) / RC_LANES;
+  const bool live = i < n;
+  const uint64_t ki = live ? f64_order(G[i]) : 0ull;
+  const int64_t ii = live ? (ids ? ids[i] : i) : 0;
+  int rank = 0;
+  for (int t0 = 0; t0 < n; t0 += 2048) {
+    const int m = min(2048, n - t0);
+    __syncthreads();
+    for (int j = threadIdx.x; j < m; j += blockDim.x) {
+      sk[j] = f64_order(G[t0 + j]);
+      sid[j] = ids ? ids[t0 + j] : t0 + j;
+    }
+    __syncthreads();
+    if (live) {
+#pragma unroll 8
+      for (int j = t; j < m; j += RC_LANES) {
+        const uint64_t kj = sk[j];
+        const int64_t ij = sid[j];
+        rank += (kj < ki) | ((kj == ki) & ((ij < ii) | ((ij == ii) & (t0 + j < i))));
+      }
+    }
+  }
+#pragma unroll
+  for (int o = RC_LANES / 2; o > 0; o >>= 1) rank += __shfl_xor_sync(0xffffffffu, rank, o);
+  if (live && t == 0) perm[rank] = i;
+}
+
 // ---------------------------------------------------------------- radix ----
 constexpr int RT_THREADS = 256;
 constexpr int RT_ITEMS = 8;
@@ -204,6 +248,12 @@ int64_t rank_workspace_bytes(int64_t n) {
 int launch_rank(const double* G, const int64_t* ids, int64_t n, int64_t* perm, void* ws,
                 int64_t ws_bytes, cudaStream_t st) {
   if (n <= 0) return SS_OK;
+  if (n <= COUNT_MAX) {
+    count_launch();
+    k_rank_count<<<(unsigned)((n * RC_LANES + 255) / 256), 256, 0, st>>>(G, ids, (int)n, perm);
+    SS_LAUNCH_CHECK();
+    return SS_OK;
+  }
   if (n <= SMALL_SORT_MAX) {
     int npad = 1;
     while (npad < n) npad <<= 1;

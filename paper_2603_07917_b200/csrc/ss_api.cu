@@ -88,6 +88,7 @@ struct ss_bank {
   float* inv = nullptr;
   int32_t* lens = nullptr;
   int64_t* seq = nullptr;
+  int32_t* len_cnt = nullptr;  // exact-length histogram of the window [65536]
   int* d_err = nullptr;
   void* ws = nullptr;
   size_t ws_bytes = 0;
@@ -213,12 +214,14 @@ int ss_bank_create(ss_bank_t** out, int32_t device, int64_t capacity, int32_t di
   else if ((e = cudaMalloc(&h->inv, (size_t)capacity * 4)) != cudaSuccess) fail(e);
   else if ((e = cudaMalloc(&h->lens, (size_t)capacity * 4)) != cudaSuccess) fail(e);
   else if ((e = cudaMalloc(&h->seq, (size_t)capacity * 8)) != cudaSuccess) fail(e);
+  else if ((e = cudaMalloc(&h->len_cnt, 65536 * 4)) != cudaSuccess) fail(e);
   else if ((e = cudaMalloc(&h->d_err, sizeof(int))) != cudaSuccess) fail(e);
   if (rc == SS_OK) {
     cudaMemset(h->emb, 0, (size_t)capacity * dim);
     cudaMemset(h->inv, 0xff, (size_t)capacity * 4);  // NaN: never matches
     cudaMemset(h->lens, 0, (size_t)capacity * 4);
     cudaMemset(h->seq, 0xff, (size_t)capacity * 8);  // -1: empty slot
+    cudaMemset(h->len_cnt, 0, 65536 * 4);
     cudaMemset(h->d_err, 0, sizeof(int));
     e = cudaDeviceSynchronize();
     if (e != cudaSuccess) fail(e);
@@ -238,6 +241,7 @@ int ss_bank_destroy(ss_bank_t* h) {
   cudaFree(h->inv);
   cudaFree(h->lens);
   cudaFree(h->seq);
+  cudaFree(h->len_cnt);
   cudaFree(h->d_err);
   cudaFree(h->ws);
   delete h;
@@ -251,7 +255,7 @@ int ss_bank_push(ss_bank_t* h, const int8_t* emb, const float* inv_norm, const i
     return set_error(SS_ERR_ARG, "bank_push on a shard: use ss_bank_write with the global head");
   if (n == 0) return SS_OK;
   int64_t skip = n > h->cap ? n - h->cap : 0;
-  int rc = launch_bank_write(h->emb, h->inv, h->lens, h->seq, h->dim, emb, inv_norm, lens, nullptr,
+  int rc = launch_bank_write(h->emb, h->inv, h->lens, h->seq, h->len_cnt, h->dim, emb, inv_norm, lens, nullptr,
                              nullptr, n, h->head, h->cap, skip, h->d_err, (cudaStream_t)stream);
   if (rc) return rc;
   h->head += n;
@@ -261,7 +265,7 @@ int ss_bank_push(ss_bank_t* h, const int8_t* emb, const float* inv_norm, const i
 int ss_bank_write(ss_bank_t* h, const int8_t* emb, const float* inv_norm, const int32_t* lens,
                   const int64_t* seq, const int64_t* local_slot, int64_t n, void* stream) {
   if (!h || n < 0 || !seq || !local_slot) return set_error(SS_ERR_ARG, "bank_write: bad args");
-  return launch_bank_write(h->emb, h->inv, h->lens, h->seq, h->dim, emb, inv_norm, lens, seq,
+  return launch_bank_write(h->emb, h->inv, h->lens, h->seq, h->len_cnt, h->dim, emb, inv_norm, lens, seq,
                            local_slot, n, 0, h->cap, 0, h->d_err, (cudaStream_t)stream);
 }
 
@@ -310,7 +314,7 @@ int ss_bank_fallback_hist(ss_bank_t* h, int32_t max_len, int32_t nbins, int64_t*
                           int64_t* sv2, void* stream) {
   if (!h) return set_error(SS_ERR_ARG, "null bank");
   if (int rc = check_bins(max_len, nbins)) return rc;
-  return launch_fallback_hist(h->lens, h->seq, h->cap, max_len, nbins, cnt, sv, sv2,
+  return launch_fallback_hist(h->len_cnt, max_len, nbins, cnt, sv, sv2,
                               (cudaStream_t)stream);
 }
 
@@ -453,13 +457,22 @@ static int round_impl(ss_bank* h, const int8_t* q, const float* q_inv, const int
   uint64_t* comp = reinterpret_cast<uint64_t*>(ws + L.comp);
   int32_t* len = reinterpret_cast<int32_t*>(ws + L.len);
   int64_t* fb = reinterpret_cast<int64_t*>(ws + L.fb);
-  // the top-k partials live after the round buffers
-  int rc = topk_impl(h, q, q_inv, nq, k, theta, algo, comp, len, base + L.end, st);
+  // stage 1: similarity kernel writes per-slice partial top-k lists, which
+  // live after the round buffers; merge + stages 1b-3 run fused per request
+  if (k < 1 || k > 256) return set_error(SS_ERR_ARG, "k must lie in [1, 256], got %d", k);
+  TopkArgs a{q, q_inv, nq, h->emb, h->inv, h->cap, h->dim, k, theta, h->head, h->gcap,
+             h->slot_offset};
+  int slices = 1;
+  if (int rc = topk_plan(h, a, algo, slices)) return rc;
+  uint64_t* partials = reinterpret_cast<uint64_t*>((char*)h->ws + base + L.end);
+  int rc = (algo == SS_ALGO_TCGEN05) ? launch_topk_tc(a, partials, slices, st)
+                                     : launch_topk_scan(a, partials, slices, st);
   if (rc) return rc;
-  rc = launch_fallback_hist(h->lens, h->seq, h->cap, max_len, nbins, fb, fb + nbins, fb + 2 * nbins, st);
+  rc = launch_fallback_hist(h->len_cnt, max_len, nbins, fb, fb + nbins, fb + 2 * nbins, st);
   if (rc) return rc;
-  rc = launch_finish(comp, len, nq, k, min_matches, max_len, nbins, input_len, fb, fb + nbins,
-                     fb + 2 * nbins, P, npts, pbin, pcnt, pD, nullptr, used_fb, G, st);
+  rc = launch_merge_finish(partials, slices, nq, k, h->lens, h->head, h->gcap, h->slot_offset, comp,
+                           len, min_matches, max_len, nbins, input_len, fb, fb + nbins,
+                           fb + 2 * nbins, P, npts, pbin, pcnt, pD, nullptr, used_fb, G, st);
   if (rc) return rc;
   return launch_rank(G, ids, nq, perm, ws + L.rank, (int64_t)rank_workspace_bytes(nq), st);
 }

@@ -24,14 +24,13 @@ int launch_cost_dist(int kind, double w_in, double w_out, const double* I, const
                      cudaStream_t st);
 
 // bank maintenance (k_bank.cu)
-int launch_bank_write(int8_t* emb, float* inv, int32_t* lens, int64_t* seq, int dim,
-                      const int8_t* src_emb, const float* src_inv, const int32_t* src_lens,
-                      const int64_t* src_seq, const int64_t* src_slot, int64_t n,
-                      int64_t first_seq, int64_t capacity, int64_t skip, int* err,
+int launch_bank_write(int8_t* emb, float* inv, int32_t* lens, int64_t* seq, int32_t* len_cnt,
+                      int dim, const int8_t* src_emb, const float* src_inv,
+                      const int32_t* src_lens, const int64_t* src_seq, const int64_t* src_slot,
+                      int64_t n, int64_t first_seq, int64_t capacity, int64_t skip, int* err,
                       cudaStream_t st);
-int launch_fallback_hist(const int32_t* lens, const int64_t* seq, int64_t capacity,
-                         int max_len, int nbins, int64_t* cnt, int64_t* sv, int64_t* sv2,
-                         cudaStream_t st);
+int launch_fallback_hist(const int32_t* len_cnt, int max_len, int nbins, int64_t* cnt,
+                         int64_t* sv, int64_t* sv2, cudaStream_t st);
 
 // similarity + top-k
 struct TopkArgs {
@@ -62,6 +61,12 @@ int launch_finish(const uint64_t* comp, const int32_t* len, int64_t nq, int k,
                   const int64_t* fb_cnt, const int64_t* fb_sv, const int64_t* fb_sv2, int P,
                   int32_t* npts, int32_t* pbin, int32_t* pcnt, int64_t* pD, int64_t* psv,
                   uint8_t* used_fb, double* G, cudaStream_t st);
+int launch_merge_finish(const uint64_t* partials, int nlists, int64_t nq, int k,
+                        const int32_t* bank_lens, int64_t head, int64_t gcap, int64_t slot_offset,
+                        uint64_t* out_comp, int32_t* out_len, int min_matches, int max_len,
+                        int nbins, const int32_t* I, const int64_t* fb_cnt, const int64_t* fb_sv,
+                        const int64_t* fb_sv2, int P, int32_t* npts, int32_t* pbin, int32_t* pcnt,
+                        int64_t* pD, int64_t* psv, uint8_t* used_fb, double* G, cudaStream_t st);
 int launch_refresh(int64_t n, const int32_t* I, const int32_t* g_new, int32_t* bucket_io,
                    int bucket_size, const int32_t* npts, const int32_t* pcnt,
                    const int64_t* pD, int P, double* G_io, uint8_t* refreshed, int force,

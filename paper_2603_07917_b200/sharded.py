@@ -1,0 +1,164 @@
+"""Multi-GPU scheduling round over a row-sharded history bank.
+
+One process per GPU (torch.distributed, NCCL over NVLink on the box; gloo in
+the CPU tests).  The global FIFO ring of ``global_capacity`` slots is split
+into contiguous shards: rank r owns global slots [r*L, (r+1)*L), L =
+global_capacity / world.  Every rank owns its own queue of pending requests
+(one scheduler per GPU, "multiple concurrent schedulers"), so a
+round is weak-scaled: each rank contributes nq requests.
+
+Per round (only stage 1 is partitioned; stages 2-4 run on the queue owner):
+  1. all-gather the queries of every rank's queue            (NCCL all_gather)
+  2. local top-k of all world*nq queries against the local shard, fused in
+     the tcgen05 kernel, with the candidates' lengths attached (ss_topk)
+  3. exchange: rank r receives, from every shard, the k candidates of its own
+     queries                                                   (NCCL all_to_all)
+  4. merge world x k candidates per query into the global top-k (ss_merge_topk)
+  5. fallback histogram: per-shard exact integer histograms summed
+                                                               (NCCL all_reduce)
+  6. histogram -> cost -> Gittins (ss_finish) and rank (ss_rank) for the queue.
+Composites carry the global ring rank (slot - head) mod C, so tie-breaking by
+insertion_seq is identical to the single-GPU round.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+__all__ = ["ShardPlan", "gather_queries", "exchange_candidates", "allreduce_hist",
+           "ShardedHistory", "ShardedScheduler"]
+
+
+@dataclass(frozen=True)
+class ShardPlan:
+    """Contiguous row sharding of a global ring of ``global_capacity`` slots."""
+
+    global_capacity: int
+    world: int
+    rank: int
+
+    def __post_init__(self):
+        if self.global_capacity % self.world:
+            raise ValueError("global_capacity must be divisible by the world size")
+
+    @property
+    def local_capacity(self) -> int:
+        return self.global_capacity // self.world
+
+    @property
+    def slot_offset(self) -> int:
+        return self.rank * self.local_capacity
+
+    def route(self, head: int, n: int):
+        """Records head..head+n-1 (only the newest global_capacity survive):
+        (index into the batch, seq, local slot) of those landing on this rank."""
+        first = max(0, n - self.global_capacity)
+        idx = np.arange(first, n, dtype=np.int64)
+        seq = head + idx
+        gslot = seq % self.global_capacity
+        mine = (gslot // self.local_capacity) == self.rank
+        return idx[mine], seq[mine], gslot[mine] - self.slot_offset
+
+
+def gather_queries(q: torch.Tensor, q_inv: torch.Tensor, group=None):
+    """All-gather every rank's queue: -> ([world*nq, dim] int8, [world*nq] f32)."""
+    world = dist.get_world_size(group)
+    nq, dim = q.shape
+    q_all = torch.empty((world * nq, dim), dtype=q.dtype, device=q.device)
+    qi_all = torch.empty(world * nq, dtype=q_inv.dtype, device=q_inv.device)
+    dist.all_gather_into_tensor(q_all, q.contiguous(), group=group)
+    dist.all_gather_into_tensor(qi_all, q_inv.contiguous(), group=group)
+    return q_all, qi_all
+
+
+def exchange_candidates(comp: torch.Tensor, ln: torch.Tensor, group=None):
+    """comp/ln [world*nq, k] (this shard's candidates for every rank's queries)
+    -> [world, nq, k]: every shard's candidates for THIS rank's queries."""
+    world = dist.get_world_size(group)
+    out_c = torch.empty_like(comp)
+    out_l = torch.empty_like(ln)
+    dist.all_to_all_single(out_c, comp.contiguous(), group=group)
+    dist.all_to_all_single(out_l, ln.contiguous(), group=group)
+    nq = comp.shape[0] // world
+    return out_c.reshape(world, nq, -1), out_l.reshape(world, nq, -1)
+
+
+def allreduce_hist(fb: torch.Tensor, group=None) -> torch.Tensor:
+    """Exact sum of per-shard integer histograms (int64)."""
+    dist.all_reduce(fb, op=dist.ReduceOp.SUM, group=group)
+    return fb
+
+
+class ShardedHistory:
+    """This rank's shard of the global history ring, on its own GPU."""
+
+    def __init__(self, global_capacity: int, dim: int = 384, group=None):
+        from .history import HistoryWindow
+
+        self.group = group
+        self.plan = ShardPlan(int(global_capacity), dist.get_world_size(group),
+                              dist.get_rank(group))
+        self.window = HistoryWindow(self.plan.local_capacity, dim,
+                                    global_capacity=self.plan.global_capacity,
+                                    slot_offset=self.plan.slot_offset)
+        self.head = 0
+
+    def push(self, emb, lens) -> None:
+        """Append records (the same batch on every rank); each rank stores the
+        rows that land in its shard.  Evicts the oldest globally."""
+        n = int(lens.shape[0])
+        idx, seq, slot = self.plan.route(self.head, n)
+        if idx.size:
+            ti = torch.as_tensor(idx, device=emb.device if isinstance(emb, torch.Tensor) else "cuda")
+            e = torch.as_tensor(emb, device="cuda")[ti]
+            ln = torch.as_tensor(lens, device="cuda")[ti]
+            self.window.write(e, ln, torch.as_tensor(seq, device="cuda"),
+                              torch.as_tensor(slot, device="cuda"))
+        self.head += n
+        self.window.set_head(self.head)
+
+
+class ShardedScheduler:
+    """The scheduling round of SageScheduler, with stage 1 sharded."""
+
+    def __init__(self, history: ShardedHistory, cfg):
+        self.h = history
+        self.cfg = cfg
+        self.group = history.group
+        self._ws = None
+
+    def schedule_round(self, q, q_inv, input_len, ids=None):
+        from . import _lib
+        from .scheduler import rank as _rank
+
+        c = self.cfg
+        nq = q.shape[0]
+        q_all, qi_all = gather_queries(q, q_inv, self.group)                    # 1
+        comp_all, len_all = self.h.window.topk(q_all, qi_all, c.k, c.theta, c.algo)  # 2
+        comp_x, len_x = exchange_candidates(comp_all, len_all, self.group)      # 3
+        world = comp_x.shape[0]
+        comp = torch.empty((nq, c.k), dtype=torch.int64, device="cuda")
+        ln = torch.empty((nq, c.k), dtype=torch.int32, device="cuda")
+        _lib.call("ss_merge_topk", _lib.ptr(comp_x), _lib.ptr(len_x), world, nq, c.k,
+                  _lib.ptr(comp), _lib.ptr(ln), _lib.stream_ptr())              # 4
+        fb = allreduce_hist(self.h.window.fallback_hist(c.max_len, c.nbins), self.group)  # 5
+        P = c.nbins
+        out = dict(npts=torch.zeros(nq, dtype=torch.int32, device="cuda"),
+                   pbin=torch.zeros((nq, P), dtype=torch.int32, device="cuda"),
+                   pcnt=torch.zeros((nq, P), dtype=torch.int32, device="cuda"),
+                   pD=torch.zeros((nq, P), dtype=torch.int64, device="cuda"),
+                   used_fb=torch.zeros(nq, dtype=torch.uint8, device="cuda"),
+                   G=torch.empty(nq, dtype=torch.float64, device="cuda"))
+        I = torch.as_tensor(input_len, device="cuda").to(torch.int32)
+        _lib.call("ss_finish", _lib.ptr(comp), _lib.ptr(ln), nq, c.k, c.min_matches, c.max_len,
+                  c.nbins, _lib.ptr(I), _lib.ptr(fb[0]), _lib.ptr(fb[1]), _lib.ptr(fb[2]), P,
+                  _lib.ptr(out["npts"]), _lib.ptr(out["pbin"]), _lib.ptr(out["pcnt"]),
+                  _lib.ptr(out["pD"]), None, _lib.ptr(out["used_fb"]), _lib.ptr(out["G"]),
+                  _lib.stream_ptr())                                            # 6
+        perm = _rank(out["G"], None if ids is None else torch.as_tensor(ids, device="cuda"))
+        out["comp"], out["len"] = comp, ln
+        return perm, out["G"], out

@@ -360,3 +360,36 @@ def test_rank_bit_exact(cuda, n):
     assert np.array_equal(perm, O.rank(G, ids))
     perm = rank(_t(G)).cpu().numpy()
     assert np.array_equal(perm, O.rank(G, np.arange(n)))
+
+
+# ---------------------------------------------------- sharded round (N=1) ---
+def test_sharded_round_world1_equals_single_gpu(cuda):
+    """The multi-GPU round (query all-gather, candidate all-to-all, merge,
+    histogram all-reduce) run as a 1-rank NCCL group equals the fused
+    single-GPU round bit for bit."""
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_2603_07917_b200.scheduler import RoundConfig, SageScheduler
+    from paper_2603_07917_b200.sharded import ShardedHistory, ShardedScheduler
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda:0"))
+    try:
+        n, dim, nq = 20_000, 384, 200
+        emb, lens, _, _ = O.make_bank(n + nq, dim, 50, 9)
+        cfg = RoundConfig(k=32, theta=0.8, nbins=64)
+        sh = ShardedHistory(n, dim)
+        sh.push(torch.as_tensor(emb[:n], device="cuda"), torch.as_tensor(lens[:n], device="cuda"))
+        q, qi = emb[n:], O.inv_norm(emb[n:])
+        I = np.random.default_rng(0).integers(1, 4097, nq).astype(np.int32)
+        ids = np.arange(nq)
+        p1, G1, _ = ShardedScheduler(sh, cfg).schedule_round(_t(q), _t(qi), _t(I), _t(ids))
+        w, *_ = _bank(n, dim, 50, 9, nq)
+        p0, G0, _ = SageScheduler(w, cfg).schedule_round(_t(q), _t(qi), _t(I), _t(ids))
+        assert torch.equal(G1, G0) and torch.equal(p1, p0)
+    finally:
+        dist.destroy_process_group()
