@@ -251,7 +251,8 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
 k_topk_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmB,
           const float* __restrict__ q_inv, int64_t nq, const float* __restrict__ inv,
           int64_t n_rows, int nkb, int stages, int k, float theta, int64_t hmod, int64_t gcap,
-          int64_t slot_offset, int64_t tiles_per_slice, uint64_t* __restrict__ partials, int dbg) {
+          int64_t slot_offset, int64_t tiles_per_slice, uint64_t* __restrict__ partials, int dbg,
+          uint32_t* __restrict__ gthr) {
   constexpr int BN_CTA = tc::BN / CG;          // B rows this CTA loads per tile
   constexpr int B_STAGE = BN_CTA * tc::BK;     // bytes per K-block stage per CTA
   extern __shared__ uint8_t smem_raw[];
@@ -402,8 +403,11 @@ k_topk_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUten
       }
       __syncwarp();
       if (t + 1 < ntiles) fetch_iw(t + 1);  // overlaps this tile's epilogue
+      // the tightest k-th-key lower bound any slice has proven for this query
+      const uint32_t gv = (gthr != nullptr && q < nq) ? __ldcg(gthr + q) : 0u;
       mbar_wait(&tfull[acc], (t >> 1) & 1);
       tc_fence_after();
+      if (gv) thr = fmaxf(thr, s_threshold(f32_unorder(gv), iq));
       const uint32_t tbase = tmem + ((uint32_t)(quarter * 32) << 16) + acc * tc::BN;
       auto chunk = [&](const int (&v)[32], const int c) {
         if (dbg & 4) return;  // debug: TMEM drain only
@@ -451,10 +455,12 @@ k_topk_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUten
                   if (++hcnt == k) {
                     hroot = tc_heapify(heap, k);
                     thr = fmaxf(thr, s_threshold(comp_key(hroot), iq));
+                    if (gthr) atomicMax(gthr + q, (uint32_t)(hroot >> 32));
                   }
                 } else if (comp > hroot) {
                   hroot = tc_heap_replace(heap, k, comp);
                   thr = fmaxf(thr, s_threshold(comp_key(hroot), iq));
+                  if (gthr) atomicMax(gthr + q, (uint32_t)(hroot >> 32));
                 }
               }
             }
@@ -608,10 +614,11 @@ static int launch_cg(const TopkArgs& a, uint64_t* partials, int n_slices, cudaSt
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   const int dbg = env_int("SS_TC_DEBUG", 0) | (tc_prefetch() << 8);
+  if (a.gthr) SS_CUDA_TRY(cudaMemsetAsync(a.gthr, 0, (size_t)a.nq * sizeof(uint32_t), st));
   count_launch();
   SS_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_topk_tc<CG>, mq, mb, a.q_inv, a.nq, a.inv, a.n_rows,
                                  a.dim / tc::BK, stages, a.k, a.theta, a.head % a.gcap, a.gcap,
-                                 a.slot_offset, tps, partials, dbg));
+                                 a.slot_offset, tps, partials, dbg, a.gthr));
   return SS_OK;
 }
 

@@ -92,7 +92,31 @@ struct ss_bank {
   int* d_err = nullptr;
   void* ws = nullptr;
   size_t ws_bytes = 0;
+  uint32_t* gthr = nullptr;  // per-query shared k-th-key bound for the top-k slices
+  int64_t gthr_cap = 0;
 };
+
+// grow-on-demand (call once outside CUDA-graph capture); nullptr on failure
+// simply disables the cross-slice threshold sharing
+static uint32_t* gthr_reserve(ss_bank* h, int64_t nq) {
+  // Sharing max(slice roots) was measured to give no pruning (slices advance
+  // in lockstep, so the max of their k-th keys ~ each one's); kept behind
+  // SS_TC_GTHR=1 as an experiment knob.
+  static const bool on = getenv("SS_TC_GTHR") && atoi(getenv("SS_TC_GTHR")) == 1;
+  if (!on) return nullptr;
+  if (nq <= h->gthr_cap) return h->gthr;
+  if (h->gthr) cudaFree(h->gthr);
+  h->gthr = nullptr;
+  h->gthr_cap = 0;
+  int64_t want = nq + nq / 4 + 64;
+  if (cudaMalloc(&h->gthr, (size_t)want * sizeof(uint32_t)) != cudaSuccess) {
+    cudaGetLastError();
+    h->gthr = nullptr;
+    return nullptr;
+  }
+  h->gthr_cap = want;
+  return h->gthr;
+}
 
 static int ws_reserve(ss_bank* h, size_t bytes) {
   if (bytes <= h->ws_bytes) return SS_OK;
@@ -244,6 +268,7 @@ int ss_bank_destroy(ss_bank_t* h) {
   cudaFree(h->len_cnt);
   cudaFree(h->d_err);
   cudaFree(h->ws);
+  cudaFree(h->gthr);
   delete h;
   return SS_OK;
 }
@@ -347,6 +372,7 @@ static int topk_impl(ss_bank* h, const int8_t* q, const float* q_inv, int64_t nq
   if (nq == 0) return SS_OK;
   TopkArgs a{q, q_inv, nq, h->emb, h->inv, h->cap, h->dim, k, theta, h->head, h->gcap,
              h->slot_offset};
+  a.gthr = gthr_reserve(h, nq);
   int slices = 1;
   if (int rc = topk_plan(h, a, algo, slices)) return rc;
   size_t need = ws_offset + align_up((size_t)slices * nq * k * 8);
@@ -372,6 +398,7 @@ int ss_topk_partials(ss_bank_t* h, const int8_t* q, const float* q_inv, int64_t 
   if (k < 1 || k > 256 || nq < 0) return set_error(SS_ERR_ARG, "topk_partials: bad k/nq");
   TopkArgs a{q, q_inv, nq, h->emb, h->inv, h->cap, h->dim, k, theta, h->head, h->gcap,
              h->slot_offset};
+  a.gthr = gthr_reserve(h, nq);
   int slices = 1;
   if (int rc = topk_plan(h, a, algo, slices)) return rc;
   if (slices > max_slices) slices = max_slices;
@@ -462,6 +489,7 @@ static int round_impl(ss_bank* h, const int8_t* q, const float* q_inv, const int
   if (k < 1 || k > 256) return set_error(SS_ERR_ARG, "k must lie in [1, 256], got %d", k);
   TopkArgs a{q, q_inv, nq, h->emb, h->inv, h->cap, h->dim, k, theta, h->head, h->gcap,
              h->slot_offset};
+  a.gthr = gthr_reserve(h, nq);
   int slices = 1;
   if (int rc = topk_plan(h, a, algo, slices)) return rc;
   uint64_t* partials = reinterpret_cast<uint64_t*>((char*)h->ws + base + L.end);

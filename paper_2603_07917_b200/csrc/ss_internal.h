@@ -44,6 +44,10 @@ struct TopkArgs {
   int k;
   float theta;
   int64_t head, gcap, slot_offset;  // rel = (slot_offset + j - head) mod gcap
+  // optional [nq] scratch: per-query best known lower bound of the global k-th
+  // key (orderable bits), shared by all slices so each slice filters with the
+  // tightest threshold any slice has proven
+  uint32_t* gthr = nullptr;
 };
 int launch_topk_scan(const TopkArgs& a, uint64_t* partials, int n_slices, cudaStream_t st);
 int topk_scan_slices(const TopkArgs& a, int device);

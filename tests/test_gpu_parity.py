@@ -350,6 +350,47 @@ def test_refresh_bit_exact(cuda):
     assert (dG == -1.0).all() and int(ref_flag.sum()) == 0
 
 
+def test_c3_refresh_storm_full_size(cuda):
+    """BASELINE configs[2]: 200k running+pending requests, 512-bin cost laws
+    (from 64 length draws each), index recompute + full re-rank.  Laws and G
+    bit-exact on a 20k-request sample vs the oracle; the full ranking is
+    exactly the (G, id) order of the 200k indices."""
+    from paper_2603_07917_b200 import _lib
+    from paper_2603_07917_b200.scheduler import rank
+    n, nbins, k = 200_000, 512, 64
+    rng = np.random.default_rng(31)
+    lens = np.clip(np.rint(np.exp(rng.normal(5.5, 0.8, (n, k)))), 1, 2048).astype(np.int32)
+    I = rng.integers(1, 4097, n).astype(np.int32)
+    g = np.where(rng.random(n) < 0.4, rng.integers(0, 2049, n), 0).astype(np.int32)
+    d = "cuda"
+    comp = torch.ones((n, k), dtype=torch.int64, device=d)  # every draw is a "neighbour"
+    fb = torch.zeros((3, nbins), dtype=torch.int64, device=d)
+    npts = torch.zeros(n, dtype=torch.int32, device=d)
+    pbin = torch.zeros((n, nbins), dtype=torch.int32, device=d)
+    pcnt = torch.zeros((n, nbins), dtype=torch.int32, device=d)
+    pD = torch.zeros((n, nbins), dtype=torch.int64, device=d)
+    G = torch.zeros(n, dtype=torch.float64, device=d)
+    dl, dI, dg = _t(lens), _t(I), _t(g)
+    P = lambda t: t.data_ptr()  # noqa: E731
+    _lib.call("ss_finish", P(comp), P(dl), n, k, 1, 2048, nbins, P(dI), P(fb[0]), P(fb[1]),
+              P(fb[2]), nbins, P(npts), P(pbin), P(pcnt), P(pD), None, None, P(G),
+              _lib.stream_ptr())
+    bucket = torch.zeros(n, dtype=torch.int32, device=d)
+    _lib.call("ss_refresh", n, P(dI), P(dg), P(bucket), 200, P(npts), P(pcnt), P(pD), nbins,
+              P(G), None, 1, _lib.stream_ptr())
+    ids = _t(np.arange(n, dtype=np.int64))
+    perm = rank(G, ids).cpu().numpy()
+    Gh = G.cpu().numpy()
+    assert np.array_equal(perm, O.rank(Gh, np.arange(n)))
+    sample = rng.choice(n, 20_000, replace=False)
+    np_, pc, pd_ = npts.cpu().numpy(), pcnt.cpu().numpy(), pD.cpu().numpy()
+    for i in sample:
+        bins, c, D = O.hist_to_points(*O.bin_hist(lens[i], 2048, nbins), I[i])
+        assert np_[i] == c.size
+        assert np.array_equal(pc[i, :c.size], c) and np.array_equal(pd_[i, :c.size], D)
+        assert Gh[i] == O.gittins_points(c, D, int(I[i]), int(g[i])), i
+
+
 @pytest.mark.parametrize("n", [1, 7, 1024, 4096, 4097, 200_000])
 def test_rank_bit_exact(cuda, n):
     from paper_2603_07917_b200.scheduler import rank
