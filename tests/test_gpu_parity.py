@@ -350,6 +350,80 @@ def test_refresh_bit_exact(cuda):
     assert (dG == -1.0).all() and int(ref_flag.sum()) == 0
 
 
+def test_c5_replay_rolling_inserts_bit_exact(cuda):
+    """BASELINE configs[4] at test scale: trace replay with rolling bank inserts
+    (completions evict the oldest records), admission predict, bucket
+    refreshes and a full re-rank every round -- G and the order bit-exact vs an
+    independent numpy replica of the same loop over the oracle."""
+    from paper_2603_07917_b200.history import HistoryWindow
+    from paper_2603_07917_b200.replay import Trace, replay
+    from paper_2603_07917_b200.scheduler import RoundConfig
+    cap, dim, ntr = 3000, 128, 1500
+    emb, lens, _, _ = O.make_bank(cap + ntr, dim, 40, 77)
+    rng = np.random.default_rng(78)
+    tr = Trace(emb=emb[cap:], inv=O.inv_norm(emb[cap:]),
+               input_len=rng.integers(1, 4097, ntr).astype(np.int32),
+               true_len=np.clip(lens[cap:], 1, 600).astype(np.int32))
+    cfg = RoundConfig(k=16, theta=0.8, min_matches=5, max_len=2048, nbins=64)
+    A, TOK, B, R = 64, 40, 48, 30
+    w = HistoryWindow(cap, dim)
+    w.push(emb[:cap], lens[:cap])
+
+    # ---- numpy replica ----
+    bank_e = list(emb[:cap])
+    bank_l = list(lens[:cap])
+    st = {}  # rid -> dict(c, D, I, g, bucket, G)
+    running = []
+    nxt = 0
+    expected = []
+    for r in range(R):
+        done = []
+        for rid in running:
+            st[rid]["g"] += TOK
+            if st[rid]["g"] >= tr.true_len[rid]:
+                done.append(rid)
+        for rid in done:
+            bank_e.append(tr.emb[rid])
+            bank_l.append(tr.true_len[rid])
+            del st[rid]
+        bank_e, bank_l = bank_e[-cap:], bank_l[-cap:]
+        head = cap + sum(1 for _ in ())  # seq only matters relatively
+        n_new = min(A, ntr - nxt, 10_000)
+        be = np.array(bank_e)
+        bl = np.array(bank_l)
+        seq = np.arange(len(bank_e))
+        if n_new:
+            ids = np.arange(nxt, nxt + n_new)
+            keys = O.scores(tr.emb[ids], tr.inv[ids], be, O.inv_norm(be))
+            res = O.predict_round(keys, seq, bl, tr.input_len[ids], cfg.k, cfg.theta,
+                                  cfg.min_matches, cfg.max_len, cfg.nbins, window_lens=bl)
+            for rid, x in zip(ids, res):
+                st[int(rid)] = dict(c=x["c"], D=x["D"], I=int(tr.input_len[rid]), g=0, bucket=0,
+                                    G=x["G"])
+            nxt += n_new
+        act = np.array(sorted(st), dtype=np.int64)
+        for rid in act:
+            s = st[int(rid)]
+            if s["g"] // 200 > s["bucket"]:
+                s["G"] = O.gittins_points(s["c"], s["D"], s["I"], s["g"])
+                s["bucket"] = s["g"] // 200
+        G = np.array([st[int(i)]["G"] for i in act])
+        perm = O.rank(G, act)
+        running = [int(act[p]) for p in perm[:B]]
+        expected.append((act, G, perm))
+        del head
+
+    got = []
+    stats = replay(w, tr, cfg, A, TOK, B, max_active=2048, rounds=R,
+                   on_round=lambda r, info: got.append(info))
+    assert stats.completed > 50 and stats.refreshed > 20
+    assert len(got) == len(expected)
+    for (act, G, perm), info in zip(expected, got):
+        assert np.array_equal(info["active_ids"], act)
+        assert np.array_equal(info["G"], G)
+        assert np.array_equal(info["perm"], perm)
+
+
 def test_c3_refresh_storm_full_size(cuda):
     """BASELINE configs[2]: 200k running+pending requests, 512-bin cost laws
     (from 64 length draws each), index recompute + full re-rank.  Laws and G
