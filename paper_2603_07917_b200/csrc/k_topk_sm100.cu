@@ -252,7 +252,7 @@ k_topk_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUten
           const float* __restrict__ q_inv, int64_t nq, const float* __restrict__ inv,
           int64_t n_rows, int nkb, int stages, int k, float theta, int64_t hmod, int64_t gcap,
           int64_t slot_offset, int64_t tiles_per_slice, uint64_t* __restrict__ partials, int dbg,
-          uint32_t* __restrict__ gthr) {
+          uint32_t* __restrict__ grth, int rshare) {
   constexpr int BN_CTA = tc::BN / CG;          // B rows this CTA loads per tile
   constexpr int B_STAGE = BN_CTA * tc::BK;     // bytes per K-block stage per CTA
   extern __shared__ uint8_t smem_raw[];
@@ -370,6 +370,8 @@ k_topk_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUten
     const float iq = (q < nq) ? q_inv[q] : __int_as_float(0x7fc00000);
     // per-query heap state in registers (see topk_heap.cuh for the invariant)
     int hcnt = 0;
+    uint32_t rtop[4] = {0u, 0u, 0u, 0u};  // this slice's best R keys (orderable), descending
+    uint32_t bnd_next = 0u;
     uint64_t hroot = 0;
     uint64_t* heap = s_heap + qrow;
     float* wiw = s_iw + ew * 2 * tc::BN;  // double-buffered per warp
@@ -403,11 +405,15 @@ k_topk_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUten
       }
       __syncwarp();
       if (t + 1 < ntiles) fetch_iw(t + 1);  // overlaps this tile's epilogue
-      // the tightest k-th-key lower bound any slice has proven for this query
-      const uint32_t gv = (gthr != nullptr && q < nq) ? __ldcg(gthr + q) : 0u;
+      // cross-slice bound: every slice publishes the R-th best key it has seen
+      // (R = ceil(k / slices)); once all have, the union holds >= k rows at or
+      // above the minimum of those, so the global k-th key is >= it
+      // (maintained by the publishers in gmin[q]; loaded one tile ahead)
+      const uint32_t bnd = bnd_next;
+      if (rshare && q < nq && t + 1 < ntiles) bnd_next = __ldcg(grth + q);
       mbar_wait(&tfull[acc], (t >> 1) & 1);
       tc_fence_after();
-      if (gv) thr = fmaxf(thr, s_threshold(f32_unorder(gv), iq));
+      if (bnd) thr = fmaxf(thr, s_threshold(f32_unorder(bnd), iq));
       const uint32_t tbase = tmem + ((uint32_t)(quarter * 32) << 16) + acc * tc::BN;
       auto chunk = [&](const int (&v)[32], const int c) {
         if (dbg & 4) return;  // debug: TMEM drain only
@@ -447,6 +453,30 @@ k_topk_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUten
             {
               const float key = __fmul_rn(sl[j], iq);
               if (key >= theta) {
+                if (rshare) {  // this slice's top-R keys; publish the R-th when it rises
+                  uint32_t x = f32_order(key);
+                  auto rth = [&]() {
+                    return rshare == 1 ? rtop[0] : rshare == 2 ? rtop[1] : rshare == 3 ? rtop[2] : rtop[3];
+                  };
+                  const uint32_t old = rth();
+#pragma unroll
+                  for (int i = 0; i < 4; ++i) {
+                    if (i < rshare) {
+                      const uint32_t hi = max(rtop[i], x);
+                      x = min(rtop[i], x);
+                      rtop[i] = hi;
+                    }
+                  }
+                  const uint32_t now = rth();
+                  if (now != old) {  // publish, then refresh gmin[q] = min over slices
+                    uint32_t* slots = grth + nq;  // [slices][nq] after gmin[nq]
+                    __stcg(slots + (int64_t)slice * nq + q, now);
+                    uint32_t m = ~0u;
+                    for (int s2 = 0; s2 < (int)gridDim.y; ++s2)
+                      m = min(m, __ldcg(slots + (int64_t)s2 * nq + q));
+                    if (m) atomicMax(grth + q, m);
+                  }
+                }
                 int64_t rel = gbase + j;
                 if (rel < 0) rel += gcap;
                 const uint64_t comp = make_comp(key, (uint32_t)rel);
@@ -455,12 +485,10 @@ k_topk_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUten
                   if (++hcnt == k) {
                     hroot = tc_heapify(heap, k);
                     thr = fmaxf(thr, s_threshold(comp_key(hroot), iq));
-                    if (gthr) atomicMax(gthr + q, (uint32_t)(hroot >> 32));
                   }
                 } else if (comp > hroot) {
                   hroot = tc_heap_replace(heap, k, comp);
                   thr = fmaxf(thr, s_threshold(comp_key(hroot), iq));
-                  if (gthr) atomicMax(gthr + q, (uint32_t)(hroot >> 32));
                 }
               }
             }
@@ -614,11 +642,19 @@ static int launch_cg(const TopkArgs& a, uint64_t* partials, int n_slices, cudaSt
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   const int dbg = env_int("SS_TC_DEBUG", 0) | (tc_prefetch() << 8);
-  if (a.gthr) SS_CUDA_TRY(cudaMemsetAsync(a.gthr, 0, (size_t)a.nq * sizeof(uint32_t), st));
+  // cross-slice bound sharing: R = ceil(k / slices) <= 4 so every slice
+  // tracks its best R keys in registers (needs >= 16 slices at k = 64)
+  int rshare = 0;
+  if (a.gthr && n_slices >= 2 && n_slices <= kMaxShareSlices) {
+    const int R = (a.k + n_slices - 1) / n_slices;
+    if (R <= 4) rshare = R;
+  }
+  if (rshare)
+    SS_CUDA_TRY(cudaMemsetAsync(a.gthr, 0, (size_t)(n_slices + 1) * a.nq * sizeof(uint32_t), st));
   count_launch();
   SS_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_topk_tc<CG>, mq, mb, a.q_inv, a.nq, a.inv, a.n_rows,
                                  a.dim / tc::BK, stages, a.k, a.theta, a.head % a.gcap, a.gcap,
-                                 a.slot_offset, tps, partials, dbg, a.gthr));
+                                 a.slot_offset, tps, partials, dbg, a.gthr, rshare));
   return SS_OK;
 }
 

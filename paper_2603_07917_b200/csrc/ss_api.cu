@@ -99,11 +99,12 @@ struct ss_bank {
 // grow-on-demand (call once outside CUDA-graph capture); nullptr on failure
 // simply disables the cross-slice threshold sharing
 static uint32_t* gthr_reserve(ss_bank* h, int64_t nq) {
-  // Sharing max(slice roots) was measured to give no pruning (slices advance
-  // in lockstep, so the max of their k-th keys ~ each one's); kept behind
-  // SS_TC_GTHR=1 as an experiment knob.
+  // cross-slice R-th-best sharing in the tcgen05 top-k: correct, but measured
+  // slower than independent slices (profiles/ROUND1.md), so opt-in via
+  // SS_TC_GTHR=1
   static const bool on = getenv("SS_TC_GTHR") && atoi(getenv("SS_TC_GTHR")) == 1;
   if (!on) return nullptr;
+  nq *= kMaxShareSlices + 1;
   if (nq <= h->gthr_cap) return h->gthr;
   if (h->gthr) cudaFree(h->gthr);
   h->gthr = nullptr;

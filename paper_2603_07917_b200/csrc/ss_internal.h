@@ -47,8 +47,9 @@ struct TopkArgs {
   // optional [nq] scratch: per-query best known lower bound of the global k-th
   // key (orderable bits), shared by all slices so each slice filters with the
   // tightest threshold any slice has proven
-  uint32_t* gthr = nullptr;
+  uint32_t* gthr = nullptr;  // [slices][nq], slices <= kMaxShareSlices
 };
+constexpr int kMaxShareSlices = 160;
 int launch_topk_scan(const TopkArgs& a, uint64_t* partials, int n_slices, cudaStream_t st);
 int topk_scan_slices(const TopkArgs& a, int device);
 int launch_topk_tc(const TopkArgs& a, uint64_t* partials, int n_slices, cudaStream_t st);
