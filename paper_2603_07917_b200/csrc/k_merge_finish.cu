@@ -13,7 +13,7 @@
 
 namespace ss {
 
-constexpr int MF_THREADS = 256;
+constexpr int MF_THREADS = 512;
 
 // ---------------------------------------------------------------------------
 // select the top-k of M candidate composites (cand[0..M) in smem) into
@@ -165,6 +165,70 @@ __device__ void block_select_topk(uint64_t* cand, int32_t* cpay, int M, int nlis
       __syncthreads();
     }
   }
+}
+
+// Unordered top-k SET (all the histogram needs): tau-prune as above, then the
+// k-th largest composite by a 64-step bitwise search where each step is one
+// __syncthreads_count over one candidate per thread (composites are unique,
+// so {c >= kth} has exactly min(k, m) members).  Falls back to the ordered
+// selection when more than blockDim candidates survive the prune.
+__device__ void block_select_set(uint64_t* cand, int32_t* cpay, int M, int nlists, int k, int kpad,
+                                 uint64_t* sel, int32_t* spay, int* hist, int* s_misc) {
+  __shared__ uint64_t tau_s;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  if (tid == 0) { tau_s = 1ull; s_misc[3] = 0; }
+  __syncthreads();
+  for (int l = warp; l < nlists; l += nw) {
+    uint64_t mn = ~0ull;
+    for (int j = lane; j < k; j += 32) mn = min(mn, cand[l * k + j]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    if (lane == 0 && mn != 0ull) atomicMax(reinterpret_cast<unsigned long long*>(&tau_s), mn);
+  }
+  __syncthreads();
+  const uint64_t tau = tau_s;
+  int nz = 0;
+  for (int i = tid; i < M; i += blockDim.x) nz += (cand[i] >= tau);
+  for (int o = 16; o > 0; o >>= 1) nz += __shfl_xor_sync(0xffffffffu, nz, o);
+  if (lane == 0) atomicAdd(&s_misc[3], nz);
+  __syncthreads();
+  const int m1 = s_misc[3];
+  if (m1 > (int)blockDim.x) {  // rare: the ordered path handles any size
+    block_select_topk(cand, cpay, M, nlists, k, kpad, sel, spay, hist, s_misc);
+    return;
+  }
+  // compact the survivors, one per thread
+  __shared__ uint64_t one[1024];
+  __shared__ int32_t onep[1024];
+  if (tid == 0) s_misc[0] = 0;
+  __syncthreads();
+  for (int i = tid; i < M; i += blockDim.x) {
+    const uint64_t c = cand[i];
+    if (c >= tau) {
+      const int p = atomicAdd(&s_misc[0], 1);
+      one[p] = c;
+      onep[p] = cpay[i];
+    }
+  }
+  __syncthreads();
+  const uint64_t mine = (tid < m1) ? one[tid] : 0ull;
+  uint64_t T = 1ull;  // keep everything when m1 <= k
+  if (m1 > k) {
+    T = 0ull;
+    for (int b = 63; b >= 0; --b) {
+      const uint64_t t = T | (1ull << b);
+      if (__syncthreads_count(mine >= t) >= k) T = t;
+    }
+  }
+  for (int i = tid; i < kpad; i += blockDim.x) { sel[i] = 0ull; spay[i] = 0; }
+  if (tid == 0) s_misc[0] = 0;
+  __syncthreads();
+  if (mine != 0ull && mine >= T) {
+    const int p = atomicAdd(&s_misc[0], 1);
+    sel[p] = mine;
+    spay[p] = onep[tid];
+  }
+  __syncthreads();
 }
 
 // load nlists x k candidates of query q; payload = carried length (len) or
@@ -478,7 +542,7 @@ k_merge_finish(const uint64_t* __restrict__ partials, int nlists, int64_t nq, in
   const int64_t q = blockIdx.x;
   load_candidates(partials, nullptr, nlists, nq, k, q, cand, cpay, bank_lens, head, gcap,
                   slot_offset);
-  block_select_topk(cand, cpay, M, nlists, k, kpad, sel, spay, hist, s_misc);
+  block_select_set(cand, cpay, M, nlists, k, kpad, sel, spay, hist, s_misc);  // unordered set
   resolve_lens(sel, spay, k, bank_lens, head, gcap, slot_offset);
   for (int i = threadIdx.x; i < k; i += blockDim.x) {
     if (out_comp) out_comp[q * k + i] = sel[i];
@@ -490,6 +554,224 @@ k_merge_finish(const uint64_t* __restrict__ partials, int nlists, int64_t nq, in
              s_misc, s_warp);
 }
 
+// ---------------------------------------------------------------------------
+// warp-per-request merge + finish (the single-GPU round's default): no block
+// barriers, all 32-wide ballots / shuffles, one request per warp, so 1024
+// requests are one wave of short warps.
+//   1. candidates of all slices -> per-warp smem; tau = max over full lists of
+//      their minimum (the global k-th is >= it); survivors compacted in place
+//   2. k-th largest composite: bitwise search on the high 32 bits (the key),
+//      then on the low 32 bits (rel) only if the key itself is tied
+//   3. winners' lengths, histogram (smem atomics) or fallback, ascending
+//      ballot compaction of the bins, exact integer Gittins (warp scan)
+// ---------------------------------------------------------------------------
+constexpr int MFW_WARPS = 4;
+
+__device__ __forceinline__ int warp_sum_i32(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__global__ void __launch_bounds__(MFW_WARPS * 32)
+k_merge_finish_w(const uint64_t* __restrict__ partials, int nlists, int64_t nq, int k,
+                 const int32_t* __restrict__ bank_lens, int64_t head, int64_t gcap,
+                 int64_t slot_offset, uint64_t* __restrict__ out_comp, int32_t* __restrict__ out_len,
+                 int min_matches, int max_len, int nbins, const int32_t* __restrict__ I,
+                 const int64_t* __restrict__ fb_cnt, const int64_t* __restrict__ fb_sv,
+                 const int64_t* __restrict__ fb_sv2, int P, int32_t* __restrict__ npts,
+                 int32_t* __restrict__ pbin, int32_t* __restrict__ pcnt, int64_t* __restrict__ pD,
+                 int64_t* __restrict__ psv, uint8_t* __restrict__ used_fb, double* __restrict__ G,
+                 size_t warp_bytes) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t q = (int64_t)blockIdx.x * MFW_WARPS + warp;
+  if (q >= nq) return;  // warp-uniform; no block barriers below
+  const int M = nlists * k;
+  unsigned char* base = smem + warp * warp_bytes;
+  uint64_t* cand = reinterpret_cast<uint64_t*>(base);       // [M]
+  uint64_t* sel = cand + M;                                 // [k]
+  int32_t* slen = reinterpret_cast<int32_t*>(sel + k);      // [k]
+  FinishSmem f = carve_finish(reinterpret_cast<unsigned char*>(slen + ((k + 3) & ~3)), nbins);
+  __shared__ int whist_all[MFW_WARPS][256];
+  int* whist = whist_all[warp];
+  const unsigned lt = (1u << lane) - 1u;
+
+  // 1. load (all loads independent of each other: many in flight) + tau
+  if ((k & 31) == 0) {  // k multiple of 32: fixed per-list pattern, 8 lists' loads in flight
+    const int per = k >> 5;
+    const uint64_t* src0 = partials + q * k + lane;
+    const int64_t lstride = nq * (int64_t)k;
+    int l = 0;
+    for (; l + 8 <= nlists; l += 8) {
+      for (int jj = 0; jj < per; ++jj) {
+        uint64_t v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = __ldcs(src0 + (l + u) * lstride + jj * 32);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) cand[(l + u) * k + jj * 32 + lane] = v[u];
+      }
+    }
+    for (; l < nlists; ++l)
+      for (int jj = 0; jj < per; ++jj) cand[l * k + jj * 32 + lane] = __ldcs(src0 + l * lstride + jj * 32);
+  } else {
+    int l = 0, j = lane;
+    while (j >= k) { j -= k; ++l; }
+    for (int i = lane; i < M; i += 32) {
+      cand[i] = __ldcs(partials + ((int64_t)l * nq + q) * k + j);
+      j += 32;
+      while (j >= k) { j -= k; ++l; }
+    }
+  }
+  __syncwarp();
+  uint64_t tau = 1ull;
+  for (int l = 0; l < nlists; ++l) {
+    uint64_t mn = ~0ull;
+    for (int j = lane; j < k; j += 32) mn = min(mn, cand[l * k + j]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    if (mn != 0ull) tau = max(tau, mn);
+  }
+  int m1 = 0;
+  for (int i0 = 0; i0 < M; i0 += 32) {
+    const int i = i0 + lane;
+    const uint64_t c = (i < M) ? cand[i] : 0ull;
+    const bool keep = c >= tau;
+    const unsigned b = __ballot_sync(0xffffffffu, keep);
+    __syncwarp();
+    if (keep) cand[m1 + __popc(b & lt)] = c;
+    m1 += __popc(b);
+    __syncwarp();
+  }
+  // 2. k-th largest (unique composites): T such that |{c >= T}| = min(k, m1)
+  uint64_t T = 1ull;
+  if (m1 > k) {
+    // k-th largest high word by an MSB-first 8-bit radix select (4 passes)
+    uint32_t th = 0, hmask = 0;
+    int need_hi = k;
+    for (int shift = 24; shift >= 0; shift -= 8) {
+      for (int d = lane; d < 256; d += 32) whist[d] = 0;
+      __syncwarp();
+      for (int i = lane; i < m1; i += 32) {
+        const uint32_t h = (uint32_t)(cand[i] >> 32);
+        if ((h & hmask) == th) atomicAdd(&whist[(h >> shift) & 255u], 1);
+      }
+      __syncwarp();
+      int local = 0;  // lane owns digits 255-8*lane .. 248-8*lane (descending)
+#pragma unroll
+      for (int t = 0; t < 8; ++t) local += whist[255 - 8 * lane - t];
+      const int incl = warp_incl_scan_i32(local, lane);
+      const int excl = incl - local;
+      int dsel = -1, nsel = 0;
+      if (excl < need_hi && incl >= need_hi) {
+        int cum = excl;
+        for (int t = 0; t < 8; ++t) {
+          const int d = 255 - 8 * lane - t;
+          if (cum + whist[d] >= need_hi) { dsel = d; nsel = need_hi - cum; break; }
+          cum += whist[d];
+        }
+      }
+      const unsigned who = __ballot_sync(0xffffffffu, dsel >= 0);
+      const int src = __ffs(who) - 1;
+      dsel = __shfl_sync(0xffffffffu, dsel, src);
+      need_hi = __shfl_sync(0xffffffffu, nsel, src);
+      th |= (uint32_t)dsel << shift;
+      hmask |= 255u << shift;
+      __syncwarp();
+    }
+    int gt = 0, eq = 0;
+    for (int i = lane; i < m1; i += 32) {
+      const uint32_t h = (uint32_t)(cand[i] >> 32);
+      gt += (h > th);
+      eq += (h == th);
+    }
+    gt = warp_sum_i32(gt);
+    eq = warp_sum_i32(eq);
+    const int need = k - gt;
+    uint32_t tl = 0;
+    if (eq > need) {  // key tie at the boundary: resolve on rel (insertion order)
+      for (int bit = 31; bit >= 0; --bit) {
+        const uint32_t t = tl | (1u << bit);
+        int cnt = 0;
+        for (int i = lane; i < m1; i += 32)
+          cnt += ((uint32_t)(cand[i] >> 32) == th) && ((uint32_t)cand[i] >= t);
+        if (warp_sum_i32(cnt) >= need) tl = t;
+      }
+    }
+    T = ((uint64_t)th << 32) | tl;
+  }
+  // 3a. winners (unordered) and their lengths
+  int m = 0;
+  for (int i0 = 0; i0 < m1; i0 += 32) {
+    const int i = i0 + lane;
+    const uint64_t c = (i < m1) ? cand[i] : 0ull;
+    const bool w = (c != 0ull) && c >= T;
+    const unsigned b = __ballot_sync(0xffffffffu, w);
+    if (w) {
+      const int p = m + __popc(b & lt);
+      sel[p] = c;
+      int64_t g = (int64_t)comp_rel(c) + head % gcap;
+      if (g >= gcap) g -= gcap;
+      slen[p] = bank_lens[g - slot_offset];
+    }
+    m += __popc(b);
+  }
+  __syncwarp();
+  for (int i = lane; i < k; i += 32) {
+    if (out_comp) out_comp[q * k + i] = (i < m) ? sel[i] : 0ull;
+    if (out_len) out_len[q * k + i] = (i < m) ? slen[i] : 0;
+  }
+  // 3b. histogram of the winners (or the fallback law)
+  const long long Iq = I[q];
+  const int w = max_len / nbins;
+  const bool fb = m < min_matches;
+  if (!fb) {
+    for (int b = lane; b < nbins; b += 32) { f.h_cnt[b] = 0; f.h_sv[b] = 0; f.h_sv2[b] = 0; }
+    __syncwarp();
+    for (int i = lane; i < m; i += 32) {
+      const int L = min(max(slen[i], 1), max_len);
+      const int b = (L - 1) / w;
+      atomicAdd(&f.h_cnt[b], 1);
+      atomicAdd(reinterpret_cast<unsigned long long*>(&f.h_sv[b]), (unsigned long long)L);
+      atomicAdd(reinterpret_cast<unsigned long long*>(&f.h_sv2[b]),
+                (unsigned long long)((long long)L * L));
+    }
+  } else {
+    for (int b = lane; b < nbins; b += 32) {
+      f.h_cnt[b] = (int32_t)fb_cnt[b];
+      f.h_sv[b] = fb_sv[b];
+      f.h_sv2[b] = fb_sv2[b];
+    }
+  }
+  __syncwarp();
+  int np = 0;
+  for (int b0 = 0; b0 < nbins; b0 += 32) {
+    const int b = b0 + lane;
+    const int c = (b < nbins) ? f.h_cnt[b] : 0;
+    const unsigned bal = __ballot_sync(0xffffffffu, c > 0);
+    if (c > 0) {
+      const int pos = np + __popc(bal & lt);
+      const long long D = f.h_sv2[b] + 2 * Iq * f.h_sv[b];
+      f.l_c[pos] = c;
+      f.l_D[pos] = D;
+      if (pos < P) {
+        pbin[q * P + pos] = b;
+        pcnt[q * P + pos] = c;
+        pD[q * P + pos] = D;
+        if (psv) psv[q * P + pos] = f.h_sv[b];
+      }
+    }
+    np += __popc(bal);
+  }
+  __syncwarp();
+  const double g = (np > 0) ? warp_gittins_exact(f.l_c, f.l_D, np, 0, (int)Iq, 0, 0, lane) : INFINITY;
+  if (lane == 0) {
+    G[q] = g;
+    npts[q] = np;
+    if (used_fb) used_fb[q] = fb ? 1 : 0;
+  }
+}
+
 int launch_merge_finish(const uint64_t* partials, int nlists, int64_t nq, int k,
                         const int32_t* bank_lens, int64_t head, int64_t gcap, int64_t slot_offset,
                         uint64_t* out_comp, int32_t* out_len, int min_matches, int max_len,
@@ -497,6 +779,23 @@ int launch_merge_finish(const uint64_t* partials, int nlists, int64_t nq, int k,
                         const int64_t* fb_sv2, int P, int32_t* npts, int32_t* pbin, int32_t* pcnt,
                         int64_t* pD, int64_t* psv, uint8_t* used_fb, double* G, cudaStream_t st) {
   if (nq <= 0) return SS_OK;
+  {
+    const size_t wb = (((size_t)nlists * k * 8 + (size_t)k * 8 + (size_t)((k + 3) & ~3) * 4 + 15) &
+                       ~(size_t)15) + ((finish_smem(nbins) + 15) & ~(size_t)15);
+    const size_t smem = wb * MFW_WARPS;
+    if (smem <= 200 * 1024) {
+      if (smem > 48 * 1024)
+        SS_CUDA_TRY(cudaFuncSetAttribute(k_merge_finish_w,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      count_launch();
+      k_merge_finish_w<<<(unsigned)((nq + MFW_WARPS - 1) / MFW_WARPS), MFW_WARPS * 32, smem, st>>>(
+          partials, nlists, nq, k, bank_lens, head, gcap, slot_offset, out_comp, out_len,
+          min_matches, max_len, nbins, I, fb_cnt, fb_sv, fb_sv2, P, npts, pbin, pcnt, pD, psv,
+          used_fb, G, wb);
+      SS_LAUNCH_CHECK();
+      return SS_OK;
+    }
+  }
   int kpad = 1;
   while (kpad < k) kpad <<= 1;
   const size_t smem = ((merge_smem(nlists, k, kpad) + 15) & ~(size_t)15) + finish_smem(nbins);
