@@ -497,6 +497,15 @@ k_topk_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUten
       };
       // software pipeline: the TMEM load of chunk c+1 is in flight while
       // chunk c is scanned
+      if (dbg & 16) {  // debug: no TMEM reads at all (MMA + TMA floor)
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if constexpr (CG == 2) mbar_arrive_leader(&tempty[acc]);
+          else mbar_arrive(&tempty[acc]);
+        }
+        continue;
+      }
       int va[32], vb[32];
       tmem_ld32_async(tbase, va);
       tmem_wait_regs(va);
@@ -603,7 +612,18 @@ bool topk_tc_supported(const TopkArgs& a) {
   return tc_stages(a.dim, a.k, 1) >= 2;
 }
 
+// the A-in-TMEM variant (two epilogue warps per sub-partition): measured
+// faster for pure top-k (theta <= 0, heap-heavy) at nq > 128, equal or slower
+// otherwise (profiles/ROUND1.md).  SS_TC_TS=0/1 forces it off/on.
+static bool use_ts(const TopkArgs& a) {
+  static const int v = env_int("SS_TC_TS", -1);
+  if (!topk_ts_supported(a)) return false;
+  if (v == 0 || v == 1) return v == 1;
+  return a.theta <= 0.0f && a.nq > 128;
+}
+
 int topk_tc_slices(const TopkArgs& a, int device) {
+  if (use_ts(a)) return topk_ts_lists(a, device);
   int sms = sm_count(device);
   const int cg = tc_cg(a.nq);
   int64_t qtiles = (a.nq + tc::BM - 1) / tc::BM;
@@ -660,6 +680,7 @@ static int launch_cg(const TopkArgs& a, uint64_t* partials, int n_slices, cudaSt
 
 int launch_topk_tc(const TopkArgs& a, uint64_t* partials, int n_slices, cudaStream_t st) {
   if (!topk_tc_supported(a)) return set_error(SS_ERR_UNSUPPORTED, "tcgen05 path unsupported");
+  if (use_ts(a)) return launch_topk_ts(a, partials, n_slices, st);
   return tc_cg(a.nq) == 2 ? launch_cg<2>(a, partials, n_slices, st)
                           : launch_cg<1>(a, partials, n_slices, st);
 }

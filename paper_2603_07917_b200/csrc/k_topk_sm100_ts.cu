@@ -1,0 +1,413 @@
+// Stage 1, large-batch path, v2: the query block (A operand) lives in TMEM.
+//
+// Same math and parity contract as k_topk_sm100.cu (tcgen05.mma kind::i8,
+// exact int32 dots, fused per-query top-k), restructured so the epilogue has
+// two warps per SM sub-partition:
+//   * A (128 queries x dim int8) is written once into TMEM columns
+//     [A_COL, A_COL + dim/4) by the epilogue warps (tcgen05.st), and the MMA
+//     reads it from there ("TS" form), so no shared memory holds A;
+//   * that frees room for two heap sets: 8 epilogue warps, two per TMEM lane
+//     quarter, each pair splitting every tile's columns in half and keeping
+//     its own per-query heap (each half is emitted as its own partial list);
+//   * N = 128 bank rows per tile with THREE accumulator buffers in TMEM, so
+//     the MMA can run up to two tiles ahead of the epilogue.
+// Warps: 0 TMA producer (bank tiles), 1 TMEM allocator + MMA issuer,
+// 2..9 epilogue (group g = (warp-2)/4 handles chunks [2g, 2g+2) of a tile).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <stdlib.h>
+
+#include "ss_common.cuh"
+#include "ss_internal.h"
+#include "topk_heap.cuh"
+
+namespace ss {
+namespace ts {
+
+constexpr int BM = 128;        // queries (TMEM lanes)
+constexpr int BN = 128;        // bank rows per tile (UMMA N)
+constexpr int BK = 128;        // bytes per K-block (128B swizzle atom)
+constexpr int UK = 32;         // int8 K per MMA
+constexpr int NACC = 3;        // accumulator buffers
+constexpr int A_COL = NACC * BN;  // 384: A lives in columns [384, 384 + dim/4)
+constexpr int EPI_WARPS = 8;
+constexpr int THREADS = 64 + EPI_WARPS * 32;
+constexpr int B_STAGE = BN * BK;  // 16 KB
+constexpr int CPG = BN / 32 / 2;  // chunks per group per tile (2)
+constexpr int KMAX = 64;
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void bar_init(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(b)), "r"(n));
+}
+__device__ __forceinline__ void bar_expect(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra W_%=;\n}\n" ::"r"(su32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma2d(void* dst, const CUtensorMap* m, uint64_t* b, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];\n" ::"r"(su32(dst)),
+      "l"(m), "r"(su32(b)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void commit(uint64_t* b) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(su32(b))
+               : "memory");
+}
+// D[tmem] (+)= A[tmem] x B[smem]^T
+__device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d),
+      "r"(a), "l"(bdesc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                           ((uint32_t)(BM >> 4) << 24);
+
+__device__ __forceinline__ void ld32_async(uint32_t taddr, int (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+      "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];\n"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+        "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+        "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void wait_ld(int (&v)[32]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n"
+               : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]),
+                 "+r"(v[6]), "+r"(v[7]), "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]),
+                 "+r"(v[12]), "+r"(v[13]), "+r"(v[14]), "+r"(v[15]), "+r"(v[16]), "+r"(v[17]),
+                 "+r"(v[18]), "+r"(v[19]), "+r"(v[20]), "+r"(v[21]), "+r"(v[22]), "+r"(v[23]),
+                 "+r"(v[24]), "+r"(v[25]), "+r"(v[26]), "+r"(v[27]), "+r"(v[28]), "+r"(v[29]),
+                 "+r"(v[30]), "+r"(v[31])
+               :
+               : "memory");
+}
+__device__ __forceinline__ void st32(uint32_t taddr, const uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, "
+      "%17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};\n" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]),
+      "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]),
+      "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]),
+      "r"(v[30]), "r"(v[31])
+      : "memory");
+}
+
+__device__ __noinline__ uint64_t heapify(uint64_t* heap, int k) {
+  for (int i = k / 2 - 1; i >= 0; --i) heap_sift_down<BM>(heap, k, i, heap[i * BM]);
+  return heap[0];
+}
+__device__ __noinline__ uint64_t heap_replace(uint64_t* heap, int k, uint64_t x) {
+  heap_sift_down<BM>(heap, k, 0, x);
+  return heap[0];
+}
+
+__global__ void __launch_bounds__(THREADS, 1)
+k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
+          const float* __restrict__ q_inv, int64_t nq, const float* __restrict__ inv, int64_t n_rows,
+          int dim, int stages, int k, float theta, int64_t hmod, int64_t gcap, int64_t slot_offset,
+          int64_t tiles_per_slice, uint64_t* __restrict__ partials) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sB = smem;                                                    // stages x 16 KB
+  uint64_t* s_heap = reinterpret_cast<uint64_t*>(sB + stages * B_STAGE);  // [2][k][128]
+  float* s_iw = reinterpret_cast<float*>(s_heap + 2 * (size_t)k * BM);   // [8 warps][2][64]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(s_iw + EPI_WARPS * 2 * 64);
+  uint64_t* a_full = bars;
+  uint64_t* full = bars + 1;
+  uint64_t* empty = full + stages;
+  uint64_t* tfull = empty + stages;
+  uint64_t* tempty = tfull + NACC;
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(tempty + NACC);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int qt = blockIdx.x, slice = blockIdx.y;
+  const int nkb = dim / BK;
+  const int64_t tile0 = (int64_t)slice * tiles_per_slice;
+  const int64_t total_tiles = (n_rows + BN - 1) / BN;
+  const int ntiles = (int)max((int64_t)0, min(total_tiles, tile0 + tiles_per_slice) - tile0);
+
+  if (threadIdx.x == 0) {
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmB) : "memory");
+    bar_init(a_full, 4);
+    for (int s = 0; s < stages; ++s) { bar_init(&full[s], 1); bar_init(&empty[s], 1); }
+    for (int b = 0; b < NACC; ++b) { bar_init(&tfull[b], 1); bar_init(&tempty[b], EPI_WARPS); }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(su32(s_tmem)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *s_tmem;
+
+  if (warp == 0) {
+    // ------------------------------------------------------ TMA producer ---
+    if (lane == 0 && ntiles > 0) {
+      int it = 0;
+      for (int t = 0; t < ntiles; ++t) {
+        const int row0 = (int)((tile0 + t) * BN);
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int s = it % stages;
+          bar_wait(&empty[s], ((it / stages) & 1) ^ 1);
+          bar_expect(&full[s], B_STAGE);
+          tma2d(sB + s * B_STAGE, &tmB, &full[s], kb * BK, row0);
+        }
+      }
+      for (int i = max(0, it - stages); i < it; ++i) bar_wait(&empty[i % stages], (i / stages) & 1);
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------- MMA issuer ----
+    if (lane == 0 && ntiles > 0) {
+      bar_wait(a_full, 0);
+      fence_after();
+      const uint32_t b_base = su32(sB);
+      int it = 0;
+      for (int t = 0; t < ntiles; ++t) {
+        const int acc = t % NACC;
+        bar_wait(&tempty[acc], ((t / NACC) & 1) ^ 1);
+        fence_after();
+        const uint32_t d = tmem + acc * BN;
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int s = it % stages;
+          bar_wait(&full[s], (it / stages) & 1);
+          fence_after();
+#pragma unroll
+          for (int kk = 0; kk < BK / UK; ++kk)
+            mma_ts(d, tmem + A_COL + (kb * (BK / UK) + kk) * (UK / 4),
+                   desc_sw128(b_base + s * B_STAGE + kk * UK), IDESC, (kb | kk) != 0);
+          commit(&empty[s]);
+        }
+        commit(&tfull[acc]);
+      }
+    }
+  } else {
+    // --------------------------------------------------------- epilogue ----
+    const int ew = warp - 2;                // 0..7
+    const int grp = ew >> 2;                // column half of each tile
+    const int quarter = warp & 3;           // TMEM lane quarter
+    const int qrow = quarter * 32 + lane;
+    const int64_t q = (int64_t)qt * BM + qrow;
+    const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
+    // group 0 writes this query's int8 vector into TMEM (A operand)
+    if (grp == 0) {
+      const int ncol = dim / 4;
+      for (int c0 = 0; c0 < ncol; c0 += 32) {
+        uint32_t v[32];
+        const uint4* src = reinterpret_cast<const uint4*>(Q + q * dim) + c0 / 4;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          uint4 x = (q < nq) ? __ldg(src + u) : make_uint4(0, 0, 0, 0);
+          v[4 * u + 0] = x.x; v[4 * u + 1] = x.y; v[4 * u + 2] = x.z; v[4 * u + 3] = x.w;
+        }
+        st32(tmem + lane_base + A_COL + c0, v);
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+      fence_before();
+      __syncwarp();
+      if (lane == 0) bar_arrive(a_full);
+    }
+    const float iq = (q < nq) ? q_inv[q] : __int_as_float(0x7fc00000);
+    int hcnt = 0;
+    uint64_t hroot = 0;
+    uint64_t* heap = s_heap + (size_t)grp * k * BM + qrow;
+    float* wiw = s_iw + ew * 128;
+    const float NaNf = __int_as_float(0x7fc00000);
+    float pre[2];
+    auto fetch_iw = [&](int t) {
+      const int64_t r0 = (tile0 + t) * BN + grp * 64 + lane * 2;
+      if (r0 + 2 <= n_rows) {
+        const float2 a = __ldg(reinterpret_cast<const float2*>(inv + r0));
+        pre[0] = a.x; pre[1] = a.y;
+      } else {
+        pre[0] = (r0 < n_rows) ? inv[r0] : NaNf;
+        pre[1] = (r0 + 1 < n_rows) ? inv[r0 + 1] : NaNf;
+      }
+    };
+    if (ntiles > 0) fetch_iw(0);
+    float thr = (iq == iq) ? s_threshold(theta, iq) : INFINITY;
+    for (int t = 0; t < ntiles; ++t) {
+      const int acc = t % NACC;
+      const int64_t row0 = (tile0 + t) * BN + grp * 64;  // first bank row of my columns
+      float* ciw = wiw + (t & 1) * 64;
+      reinterpret_cast<float2*>(ciw)[lane] = make_float2(pre[0], pre[1]);
+      __syncwarp();
+      if (t + 1 < ntiles) fetch_iw(t + 1);
+      bar_wait(&tfull[acc], (t / NACC) & 1);
+      fence_after();
+      const uint32_t tbase = tmem + lane_base + acc * BN + grp * 64;
+      auto chunk = [&](const int (&v)[32], const int c) {
+        float s[32];
+        const float4* iw4 = reinterpret_cast<const float4*>(ciw + c * 32);
+#pragma unroll
+        for (int j4 = 0; j4 < 8; ++j4) {
+          const float4 w = iw4[j4];
+          s[4 * j4 + 0] = __fmul_rn(__int2float_rn(v[4 * j4 + 0]), w.x);
+          s[4 * j4 + 1] = __fmul_rn(__int2float_rn(v[4 * j4 + 1]), w.y);
+          s[4 * j4 + 2] = __fmul_rn(__int2float_rn(v[4 * j4 + 2]), w.z);
+          s[4 * j4 + 3] = __fmul_rn(__int2float_rn(v[4 * j4 + 3]), w.w);
+        }
+        float m[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) m[j] = fmaxf(s[j], s[j + 16]);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) m[j] = fmaxf(m[j], m[j + 8]);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) m[j] = fmaxf(m[j], m[j + 4]);
+        const float mx = fmaxf(fmaxf(m[0], m[1]), fmaxf(m[2], m[3]));
+        if (mx >= thr) {
+          const int64_t gbase = slot_offset + row0 + c * 32 - hmod;
+          uint32_t mask = 0;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) mask |= (s[j] >= thr ? 1u : 0u) << j;
+          float sl[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) sl[j] = s[j];
+          while (mask) {
+            const int j = __ffs(mask) - 1;
+            mask &= mask - 1;
+            const float key = __fmul_rn(sl[j], iq);
+            if (key >= theta) {
+              int64_t rel = gbase + j;
+              if (rel < 0) rel += gcap;
+              const uint64_t comp = make_comp(key, (uint32_t)rel);
+              if (hcnt < k) {
+                heap[hcnt * BM] = comp;
+                if (++hcnt == k) {
+                  hroot = heapify(heap, k);
+                  thr = fmaxf(thr, s_threshold(comp_key(hroot), iq));
+                }
+              } else if (comp > hroot) {
+                hroot = heap_replace(heap, k, comp);
+                thr = fmaxf(thr, s_threshold(comp_key(hroot), iq));
+              }
+            }
+          }
+        }
+      };
+      int va[32], vb[32];
+      ld32_async(tbase, va);
+      wait_ld(va);
+      ld32_async(tbase + 32, vb);
+      chunk(va, 0);
+      wait_ld(vb);
+      fence_before();  // this group's half of the accumulator is drained
+      __syncwarp();
+      if (lane == 0) bar_arrive(&tempty[acc]);
+      chunk(vb, 1);
+      __syncwarp();
+    }
+    if (q < nq) {
+      uint64_t* out = partials + (((int64_t)slice * 2 + grp) * nq + q) * k;
+      for (int i = 0; i < k; ++i) out[i] = (i < hcnt) ? heap[i * BM] : 0ull;
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
+  }
+}
+
+}  // namespace ts
+
+static PFN_cuTensorMapEncodeTiled_v12000 ts_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qr) == cudaSuccess &&
+        qr == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+static size_t ts_fixed_smem(int k) {
+  return 2 * (size_t)k * ts::BM * 8 + ts::EPI_WARPS * 2 * 64 * 4 + 512 + 1024;
+}
+static int ts_stages(int k) {
+  for (int s = 8; s >= 3; --s)
+    if (ts_fixed_smem(k) + (size_t)s * ts::B_STAGE <= 227 * 1024) return s;
+  return 0;
+}
+
+bool topk_ts_supported(const TopkArgs& a) {
+  if (a.dim % ts::BK || a.dim / 4 + ts::A_COL > 512 || a.k < 1 || a.k > ts::KMAX) return false;
+  if (a.n_rows >= (1LL << 31) || a.nq >= (1LL << 31)) return false;
+  return ts_stages(a.k) >= 3;
+}
+
+// partial lists = 2 per CTA slice (one per epilogue column half)
+int topk_ts_lists(const TopkArgs& a, int device) {
+  int sms = sm_count(device);
+  int64_t qtiles = (a.nq + ts::BM - 1) / ts::BM;
+  int64_t tiles = (a.n_rows + ts::BN - 1) / ts::BN;
+  int64_t s = sms / qtiles;
+  if (s < 1) s = 1;
+  if (s > tiles) s = tiles;
+  return (int)(2 * s);
+}
+
+int launch_topk_ts(const TopkArgs& a, uint64_t* partials, int n_lists, cudaStream_t st) {
+  const int n_slices = n_lists / 2;
+  if (n_slices < 1 || n_lists % 2) return set_error(SS_ERR_ARG, "ts: lists must be even");
+  auto enc = ts_encode();
+  if (!enc) return set_error(SS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  CUtensorMap mb;
+  cuuint64_t gdim[2] = {(cuuint64_t)a.dim, (cuuint64_t)a.n_rows};
+  cuuint64_t gstride[1] = {(cuuint64_t)a.dim};
+  cuuint32_t box[2] = {(cuuint32_t)ts::BK, (cuuint32_t)ts::BN};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(&mb, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(a.emb), gdim, gstride,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(SS_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  const int stages = ts_stages(a.k);
+  const size_t smem = ts_fixed_smem(a.k) + (size_t)stages * ts::B_STAGE;
+  SS_CUDA_TRY(cudaFuncSetAttribute(ts::k_topk_ts, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int64_t tiles = (a.n_rows + ts::BN - 1) / ts::BN;
+  const int64_t tps = (tiles + n_slices - 1) / n_slices;
+  dim3 grid((unsigned)((a.nq + ts::BM - 1) / ts::BM), (unsigned)n_slices);
+  count_launch();
+  ts::k_topk_ts<<<grid, ts::THREADS, smem, st>>>(mb, a.q, a.q_inv, a.nq, a.inv, a.n_rows, a.dim,
+                                                 stages, a.k, a.theta, a.head % a.gcap, a.gcap,
+                                                 a.slot_offset, tps, partials);
+  SS_LAUNCH_CHECK();
+  return SS_OK;
+}
+
+}  // namespace ss

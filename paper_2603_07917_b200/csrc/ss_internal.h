@@ -55,6 +55,11 @@ int topk_scan_slices(const TopkArgs& a, int device);
 int launch_topk_tc(const TopkArgs& a, uint64_t* partials, int n_slices, cudaStream_t st);
 int topk_tc_slices(const TopkArgs& a, int device);
 bool topk_tc_supported(const TopkArgs& a);
+// v2 tcgen05 kernel with the query block in TMEM (k_topk_sm100_ts.cu); its
+// "slices" are partial lists, two per CTA slice
+bool topk_ts_supported(const TopkArgs& a);
+int topk_ts_lists(const TopkArgs& a, int device);
+int launch_topk_ts(const TopkArgs& a, uint64_t* partials, int n_lists, cudaStream_t st);
 
 int launch_merge(const uint64_t* comp, const int32_t* len, int nlists, int64_t nq, int k,
                  uint64_t* out_comp, int32_t* out_len, const int32_t* bank_lens,
