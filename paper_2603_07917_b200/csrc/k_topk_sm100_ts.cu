@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
           const float* __restrict__ q_inv, int64_t nq, const float* __restrict__ inv, int64_t n_rows,
           int dim, int stages, int k, float theta, int64_t hmod, int64_t gcap, int64_t slot_offset,
-          int64_t tiles_per_slice, uint64_t* __restrict__ partials) {
+          int64_t tiles_per_slice, uint64_t* __restrict__ partials, int dbg) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sB = smem;                                                    // stages x 16 KB
@@ -206,7 +206,7 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
           fence_after();
 #pragma unroll
           for (int kk = 0; kk < BK / UK; ++kk)
-            mma_ts(d, tmem + A_COL + (kb * (BK / UK) + kk) * (UK / 4),
+            if (!(dbg & 2)) mma_ts(d, tmem + A_COL + (kb * (BK / UK) + kk) * (UK / 4),
                    desc_sw128(b_base + s * B_STAGE + kk * UK), IDESC, (kb | kk) != 0);
           commit(&empty[s]);
         }
@@ -287,7 +287,7 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
 #pragma unroll
         for (int j = 0; j < 4; ++j) m[j] = fmaxf(m[j], m[j + 4]);
         const float mx = fmaxf(fmaxf(m[0], m[1]), fmaxf(m[2], m[3]));
-        if (mx >= thr) {
+        if (!(dbg & 1) && mx >= thr) {
           const int64_t gbase = slot_offset + row0 + c * 32 - hmod;
           uint32_t mask = 0;
 #pragma unroll
@@ -317,16 +317,22 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
           }
         }
       };
+      if (dbg & 16) {
+        fence_before();
+        __syncwarp();
+        if (lane == 0) bar_arrive(&tempty[acc]);
+        continue;
+      }
       int va[32], vb[32];
       ld32_async(tbase, va);
       wait_ld(va);
       ld32_async(tbase + 32, vb);
-      chunk(va, 0);
+      if (!(dbg & 4)) chunk(va, 0);
       wait_ld(vb);
       fence_before();  // this group's half of the accumulator is drained
       __syncwarp();
       if (lane == 0) bar_arrive(&tempty[acc]);
-      chunk(vb, 1);
+      if (!(dbg & 4)) chunk(vb, 1);
       __syncwarp();
     }
     if (q < nq) {
@@ -405,7 +411,7 @@ int launch_topk_ts(const TopkArgs& a, uint64_t* partials, int n_lists, cudaStrea
   count_launch();
   ts::k_topk_ts<<<grid, ts::THREADS, smem, st>>>(mb, a.q, a.q_inv, a.nq, a.inv, a.n_rows, a.dim,
                                                  stages, a.k, a.theta, a.head % a.gcap, a.gcap,
-                                                 a.slot_offset, tps, partials);
+                                                 a.slot_offset, tps, partials, getenv("SS_TC_DEBUG") ? atoi(getenv("SS_TC_DEBUG")) : 0);
   SS_LAUNCH_CHECK();
   return SS_OK;
 }
