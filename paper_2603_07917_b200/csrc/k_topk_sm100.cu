@@ -612,14 +612,16 @@ bool topk_tc_supported(const TopkArgs& a) {
   return tc_stages(a.dim, a.k, 1) >= 2;
 }
 
-// the A-in-TMEM variant (two epilogue warps per sub-partition): measured
-// faster for pure top-k (theta <= 0, heap-heavy) at nq > 128, equal or slower
-// otherwise (profiles/ROUND1.md).  SS_TC_TS=0/1 forces it off/on.
+// the A-in-TMEM variant (k_topk_sm100_ts.cu: two epilogue warps per
+// sub-partition, accumulator drained to registers): measured faster at
+// nq > 128 for both theta = 0.8 and pure top-k; the single-query-tile
+// streaming case stays on this kernel (profiles/ROUND1.md).
+// SS_TC_TS=0/1 forces it off/on.
 static bool use_ts(const TopkArgs& a) {
   static const int v = env_int("SS_TC_TS", -1);
   if (!topk_ts_supported(a)) return false;
   if (v == 0 || v == 1) return v == 1;
-  return a.theta <= 0.0f && a.nq > 128;
+  return a.nq > 128;
 }
 
 int topk_tc_slices(const TopkArgs& a, int device) {

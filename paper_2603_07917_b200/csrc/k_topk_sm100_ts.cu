@@ -1,18 +1,21 @@
-// Stage 1, large-batch path, v2: the query block (A operand) lives in TMEM.
+// Stage 1, large-batch path, v3: the query block (A operand) lives in TMEM.
 //
 // Same math and parity contract as k_topk_sm100.cu (tcgen05.mma kind::i8,
-// exact int32 dots, fused per-query top-k), restructured so the epilogue has
-// two warps per SM sub-partition:
+// exact int32 dots, fused per-query top-k), restructured so the epilogue is
+// two warps per SM sub-partition and overlaps the MMA:
 //   * A (128 queries x dim int8) is written once into TMEM columns
-//     [A_COL, A_COL + dim/4) by the epilogue warps (tcgen05.st), and the MMA
-//     reads it from there ("TS" form), so no shared memory holds A;
+//     [A_COL, A_COL + dim/4) by the epilogue warps (tcgen05.st); the MMA
+//     reads it there ("TS" form), so no shared memory holds A;
 //   * that frees room for two heap sets: 8 epilogue warps, two per TMEM lane
-//     quarter, each pair splitting every tile's columns in half and keeping
-//     its own per-query heap (each half is emitted as its own partial list);
-//   * N = 128 bank rows per tile with THREE accumulator buffers in TMEM, so
-//     the MMA can run up to two tiles ahead of the epilogue.
+//     quarter, splitting every tile's 256 columns in halves, each half with
+//     its own per-query heap (emitted as its own partial list);
+//   * one N=256 accumulator (N=256 is what keeps the int8 MMA at full rate):
+//     each epilogue warp pulls its 4 column chunks into registers, releases
+//     the accumulator at once, and filters from registers while the MMA of
+//     the next tile runs;
+//   * bank tiles arrive in 64-byte K-blocks (SWIZZLE_64B) so 5 stages fit.
 // Warps: 0 TMA producer (bank tiles), 1 TMEM allocator + MMA issuer,
-// 2..9 epilogue (group g = (warp-2)/4 handles chunks [2g, 2g+2) of a tile).
+// 2..9 epilogue (group g = (warp-2)/4 owns columns [128g, 128g+128)).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <stdlib.h>
@@ -24,16 +27,15 @@
 namespace ss {
 namespace ts {
 
-constexpr int BM = 128;        // queries (TMEM lanes)
-constexpr int BN = 128;        // bank rows per tile (UMMA N)
-constexpr int BK = 128;        // bytes per K-block (128B swizzle atom)
-constexpr int UK = 32;         // int8 K per MMA
-constexpr int NACC = 3;        // accumulator buffers
-constexpr int A_COL = NACC * BN;  // 384: A lives in columns [384, 384 + dim/4)
+constexpr int BM = 128;          // queries (TMEM lanes)
+constexpr int BN = 256;          // bank rows per tile (UMMA N)
+constexpr int BK = 64;           // bytes per K-block (64B swizzle atom)
+constexpr int UK = 32;           // int8 K per MMA
+constexpr int A_COL = BN;        // A lives in TMEM columns [256, 256 + dim/4)
 constexpr int EPI_WARPS = 8;
 constexpr int THREADS = 64 + EPI_WARPS * 32;
 constexpr int B_STAGE = BN * BK;  // 16 KB
-constexpr int CPG = BN / 32 / 2;  // chunks per group per tile (2)
+constexpr int CPW = BN / 32 / 2;  // column chunks per epilogue warp per tile (4)
 constexpr int KMAX = 64;
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -75,13 +77,14 @@ __device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a, uint64_t bdesc, u
       "r"(a), "l"(bdesc), "r"(idesc), "r"(acc)
       : "memory");
 }
-__device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
+// K-major, 64B swizzle: rows of 64 B, 8-row atoms 512 B apart (SBO)
+__device__ __forceinline__ uint64_t desc_sw64(uint32_t saddr) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);
   d |= (uint64_t)1 << 16;
-  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)(512 >> 4) << 32;
   d |= (uint64_t)1 << 46;
-  d |= (uint64_t)2 << 61;
+  d |= (uint64_t)4 << 61;
   return d;
 }
 constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
@@ -141,14 +144,14 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
   uint8_t* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sB = smem;                                                    // stages x 16 KB
   uint64_t* s_heap = reinterpret_cast<uint64_t*>(sB + stages * B_STAGE);  // [2][k][128]
-  float* s_iw = reinterpret_cast<float*>(s_heap + 2 * (size_t)k * BM);   // [8 warps][2][64]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(s_iw + EPI_WARPS * 2 * 64);
+  float* s_iw = reinterpret_cast<float*>(s_heap + 2 * (size_t)k * BM);   // [8 warps][2][128]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(s_iw + EPI_WARPS * 2 * 128);
   uint64_t* a_full = bars;
   uint64_t* full = bars + 1;
   uint64_t* empty = full + stages;
   uint64_t* tfull = empty + stages;
-  uint64_t* tempty = tfull + NACC;
-  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(tempty + NACC);
+  uint64_t* tempty = tfull + 1;
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(tempty + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int qt = blockIdx.x, slice = blockIdx.y;
@@ -161,7 +164,8 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmB) : "memory");
     bar_init(a_full, 4);
     for (int s = 0; s < stages; ++s) { bar_init(&full[s], 1); bar_init(&empty[s], 1); }
-    for (int b = 0; b < NACC; ++b) { bar_init(&tfull[b], 1); bar_init(&tempty[b], EPI_WARPS); }
+    bar_init(tfull, 1);
+    bar_init(tempty, EPI_WARPS);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 1) {
@@ -196,21 +200,20 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
       const uint32_t b_base = su32(sB);
       int it = 0;
       for (int t = 0; t < ntiles; ++t) {
-        const int acc = t % NACC;
-        bar_wait(&tempty[acc], ((t / NACC) & 1) ^ 1);
+        bar_wait(tempty, (t & 1) ^ 1);  // every epilogue warp has pulled tile t-1 out
         fence_after();
-        const uint32_t d = tmem + acc * BN;
         for (int kb = 0; kb < nkb; ++kb, ++it) {
           const int s = it % stages;
           bar_wait(&full[s], (it / stages) & 1);
           fence_after();
 #pragma unroll
           for (int kk = 0; kk < BK / UK; ++kk)
-            if (!(dbg & 2)) mma_ts(d, tmem + A_COL + (kb * (BK / UK) + kk) * (UK / 4),
-                   desc_sw128(b_base + s * B_STAGE + kk * UK), IDESC, (kb | kk) != 0);
+            if (!(dbg & 2))
+              mma_ts(tmem, tmem + A_COL + (kb * (BK / UK) + kk) * (UK / 4),
+                     desc_sw64(b_base + s * B_STAGE + kk * UK), IDESC, (kb | kk) != 0);
           commit(&empty[s]);
         }
-        commit(&tfull[acc]);
+        commit(tfull);
       }
     }
   } else {
@@ -243,31 +246,50 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
     int hcnt = 0;
     uint64_t hroot = 0;
     uint64_t* heap = s_heap + (size_t)grp * k * BM + qrow;
-    float* wiw = s_iw + ew * 128;
+    float* wiw = s_iw + ew * 256;
     const float NaNf = __int_as_float(0x7fc00000);
-    float pre[2];
+    float pre[4];
     auto fetch_iw = [&](int t) {
-      const int64_t r0 = (tile0 + t) * BN + grp * 64 + lane * 2;
-      if (r0 + 2 <= n_rows) {
-        const float2 a = __ldg(reinterpret_cast<const float2*>(inv + r0));
-        pre[0] = a.x; pre[1] = a.y;
+      const int64_t r0 = (tile0 + t) * BN + grp * 128 + lane * 4;
+      if (r0 + 4 <= n_rows) {
+        const float4 a = __ldg(reinterpret_cast<const float4*>(inv + r0));
+        pre[0] = a.x; pre[1] = a.y; pre[2] = a.z; pre[3] = a.w;
       } else {
-        pre[0] = (r0 < n_rows) ? inv[r0] : NaNf;
-        pre[1] = (r0 + 1 < n_rows) ? inv[r0 + 1] : NaNf;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) pre[u] = (r0 + u < n_rows) ? inv[r0 + u] : NaNf;
       }
     };
     if (ntiles > 0) fetch_iw(0);
     float thr = (iq == iq) ? s_threshold(theta, iq) : INFINITY;
     for (int t = 0; t < ntiles; ++t) {
-      const int acc = t % NACC;
-      const int64_t row0 = (tile0 + t) * BN + grp * 64;  // first bank row of my columns
-      float* ciw = wiw + (t & 1) * 64;
-      reinterpret_cast<float2*>(ciw)[lane] = make_float2(pre[0], pre[1]);
+      const int64_t row0 = (tile0 + t) * BN + grp * 128;  // first bank row of my columns
+      float* ciw = wiw + (t & 1) * 128;
+      reinterpret_cast<float4*>(ciw)[lane] = make_float4(pre[0], pre[1], pre[2], pre[3]);
       __syncwarp();
       if (t + 1 < ntiles) fetch_iw(t + 1);
-      bar_wait(&tfull[acc], (t / NACC) & 1);
+      bar_wait(tfull, t & 1);
       fence_after();
-      const uint32_t tbase = tmem + lane_base + acc * BN + grp * 64;
+      const uint32_t tbase = tmem + lane_base + grp * 128;
+      if (dbg & 16) {
+        fence_before();
+        __syncwarp();
+        if (lane == 0) bar_arrive(tempty);
+        continue;
+      }
+      // pull my 4 chunks into registers, then hand the accumulator back
+      int v0[32], v1[32], v2[32], v3[32];
+      ld32_async(tbase, v0);
+      ld32_async(tbase + 32, v1);
+      ld32_async(tbase + 64, v2);
+      ld32_async(tbase + 96, v3);
+      wait_ld(v0);
+      wait_ld(v1);
+      wait_ld(v2);
+      wait_ld(v3);
+      fence_before();
+      __syncwarp();
+      if (lane == 0) bar_arrive(tempty);
+      if (dbg & 4) continue;
       auto chunk = [&](const int (&v)[32], const int c) {
         float s[32];
         const float4* iw4 = reinterpret_cast<const float4*>(ciw + c * 32);
@@ -317,22 +339,10 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
           }
         }
       };
-      if (dbg & 16) {
-        fence_before();
-        __syncwarp();
-        if (lane == 0) bar_arrive(&tempty[acc]);
-        continue;
-      }
-      int va[32], vb[32];
-      ld32_async(tbase, va);
-      wait_ld(va);
-      ld32_async(tbase + 32, vb);
-      if (!(dbg & 4)) chunk(va, 0);
-      wait_ld(vb);
-      fence_before();  // this group's half of the accumulator is drained
-      __syncwarp();
-      if (lane == 0) bar_arrive(&tempty[acc]);
-      if (!(dbg & 4)) chunk(vb, 1);
+      chunk(v0, 0);
+      chunk(v1, 1);
+      chunk(v2, 2);
+      chunk(v3, 3);
       __syncwarp();
     }
     if (q < nq) {
@@ -363,18 +373,19 @@ static PFN_cuTensorMapEncodeTiled_v12000 ts_encode() {
 }
 
 static size_t ts_fixed_smem(int k) {
-  return 2 * (size_t)k * ts::BM * 8 + ts::EPI_WARPS * 2 * 64 * 4 + 512 + 1024;
+  return 2 * (size_t)k * ts::BM * 8 + ts::EPI_WARPS * 2 * 128 * 4 + 512 + 1024;
 }
 static int ts_stages(int k) {
-  for (int s = 8; s >= 3; --s)
+  for (int s = 8; s >= 4; --s)
     if (ts_fixed_smem(k) + (size_t)s * ts::B_STAGE <= 227 * 1024) return s;
   return 0;
 }
 
 bool topk_ts_supported(const TopkArgs& a) {
-  if (a.dim % ts::BK || a.dim / 4 + ts::A_COL > 512 || a.k < 1 || a.k > ts::KMAX) return false;
+  if (a.dim % ts::BK || a.dim % 128 || a.dim / 4 + ts::A_COL > 512 || a.k < 1 || a.k > ts::KMAX)
+    return false;
   if (a.n_rows >= (1LL << 31) || a.nq >= (1LL << 31)) return false;
-  return ts_stages(a.k) >= 3;
+  return ts_stages(a.k) >= 4;
 }
 
 // partial lists = 2 per CTA slice (one per epilogue column half)
@@ -399,7 +410,7 @@ int launch_topk_ts(const TopkArgs& a, uint64_t* partials, int n_lists, cudaStrea
   cuuint32_t box[2] = {(cuuint32_t)ts::BK, (cuuint32_t)ts::BN};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(&mb, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(a.emb), gdim, gstride,
-                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_error(SS_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   const int stages = ts_stages(a.k);
@@ -408,10 +419,11 @@ int launch_topk_ts(const TopkArgs& a, uint64_t* partials, int n_lists, cudaStrea
   const int64_t tiles = (a.n_rows + ts::BN - 1) / ts::BN;
   const int64_t tps = (tiles + n_slices - 1) / n_slices;
   dim3 grid((unsigned)((a.nq + ts::BM - 1) / ts::BM), (unsigned)n_slices);
+  const char* dv = getenv("SS_TC_DEBUG");
   count_launch();
   ts::k_topk_ts<<<grid, ts::THREADS, smem, st>>>(mb, a.q, a.q_inv, a.nq, a.inv, a.n_rows, a.dim,
                                                  stages, a.k, a.theta, a.head % a.gcap, a.gcap,
-                                                 a.slot_offset, tps, partials, getenv("SS_TC_DEBUG") ? atoi(getenv("SS_TC_DEBUG")) : 0);
+                                                 a.slot_offset, tps, partials, dv ? atoi(dv) : 0);
   SS_LAUNCH_CHECK();
   return SS_OK;
 }
