@@ -6,14 +6,14 @@
 //   * A (128 queries x dim int8) is written once into TMEM columns
 //     [A_COL, A_COL + dim/4) by the epilogue warps (tcgen05.st); the MMA
 //     reads it there ("TS" form), so no shared memory holds A;
-//   * that frees room for two heap sets: 8 epilogue warps, two per TMEM lane
-//     quarter, splitting every tile's 256 columns in halves, each half with
-//     its own per-query heap (emitted as its own partial list);
-//   * one N=256 accumulator (N=256 is what keeps the int8 MMA at full rate):
-//     each epilogue warp pulls its 4 column chunks into registers, releases
-//     the accumulator at once, and filters from registers while the MMA of
-//     the next tile runs;
-//   * bank tiles arrive in 64-byte K-blocks (SWIZZLE_64B) so 5 stages fit.
+//   * 8 epilogue warps, two per TMEM lane quarter, split every tile's 256
+//     columns in halves; the two warps serving a query share its heap under
+//     a per-query shared-memory lock (inserts are rare), so one heap set and
+//     four 32 KB bank stages fit;
+//   * one N=256 accumulator (N=256 and 128B-swizzled K-blocks are what keep
+//     the int8 MMA at full rate): each epilogue warp pulls its 4 column
+//     chunks into registers, releases the accumulator at once, and filters
+//     from registers while the MMA of the next tile runs.
 // Warps: 0 TMA producer (bank tiles), 1 TMEM allocator + MMA issuer,
 // 2..9 epilogue (group g = (warp-2)/4 owns columns [128g, 128g+128)).
 #include <cuda.h>
@@ -29,12 +29,12 @@ namespace ts {
 
 constexpr int BM = 128;          // queries (TMEM lanes)
 constexpr int BN = 256;          // bank rows per tile (UMMA N)
-constexpr int BK = 64;           // bytes per K-block (64B swizzle atom)
+constexpr int BK = 128;          // bytes per K-block (128B swizzle atom)
 constexpr int UK = 32;           // int8 K per MMA
 constexpr int A_COL = BN;        // A lives in TMEM columns [256, 256 + dim/4)
 constexpr int EPI_WARPS = 8;
 constexpr int THREADS = 64 + EPI_WARPS * 32;
-constexpr int B_STAGE = BN * BK;  // 16 KB
+constexpr int B_STAGE = BN * BK;  // 32 KB
 constexpr int CPW = BN / 32 / 2;  // column chunks per epilogue warp per tile (4)
 constexpr int KMAX = 64;
 
@@ -77,14 +77,14 @@ __device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a, uint64_t bdesc, u
       "r"(a), "l"(bdesc), "r"(idesc), "r"(acc)
       : "memory");
 }
-// K-major, 64B swizzle: rows of 64 B, 8-row atoms 512 B apart (SBO)
-__device__ __forceinline__ uint64_t desc_sw64(uint32_t saddr) {
+// K-major, 128B swizzle: rows of 128 B, 8-row atoms 1024 B apart (SBO)
+__device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);
   d |= (uint64_t)1 << 16;
-  d |= (uint64_t)(512 >> 4) << 32;
+  d |= (uint64_t)(1024 >> 4) << 32;
   d |= (uint64_t)1 << 46;
-  d |= (uint64_t)4 << 61;
+  d |= (uint64_t)2 << 61;
   return d;
 }
 constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
@@ -142,10 +142,14 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
           int64_t tiles_per_slice, uint64_t* __restrict__ partials, int dbg) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
-  uint8_t* sB = smem;                                                    // stages x 16 KB
-  uint64_t* s_heap = reinterpret_cast<uint64_t*>(sB + stages * B_STAGE);  // [2][k][128]
-  float* s_iw = reinterpret_cast<float*>(s_heap + 2 * (size_t)k * BM);   // [8 warps][2][128]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(s_iw + EPI_WARPS * 2 * 128);
+  uint8_t* sB = smem;                                                    // stages x 32 KB
+  uint64_t* s_heap = reinterpret_cast<uint64_t*>(sB + stages * B_STAGE);  // [k][128]
+  uint64_t* s_hroot = s_heap + (size_t)k * BM;                           // [128]
+  int* s_hcnt = reinterpret_cast<int*>(s_hroot + BM);                    // [128]
+  int* s_hlock = s_hcnt + BM;                                            // [128]
+  float* s_iw = reinterpret_cast<float*>(s_hlock + BM);                  // [8 warps][2][128]
+  float* s_ib = s_iw + EPI_WARPS * 2 * 128;                              // [8 warps][2][8]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(s_ib + EPI_WARPS * 2 * 8);
   uint64_t* a_full = bars;
   uint64_t* full = bars + 1;
   uint64_t* empty = full + stages;
@@ -168,6 +172,7 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
     bar_init(tempty, EPI_WARPS);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
+  for (int i = threadIdx.x; i < BM; i += blockDim.x) { s_hcnt[i] = 0; s_hroot[i] = 0; s_hlock[i] = 0; }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(su32(s_tmem)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
@@ -210,7 +215,7 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
           for (int kk = 0; kk < BK / UK; ++kk)
             if (!(dbg & 2))
               mma_ts(tmem, tmem + A_COL + (kb * (BK / UK) + kk) * (UK / 4),
-                     desc_sw64(b_base + s * B_STAGE + kk * UK), IDESC, (kb | kk) != 0);
+                     desc_sw128(b_base + s * B_STAGE + kk * UK), IDESC, (kb | kk) != 0);
           commit(&empty[s]);
         }
         commit(tfull);
@@ -243,9 +248,8 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
       if (lane == 0) bar_arrive(a_full);
     }
     const float iq = (q < nq) ? q_inv[q] : __int_as_float(0x7fc00000);
-    int hcnt = 0;
-    uint64_t hroot = 0;
-    uint64_t* heap = s_heap + (size_t)grp * k * BM + qrow;
+    uint64_t* heap = s_heap + qrow;  // shared by the two column-half warps of this quarter
+    float* wib = s_ib + ew * 16;
     float* wiw = s_iw + ew * 256;
     const float NaNf = __int_as_float(0x7fc00000);
     float pre[4];
@@ -264,7 +268,23 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
     for (int t = 0; t < ntiles; ++t) {
       const int64_t row0 = (tile0 + t) * BN + grp * 128;  // first bank row of my columns
       float* ciw = wiw + (t & 1) * 128;
+      float* cib = wib + (t & 1) * 8;  // [max inv_w of chunk 0..3][min inv_w of chunk 0..3]
       reinterpret_cast<float4*>(ciw)[lane] = make_float4(pre[0], pre[1], pre[2], pre[3]);
+      {
+        // NaN (zero row / past the end) never passes the exact test: leave it
+        // out of the bounds
+        float hi = fmaxf(fmaxf(fmaxf(pre[0], pre[1]), fmaxf(pre[2], pre[3])), 0.f);
+        float lo = fminf(fminf(fminf(pre[0], pre[1]), fminf(pre[2], pre[3])), INFINITY);
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) {
+          hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+          lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        }
+        if ((lane & 7) == 0) {
+          cib[lane >> 3] = hi;
+          cib[4 + (lane >> 3)] = lo;
+        }
+      }
       __syncwarp();
       if (t + 1 < ntiles) fetch_iw(t + 1);
       bar_wait(tfull, t & 1);
@@ -290,33 +310,45 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
       __syncwarp();
       if (lane == 0) bar_arrive(tempty);
       if (dbg & 4) continue;
+      // Filter: a chunk of 32 columns can only hold a score >= thr if
+      // fl(fl(max dot) * (max inv_w)) >= thr (or the min inv_w when every dot
+      // is negative) -- monotone rounding makes this a superset test, so the
+      // exact per-column scores (one int->float conversion each, quarter rate)
+      // are only computed for the rare chunks that pass it.
       auto chunk = [&](const int (&v)[32], const int c) {
-        float s[32];
-        const float4* iw4 = reinterpret_cast<const float4*>(ciw + c * 32);
+        int m[11];
 #pragma unroll
-        for (int j4 = 0; j4 < 8; ++j4) {
-          const float4 w = iw4[j4];
-          s[4 * j4 + 0] = __fmul_rn(__int2float_rn(v[4 * j4 + 0]), w.x);
-          s[4 * j4 + 1] = __fmul_rn(__int2float_rn(v[4 * j4 + 1]), w.y);
-          s[4 * j4 + 2] = __fmul_rn(__int2float_rn(v[4 * j4 + 2]), w.z);
-          s[4 * j4 + 3] = __fmul_rn(__int2float_rn(v[4 * j4 + 3]), w.w);
-        }
-        float m[16];
+        for (int j = 0; j < 10; ++j) m[j] = __vimax3_s32(v[3 * j], v[3 * j + 1], v[3 * j + 2]);
+        m[10] = max(v[30], v[31]);
+        const int md = __vimax3_s32(__vimax3_s32(m[0], m[1], m[2]), __vimax3_s32(m[3], m[4], m[5]),
+                                    __vimax3_s32(__vimax3_s32(m[6], m[7], m[8]), m[9], m[10]));
+        const float bnd = __fmul_rn(__int2float_rn(md), md >= 0 ? cib[c] : cib[4 + c]);
+        if (!(dbg & 1) && bnd >= thr) {
+          float s[32];
+          const float4* iw4 = reinterpret_cast<const float4*>(ciw + c * 32);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) m[j] = fmaxf(s[j], s[j + 16]);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) m[j] = fmaxf(m[j], m[j + 8]);
-#pragma unroll
-        for (int j = 0; j < 4; ++j) m[j] = fmaxf(m[j], m[j + 4]);
-        const float mx = fmaxf(fmaxf(m[0], m[1]), fmaxf(m[2], m[3]));
-        if (!(dbg & 1) && mx >= thr) {
+          for (int j4 = 0; j4 < 8; ++j4) {
+            const float4 w = iw4[j4];
+            s[4 * j4 + 0] = __fmul_rn(__int2float_rn(v[4 * j4 + 0]), w.x);
+            s[4 * j4 + 1] = __fmul_rn(__int2float_rn(v[4 * j4 + 1]), w.y);
+            s[4 * j4 + 2] = __fmul_rn(__int2float_rn(v[4 * j4 + 2]), w.z);
+            s[4 * j4 + 3] = __fmul_rn(__int2float_rn(v[4 * j4 + 3]), w.w);
+          }
           const int64_t gbase = slot_offset + row0 + c * 32 - hmod;
           uint32_t mask = 0;
 #pragma unroll
           for (int j = 0; j < 32; ++j) mask |= (s[j] >= thr ? 1u : 0u) << j;
+          if (!mask) return;
           float sl[32];
 #pragma unroll
           for (int j = 0; j < 32; ++j) sl[j] = s[j];
+          // this query's heap is shared with the other column-half warp: take
+          // its lock (one lock per thread at a time, never nested)
+          while (atomicCAS(&s_hlock[qrow], 0, 1) != 0) {
+          }
+          __threadfence_block();
+          int hcnt = s_hcnt[qrow];
+          uint64_t hroot = s_hroot[qrow];
           while (mask) {
             const int j = __ffs(mask) - 1;
             mask &= mask - 1;
@@ -327,16 +359,17 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
               const uint64_t comp = make_comp(key, (uint32_t)rel);
               if (hcnt < k) {
                 heap[hcnt * BM] = comp;
-                if (++hcnt == k) {
-                  hroot = heapify(heap, k);
-                  thr = fmaxf(thr, s_threshold(comp_key(hroot), iq));
-                }
+                if (++hcnt == k) hroot = heapify(heap, k);
               } else if (comp > hroot) {
                 hroot = heap_replace(heap, k, comp);
-                thr = fmaxf(thr, s_threshold(comp_key(hroot), iq));
               }
             }
           }
+          s_hcnt[qrow] = hcnt;
+          s_hroot[qrow] = hroot;
+          __threadfence_block();
+          atomicExch(&s_hlock[qrow], 0);
+          if (hcnt >= k) thr = fmaxf(thr, s_threshold(comp_key(hroot), iq));
         }
       };
       chunk(v0, 0);
@@ -345,9 +378,11 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
       chunk(v3, 3);
       __syncwarp();
     }
-    if (q < nq) {
-      uint64_t* out = partials + (((int64_t)slice * 2 + grp) * nq + q) * k;
-      for (int i = 0; i < k; ++i) out[i] = (i < hcnt) ? heap[i * BM] : 0ull;
+    asm volatile("bar.sync 1, %0;\n" ::"n"(EPI_WARPS * 32) : "memory");  // both halves done
+    if (grp == 0 && q < nq) {
+      uint64_t* out = partials + ((int64_t)slice * nq + q) * k;
+      const int hc = s_hcnt[qrow];
+      for (int i = 0; i < k; ++i) out[i] = (i < hc) ? heap[i * BM] : 0ull;
     }
   }
   fence_before();
@@ -373,10 +408,10 @@ static PFN_cuTensorMapEncodeTiled_v12000 ts_encode() {
 }
 
 static size_t ts_fixed_smem(int k) {
-  return 2 * (size_t)k * ts::BM * 8 + ts::EPI_WARPS * 2 * 128 * 4 + 512 + 1024;
+  return (size_t)k * ts::BM * 8 + ts::BM * 16 + ts::EPI_WARPS * 2 * 136 * 4 + 512 + 1024;
 }
 static int ts_stages(int k) {
-  for (int s = 8; s >= 4; --s)
+  for (int s = 6; s >= 3; --s)
     if (ts_fixed_smem(k) + (size_t)s * ts::B_STAGE <= 227 * 1024) return s;
   return 0;
 }
@@ -385,10 +420,10 @@ bool topk_ts_supported(const TopkArgs& a) {
   if (a.dim % ts::BK || a.dim % 128 || a.dim / 4 + ts::A_COL > 512 || a.k < 1 || a.k > ts::KMAX)
     return false;
   if (a.n_rows >= (1LL << 31) || a.nq >= (1LL << 31)) return false;
-  return ts_stages(a.k) >= 4;
+  return ts_stages(a.k) >= 3;
 }
 
-// partial lists = 2 per CTA slice (one per epilogue column half)
+// one partial list per CTA slice
 int topk_ts_lists(const TopkArgs& a, int device) {
   int sms = sm_count(device);
   int64_t qtiles = (a.nq + ts::BM - 1) / ts::BM;
@@ -396,12 +431,12 @@ int topk_ts_lists(const TopkArgs& a, int device) {
   int64_t s = sms / qtiles;
   if (s < 1) s = 1;
   if (s > tiles) s = tiles;
-  return (int)(2 * s);
+  return (int)s;
 }
 
 int launch_topk_ts(const TopkArgs& a, uint64_t* partials, int n_lists, cudaStream_t st) {
-  const int n_slices = n_lists / 2;
-  if (n_slices < 1 || n_lists % 2) return set_error(SS_ERR_ARG, "ts: lists must be even");
+  const int n_slices = n_lists;
+  if (n_slices < 1) return set_error(SS_ERR_ARG, "ts: no slices");
   auto enc = ts_encode();
   if (!enc) return set_error(SS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   CUtensorMap mb;
@@ -410,7 +445,7 @@ int launch_topk_ts(const TopkArgs& a, uint64_t* partials, int n_lists, cudaStrea
   cuuint32_t box[2] = {(cuuint32_t)ts::BK, (cuuint32_t)ts::BN};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(&mb, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(a.emb), gdim, gstride,
-                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_error(SS_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   const int stages = ts_stages(a.k);

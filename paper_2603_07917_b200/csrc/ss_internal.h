@@ -55,8 +55,8 @@ int topk_scan_slices(const TopkArgs& a, int device);
 int launch_topk_tc(const TopkArgs& a, uint64_t* partials, int n_slices, cudaStream_t st);
 int topk_tc_slices(const TopkArgs& a, int device);
 bool topk_tc_supported(const TopkArgs& a);
-// v2 tcgen05 kernel with the query block in TMEM (k_topk_sm100_ts.cu); its
-// "slices" are partial lists, two per CTA slice
+// tcgen05 kernel with the query block in TMEM (k_topk_sm100_ts.cu); one
+// partial list per CTA slice
 bool topk_ts_supported(const TopkArgs& a);
 int topk_ts_lists(const TopkArgs& a, int device);
 int launch_topk_ts(const TopkArgs& a, uint64_t* partials, int n_lists, cudaStream_t st);
