@@ -196,7 +196,7 @@ def run_ours(args):
             roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                     "frac": round(achieved / peak, 4),
                     "peak_source": "measured copy bandwidth (MEASURED_PEAKS.json)"}
-        roof["kernel"] = "k_topk_tc" if algo_used == "tcgen05" else "k_topk_scan"
+        roof["kernel"] = topk_kernel_name(algo_used, NQ)
         roof["kernel_ms"] = round(kern_ms, 4)
         roof["kernel_share_of_step"] = round(kern_ms / (ms / args.steps), 3)
         roof["traffic"] = ncu_traffic(roof["kernel"])
@@ -210,7 +210,8 @@ def run_ours(args):
                        "nbins": NBINS, "theta": THETA, "min_matches": MIN_MATCHES,
                        "similarity": algo_used, "n_slices": n_slices,
                        "parallelism": f"replica x{world}" if world > 1 else "single GPU",
-                       "l2": "bank (403 MB) > L2 (126 MB): every round streams it from HBM"},
+                       "l2": f"bank ({N_BANK * (DIM + 4) / 1e6:.0f} MB) > L2 (126 MB): every "
+                             "round streams it from HBM"},
             "e2e": {"value": round(req * args.steps / (e2e_ms / 1e3), 1), "unit": "requests/s",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": round(e2e_ms / args.steps, 4)},
@@ -497,12 +498,24 @@ def time_e2e(sched, q, qi, I, ids, args):
     return e0.elapsed_time(e1), int(h2d), int(d2h)
 
 
+def topk_kernel_name(algo_used: str, nq: int) -> str:
+    """Which stage-1 kernel the library launches (mirrors use_ts() in
+    csrc/k_topk_sm100.cu): the A-in-TMEM tcgen05 kernel above one 128-query
+    tile, the streaming form of k_topk_tc at or below it."""
+    if algo_used != "tcgen05":
+        return "k_topk_scan"
+    if nq > 128 and os.environ.get("SS_TC_TS", "") != "0":
+        return "k_topk_ts"
+    return "k_topk_tc"
+
+
 def ncu_traffic(kernel: str):
-    """dram read+write bytes per launch from the committed ncu --set full summary."""
+    """dram read+write bytes per launch of `kernel` on this workload, from the
+    committed ncu --set full summary (profiles/ncu_traffic.json), else None."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         d = json.load(open(p))
-        return d.get(kernel)
+        return d.get(WORKLOAD.split(":")[0], {}).get(kernel)
     except Exception:
         return None
 

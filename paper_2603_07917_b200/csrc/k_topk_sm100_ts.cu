@@ -28,14 +28,10 @@ namespace ss {
 namespace ts {
 
 constexpr int BM = 128;          // queries (TMEM lanes)
-constexpr int BN = 256;          // bank rows per tile (UMMA N)
 constexpr int BK = 128;          // bytes per K-block (128B swizzle atom)
 constexpr int UK = 32;           // int8 K per MMA
-constexpr int A_COL = BN;        // A lives in TMEM columns [256, 256 + dim/4)
 constexpr int EPI_WARPS = 8;
 constexpr int THREADS = 64 + EPI_WARPS * 32;
-constexpr int B_STAGE = BN * BK;  // 32 KB
-constexpr int CPW = BN / 32 / 2;  // column chunks per epilogue warp per tile (4)
 constexpr int KMAX = 64;
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -87,8 +83,10 @@ __device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
   d |= (uint64_t)2 << 61;
   return d;
 }
-constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
-                           ((uint32_t)(BM >> 4) << 24);
+// kind::i8 instruction descriptor: s32 accumulator, s8 x s8, K-major A and B
+constexpr uint32_t idesc(int n) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
 
 __device__ __forceinline__ void ld32_async(uint32_t taddr, int (&v)[32]) {
   asm volatile(
@@ -135,11 +133,22 @@ __device__ __noinline__ uint64_t heap_replace(uint64_t* heap, int k, uint64_t x)
   return heap[0];
 }
 
+// BN bank rows per tile (UMMA N), NACC accumulators of BN columns in TMEM
+// (NACC = 2 lets the MMA of tile t+1 run while tile t is drained), A in
+// columns [NACC * BN, NACC * BN + dim / 4).
+template <int BN, int NACC>
 __global__ void __launch_bounds__(THREADS, 1)
 k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
           const float* __restrict__ q_inv, int64_t nq, const float* __restrict__ inv, int64_t n_rows,
           int dim, int stages, int k, float theta, int64_t hmod, int64_t gcap, int64_t slot_offset,
           int64_t tiles_per_slice, uint64_t* __restrict__ partials, int dbg) {
+  constexpr int A_COL = NACC * BN;
+  constexpr int B_STAGE = BN * BK;
+  constexpr int HALF = BN / 2;     // columns per epilogue warp per tile
+  constexpr int CPW = HALF / 32;   // 32-column chunks per epilogue warp per tile
+  static_assert(HALF % 32 == 0 && (CPW == 3 || CPW == 4), "tile shape");
+  static_assert(A_COL + 128 <= 512, "TMEM columns");
+  constexpr uint32_t IDESC = idesc(BN);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sB = smem;                                                    // stages x 32 KB
@@ -154,22 +163,23 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
   uint64_t* full = bars + 1;
   uint64_t* empty = full + stages;
   uint64_t* tfull = empty + stages;
-  uint64_t* tempty = tfull + 1;
-  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(tempty + 1);
+  uint64_t* tempty = tfull + NACC;
+  uint64_t* mdone = tempty + NACC;
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(mdone + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int qt = blockIdx.x, slice = blockIdx.y;
   const int nkb = dim / BK;
   const int64_t tile0 = (int64_t)slice * tiles_per_slice;
   const int64_t total_tiles = (n_rows + BN - 1) / BN;
-  const int ntiles = (int)max((int64_t)0, min(total_tiles, tile0 + tiles_per_slice) - tile0);
+  int ntiles = (int)max((int64_t)0, min(total_tiles, tile0 + tiles_per_slice) - tile0);
 
   if (threadIdx.x == 0) {
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmB) : "memory");
     bar_init(a_full, 4);
     for (int s = 0; s < stages; ++s) { bar_init(&full[s], 1); bar_init(&empty[s], 1); }
-    bar_init(tfull, 1);
-    bar_init(tempty, EPI_WARPS);
+    for (int b = 0; b < NACC; ++b) { bar_init(&tfull[b], 1); bar_init(&tempty[b], EPI_WARPS); }
+    bar_init(mdone, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   for (int i = threadIdx.x; i < BM; i += blockDim.x) { s_hcnt[i] = 0; s_hroot[i] = 0; s_hlock[i] = 0; }
@@ -191,6 +201,10 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
         for (int kb = 0; kb < nkb; ++kb, ++it) {
           const int s = it % stages;
           bar_wait(&empty[s], ((it / stages) & 1) ^ 1);
+          if (dbg & 8) {  // debug: MMA on stale tiles, no bank traffic
+            bar_arrive(&full[s]);
+            continue;
+          }
           bar_expect(&full[s], B_STAGE);
           tma2d(sB + s * B_STAGE, &tmB, &full[s], kb * BK, row0);
         }
@@ -205,8 +219,11 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
       const uint32_t b_base = su32(sB);
       int it = 0;
       for (int t = 0; t < ntiles; ++t) {
-        bar_wait(tempty, (t & 1) ^ 1);  // every epilogue warp has pulled tile t-1 out
+        const int acc = t % NACC;
+        // every epilogue warp has pulled tile t - NACC out of this accumulator
+        if (!(dbg & 64)) bar_wait(&tempty[acc], ((t / NACC) & 1) ^ 1);
         fence_after();
+        const uint32_t dacc = tmem + acc * BN;
         for (int kb = 0; kb < nkb; ++kb, ++it) {
           const int s = it % stages;
           bar_wait(&full[s], (it / stages) & 1);
@@ -214,11 +231,15 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
 #pragma unroll
           for (int kk = 0; kk < BK / UK; ++kk)
             if (!(dbg & 2))
-              mma_ts(tmem, tmem + A_COL + (kb * (BK / UK) + kk) * (UK / 4),
+              mma_ts(dacc, tmem + A_COL + (kb * (BK / UK) + kk) * (UK / 4),
                      desc_sw128(b_base + s * B_STAGE + kk * UK), IDESC, (kb | kk) != 0);
           commit(&empty[s]);
         }
-        commit(tfull);
+        commit(&tfull[acc]);
+      }
+      if (dbg & 64) {  // nobody drains: wait for the last MMA before teardown
+        commit(mdone);
+        bar_wait(mdone, 0);
       }
     }
   } else {
@@ -254,8 +275,10 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
     const float NaNf = __int_as_float(0x7fc00000);
     float pre[4];
     auto fetch_iw = [&](int t) {
-      const int64_t r0 = (tile0 + t) * BN + grp * 128 + lane * 4;
-      if (r0 + 4 <= n_rows) {
+      const int64_t r0 = (tile0 + t) * BN + grp * HALF + lane * 4;
+      if (lane * 4 >= HALF) {
+        pre[0] = pre[1] = pre[2] = pre[3] = NaNf;
+      } else if (r0 + 4 <= n_rows) {
         const float4 a = __ldg(reinterpret_cast<const float4*>(inv + r0));
         pre[0] = a.x; pre[1] = a.y; pre[2] = a.z; pre[3] = a.w;
       } else {
@@ -263,10 +286,12 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
         for (int u = 0; u < 4; ++u) pre[u] = (r0 + u < n_rows) ? inv[r0 + u] : NaNf;
       }
     };
+    if (dbg & 64) ntiles = 0;  // debug: MMA issue rate alone (no epilogue hand-off)
     if (ntiles > 0) fetch_iw(0);
     float thr = (iq == iq) ? s_threshold(theta, iq) : INFINITY;
     for (int t = 0; t < ntiles; ++t) {
-      const int64_t row0 = (tile0 + t) * BN + grp * 128;  // first bank row of my columns
+      const int64_t row0 = (tile0 + t) * BN + grp * HALF;  // first bank row of my columns
+      const int acc = t % NACC;
       float* ciw = wiw + (t & 1) * 128;
       float* cib = wib + (t & 1) * 8;  // [max inv_w of chunk 0..3][min inv_w of chunk 0..3]
       reinterpret_cast<float4*>(ciw)[lane] = make_float4(pre[0], pre[1], pre[2], pre[3]);
@@ -280,20 +305,20 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
           hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
           lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
         }
-        if ((lane & 7) == 0) {
+        if ((lane & 7) == 0 && (lane >> 3) < CPW) {
           cib[lane >> 3] = hi;
           cib[4 + (lane >> 3)] = lo;
         }
       }
       __syncwarp();
       if (t + 1 < ntiles) fetch_iw(t + 1);
-      bar_wait(tfull, t & 1);
+      bar_wait(&tfull[acc], (t / NACC) & 1);
       fence_after();
-      const uint32_t tbase = tmem + lane_base + grp * 128;
+      const uint32_t tbase = tmem + lane_base + acc * BN + grp * HALF;
       if (dbg & 16) {
         fence_before();
         __syncwarp();
-        if (lane == 0) bar_arrive(tempty);
+        if (lane == 0) bar_arrive(&tempty[acc]);
         continue;
       }
       // pull my 4 chunks into registers, then hand the accumulator back
@@ -301,14 +326,14 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
       ld32_async(tbase, v0);
       ld32_async(tbase + 32, v1);
       ld32_async(tbase + 64, v2);
-      ld32_async(tbase + 96, v3);
+      if constexpr (CPW == 4) ld32_async(tbase + 96, v3);
       wait_ld(v0);
       wait_ld(v1);
       wait_ld(v2);
-      wait_ld(v3);
+      if constexpr (CPW == 4) wait_ld(v3);
       fence_before();
       __syncwarp();
-      if (lane == 0) bar_arrive(tempty);
+      if (lane == 0) bar_arrive(&tempty[acc]);
       if (dbg & 4) continue;
       // Filter: a chunk of 32 columns can only hold a score >= thr if
       // fl(fl(max dot) * (max inv_w)) >= thr (or the min inv_w when every dot
@@ -375,7 +400,7 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
       chunk(v0, 0);
       chunk(v1, 1);
       chunk(v2, 2);
-      chunk(v3, 3);
+      if constexpr (CPW == 4) chunk(v3, 3);
       __syncwarp();
     }
     asm volatile("bar.sync 1, %0;\n" ::"n"(EPI_WARPS * 32) : "memory");  // both halves done
@@ -410,57 +435,72 @@ static PFN_cuTensorMapEncodeTiled_v12000 ts_encode() {
 static size_t ts_fixed_smem(int k) {
   return (size_t)k * ts::BM * 8 + ts::BM * 16 + ts::EPI_WARPS * 2 * 136 * 4 + 512 + 1024;
 }
-static int ts_stages(int k) {
-  for (int s = 6; s >= 3; --s)
-    if (ts_fixed_smem(k) + (size_t)s * ts::B_STAGE <= 227 * 1024) return s;
+
+// Tile shape: BN = 192 rows with two TMEM accumulators (the MMA of the next
+// tile overlaps the drain of this one) or BN = 256 with one.  SS_TC_TSN=256
+// forces the single-accumulator form.
+static int ts_bn() {
+  static const int v = getenv("SS_TC_TSN") ? atoi(getenv("SS_TC_TSN")) : 192;
+  return v == 256 ? 256 : 192;
+}
+static int ts_stages(int k, int bn) {
+  for (int s = 8; s >= 3; --s)
+    if (ts_fixed_smem(k) + (size_t)s * bn * ts::BK <= 227 * 1024) return s;
   return 0;
 }
 
 bool topk_ts_supported(const TopkArgs& a) {
-  if (a.dim % ts::BK || a.dim % 128 || a.dim / 4 + ts::A_COL > 512 || a.k < 1 || a.k > ts::KMAX)
+  const int acols = ts_bn() == 256 ? 256 : 384;
+  if (a.dim % ts::BK || a.dim % 128 || a.dim / 4 + acols > 512 || a.k < 1 || a.k > ts::KMAX)
     return false;
   if (a.n_rows >= (1LL << 31) || a.nq >= (1LL << 31)) return false;
-  return ts_stages(a.k) >= 3;
+  return ts_stages(a.k, ts_bn()) >= 3;
 }
 
 // one partial list per CTA slice
 int topk_ts_lists(const TopkArgs& a, int device) {
   int sms = sm_count(device);
   int64_t qtiles = (a.nq + ts::BM - 1) / ts::BM;
-  int64_t tiles = (a.n_rows + ts::BN - 1) / ts::BN;
+  int64_t tiles = (a.n_rows + ts_bn() - 1) / ts_bn();
   int64_t s = sms / qtiles;
   if (s < 1) s = 1;
   if (s > tiles) s = tiles;
   return (int)s;
 }
 
-int launch_topk_ts(const TopkArgs& a, uint64_t* partials, int n_lists, cudaStream_t st) {
-  const int n_slices = n_lists;
-  if (n_slices < 1) return set_error(SS_ERR_ARG, "ts: no slices");
+template <int BN, int NACC>
+static int launch_ts_t(const TopkArgs& a, uint64_t* partials, int n_slices, cudaStream_t st) {
   auto enc = ts_encode();
   if (!enc) return set_error(SS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   CUtensorMap mb;
   cuuint64_t gdim[2] = {(cuuint64_t)a.dim, (cuuint64_t)a.n_rows};
   cuuint64_t gstride[1] = {(cuuint64_t)a.dim};
-  cuuint32_t box[2] = {(cuuint32_t)ts::BK, (cuuint32_t)ts::BN};
+  cuuint32_t box[2] = {(cuuint32_t)ts::BK, (cuuint32_t)BN};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(&mb, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(a.emb), gdim, gstride,
                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_error(SS_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
-  const int stages = ts_stages(a.k);
-  const size_t smem = ts_fixed_smem(a.k) + (size_t)stages * ts::B_STAGE;
-  SS_CUDA_TRY(cudaFuncSetAttribute(ts::k_topk_ts, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const int64_t tiles = (a.n_rows + ts::BN - 1) / ts::BN;
+  const int stages = ts_stages(a.k, BN);
+  const size_t smem = ts_fixed_smem(a.k) + (size_t)stages * BN * ts::BK;
+  SS_CUDA_TRY(cudaFuncSetAttribute(ts::k_topk_ts<BN, NACC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem));
+  const int64_t tiles = (a.n_rows + BN - 1) / BN;
   const int64_t tps = (tiles + n_slices - 1) / n_slices;
   dim3 grid((unsigned)((a.nq + ts::BM - 1) / ts::BM), (unsigned)n_slices);
   const char* dv = getenv("SS_TC_DEBUG");
   count_launch();
-  ts::k_topk_ts<<<grid, ts::THREADS, smem, st>>>(mb, a.q, a.q_inv, a.nq, a.inv, a.n_rows, a.dim,
-                                                 stages, a.k, a.theta, a.head % a.gcap, a.gcap,
-                                                 a.slot_offset, tps, partials, dv ? atoi(dv) : 0);
+  ts::k_topk_ts<BN, NACC><<<grid, ts::THREADS, smem, st>>>(
+      mb, a.q, a.q_inv, a.nq, a.inv, a.n_rows, a.dim, stages, a.k, a.theta, a.head % a.gcap, a.gcap,
+      a.slot_offset, tps, partials, dv ? atoi(dv) : 0);
   SS_LAUNCH_CHECK();
   return SS_OK;
+}
+
+int launch_topk_ts(const TopkArgs& a, uint64_t* partials, int n_lists, cudaStream_t st) {
+  if (n_lists < 1) return set_error(SS_ERR_ARG, "ts: no slices");
+  return ts_bn() == 256 ? launch_ts_t<256, 1>(a, partials, n_lists, st)
+                        : launch_ts_t<192, 2>(a, partials, n_lists, st);
 }
 
 }  // namespace ss

@@ -202,6 +202,17 @@ def test_topk_multi_tile_ring_wrap(cuda, algo, theta):
         assert np.array_equal(ln[i, :m], lens[seqs[sel]]), i
 
 
+@pytest.mark.parametrize("theta", [0.8, 0.3, 0.0, -1.0])
+def test_topk_large_batch_tcgen05(cuda, theta):
+    """nq = 1024 (the A-in-TMEM kernel with its integer pre-filter for
+    thr > 0), 40k-row bank over 64 clusters: many neighbours per query, so
+    heaps fill and the running threshold rises above theta."""
+    w, be, bl, q, qi = _bank(40_000, 384, 64, 5, 1024)
+    keys, seq, ref = _oracle_topk(w, be, q, qi, 64, theta)
+    comp, ln = w.topk(q, qi, 64, theta, "tcgen05")
+    _check_topk(w, comp, keys, seq, ref, 64)
+
+
 @pytest.mark.parametrize("algo", ["scan", "tcgen05"])
 def test_topk_edges(cuda, algo):
     """ragged nq, partially filled ring, ties, degenerate query, k > rows."""
