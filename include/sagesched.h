@@ -184,6 +184,25 @@ int64_t ss_rank_workspace_bytes(int64_t n);
 int ss_rank(const double* G, const int64_t* ids, int64_t n, int64_t* perm,
             void* workspace, int64_t workspace_bytes, void* stream);
 
+/* ---------------------------------------------------- batch formation -- */
+/* Engine step 3, the caller right after
+ * ss_rank: walk perm (ascending priority) and admit request r while the
+ * projected KV tokens sum(I[r] + g[r] + 1) <= kv_capacity and the count
+ * <= max_batch (SPEC.md:501 defaults K = 8192, B = 64).  mode SS_PACK_CUT
+ * stops at the first request that does not fit; SS_PACK_SKIP skips it and
+ * keeps scanning.  out_batch i64[max_batch] receives the admitted request
+ * indices in priority order, *out_count their number and *out_tokens the KV
+ * tokens they project.  A request with I + 1 > kv_capacity anywhere in [0, n)
+ * ("request cannot fit", SPEC.md engine errors) gives *out_count = -1 and
+ * *out_tokens = its index.  I, g i32[n] indexed by request; device pointers;
+ * async (graph-capturable). */
+#define SS_PACK_CUT 0
+#define SS_PACK_SKIP 1
+int ss_pack_batch(const int64_t* perm, const int32_t* input_len, const int32_t* g,
+                  int64_t n, int64_t kv_capacity, int32_t max_batch, int32_t mode,
+                  int64_t* out_batch, int32_t* out_count, int64_t* out_tokens,
+                  void* stream);
+
 /* ----------------------------------------------- fused scheduling round -- */
 /* One round for a batch of nq pending requests on a single-GPU bank:
  * ss_topk -> ss_bank_fallback_hist -> ss_finish -> ss_rank.  All device

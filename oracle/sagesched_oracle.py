@@ -304,6 +304,35 @@ def rank(G, ids):
     return np.lexsort((np.asarray(ids), np.asarray(G, F64)))
 
 
+def pack_batch(perm, I, g, kv_capacity, max_batch, mode="cut"):
+    """Engine batch formation, SPEC.md:470 step 3 (pure-Python restatement).
+
+    Walk ``perm`` (ascending priority); request r projects I[r] + g[r] + 1 KV
+    tokens (I + 1 when not yet prefilled, g = 0).  "cut": admit while the
+    running sum stays <= K and the count <= B, stopping at the first request
+    that does not fit.  "skip": a request that does not fit is passed over and
+    the scan continues.  Any request with I + 1 > K raises ValueError
+    ("request cannot fit", SPEC.md engine errors).  Returns (batch, tokens).
+    """
+    I = [int(x) for x in I]
+    g = [int(x) for x in g]
+    for r, i in enumerate(I):
+        if i + 1 > kv_capacity:
+            raise ValueError(f"request {r} cannot fit: I + 1 = {i + 1} > K = {kv_capacity}")
+    batch, used = [], 0
+    for r in perm:
+        r = int(r)
+        if len(batch) >= max_batch:
+            break
+        t = I[r] + g[r] + 1
+        if used + t <= kv_capacity:
+            batch.append(r)
+            used += t
+        elif mode == "cut":
+            break
+    return batch, used
+
+
 def refresh_due(g_old, g_new, bucket=200):
     """SPEC.md:345-353."""
     return (g_new // bucket) > (g_old // bucket)

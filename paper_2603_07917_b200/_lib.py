@@ -48,6 +48,7 @@ SIGNATURES = {
     "ss_refresh": (C.c_int, [I64, P, P, P, I32, P, P, P, I32, P, P, I32, P]),
     "ss_rank_workspace_bytes": (I64, [I64]),
     "ss_rank": (C.c_int, [P, P, I64, P, P, I64, P]),
+    "ss_pack_batch": (C.c_int, [P, P, P, I64, I64, I32, I32, P, P, P, P]),
     "ss_schedule_round": (C.c_int, [P, P, P, P, P, I64, I32, F32, I32, I32, I32, I32, I32,
                                     P, P, P, P, P, P, P, P]),
     "ss_schedule_round_host": (C.c_int, [P, P, P, P, P, I64, I32, F32, I32, I32, I32, I32,

@@ -453,6 +453,17 @@ int ss_rank(const double* G, const int64_t* ids, int64_t n, int64_t* perm, void*
   return launch_rank(G, ids, n, perm, workspace, workspace_bytes, (cudaStream_t)stream);
 }
 
+int ss_pack_batch(const int64_t* perm, const int32_t* input_len, const int32_t* g, int64_t n,
+                  int64_t kv_capacity, int32_t max_batch, int32_t mode, int64_t* out_batch,
+                  int32_t* out_count, int64_t* out_tokens, void* stream) {
+  if (n < 0 || kv_capacity < 1 || max_batch < 1 || (mode != SS_PACK_CUT && mode != SS_PACK_SKIP))
+    return set_error(SS_ERR_ARG, "pack_batch: bad args (n=%lld K=%lld B=%d mode=%d)",
+                     (long long)n, (long long)kv_capacity, max_batch, mode);
+  if (!perm && n > 0) return set_error(SS_ERR_ARG, "pack_batch: perm is null");
+  return launch_pack_batch(perm, input_len, g, n, kv_capacity, max_batch, mode, out_batch,
+                           out_count, out_tokens, (cudaStream_t)stream);
+}
+
 // ----------------------------------------------------------- fused round --
 // workspace layout: [topk partials ...][comp nq*k][len nq*k][fb 3*nbins][rank ws][host-round bufs]
 struct RoundLayout {

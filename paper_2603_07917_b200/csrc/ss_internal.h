@@ -82,6 +82,11 @@ int launch_refresh(int64_t n, const int32_t* I, const int32_t* g_new, int32_t* b
                    const int64_t* pD, int P, double* G_io, uint8_t* refreshed, int force,
                    cudaStream_t st);
 
+// batch formation (k_pack.cu)
+int launch_pack_batch(const int64_t* perm, const int32_t* I, const int32_t* g, int64_t n,
+                      int64_t K, int B, int mode, int64_t* out_batch, int32_t* out_count,
+                      int64_t* out_tokens, cudaStream_t st);
+
 // rank
 int64_t rank_workspace_bytes(int64_t n);
 int launch_rank(const double* G, const int64_t* ids, int64_t n, int64_t* perm,

@@ -13,8 +13,10 @@ round:
      (evicting the oldest, SPEC.md:122-130, PAPER.md:236);
   3. running requests crossing a 200-token bucket boundary are re-indexed
      (SageScheduler.refresh, SPEC.md:345-353);
-  4. all active requests are ranked (ascending G, id) and the first
-     ``batch_size`` run next round (the count limit of SPEC.md:470).
+  4. all active requests are ranked (ascending G, id) and the batch for the
+     next round is packed on the device over the ranked list (SPEC.md:470
+     step 3: projected KV tokens I + g + 1 <= ``kv_capacity``, count <=
+     ``batch_size``; ``kv_capacity=None`` keeps only the count limit).
 """
 
 from __future__ import annotations
@@ -25,7 +27,7 @@ import numpy as np
 import torch
 
 from .history import HistoryWindow
-from .scheduler import RequestTable, RoundConfig, SageScheduler, rank
+from .scheduler import BatchPlan, RequestTable, RoundConfig, SageScheduler, pack_batch, rank
 
 __all__ = ["Trace", "ReplayStats", "replay"]
 
@@ -51,7 +53,7 @@ class ReplayStats:
 
 def replay(window: HistoryWindow, trace: Trace, cfg: RoundConfig, arrivals_per_round: int,
            tokens_per_round: int, batch_size: int, max_active: int, rounds: int,
-           on_round=None) -> ReplayStats:
+           on_round=None, kv_capacity: int | None = None, pack_mode: str = "cut") -> ReplayStats:
     """Run ``rounds`` scheduling rounds over ``trace``; ``on_round(r, info)`` sees
     each round's device state (for parity checks)."""
     dev = "cuda"
@@ -63,6 +65,8 @@ def replay(window: HistoryWindow, trace: Trace, cfg: RoundConfig, arrivals_per_r
     running: list[int] = []          # request ids that run this round
     nxt = 0
     st = ReplayStats()
+    plan = BatchPlan(batch_size)
+    K = (1 << 62) if kv_capacity is None else int(kv_capacity)
     for r in range(rounds):
         # 2. progress + completions of the requests that ran last round
         done = []
@@ -98,14 +102,17 @@ def replay(window: HistoryWindow, trace: Trace, cfg: RoundConfig, arrivals_per_r
             continue
         rows_t = torch.as_tensor(act_rows, device=dev)
         sub = _Sub(table, rows_t)
-        refreshed = sched.refresh(sub, act_rows.size, torch.as_tensor(g_host[act_rows], device=dev))
+        g_act = torch.as_tensor(g_host[act_rows], device=dev)
+        refreshed = sched.refresh(sub, act_rows.size, g_act)
         sub.write_back(table, rows_t)
         st.refreshed += int(refreshed.sum().item())
         # 4. rank every active request, run the first batch_size
-        perm = rank(sub.G[:act_rows.size], sub.ids[:act_rows.size]).cpu().numpy()
-        running = [int(act_ids[p]) for p in perm[:batch_size]]
+        perm_t = rank(sub.G[:act_rows.size], sub.ids[:act_rows.size])
+        pack_batch(perm_t, sub.I[:act_rows.size], g_act, K, batch_size, pack_mode, out=plan)
+        batch, _ = plan.host()
+        running = [int(act_ids[b]) for b in batch]
         if on_round is not None:
-            on_round(r, dict(active_ids=act_ids, G=sub.G.cpu().numpy(), perm=perm,
+            on_round(r, dict(active_ids=act_ids, G=sub.G.cpu().numpy(), perm=perm_t.cpu().numpy(),
                              g=g_host[act_rows].copy(), running=running))
         st.rounds += 1
     return st

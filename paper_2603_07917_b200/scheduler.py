@@ -23,7 +23,7 @@ import torch
 from . import _lib
 from .history import HistoryWindow
 
-__all__ = ["RoundConfig", "PredictState", "RequestTable", "SageScheduler", "rank"]
+__all__ = ["BatchPlan", "pack_batch", "RoundConfig", "PredictState", "RequestTable", "SageScheduler", "rank"]
 
 
 @dataclass(frozen=True)
@@ -80,6 +80,50 @@ def rank(G: torch.Tensor, ids: torch.Tensor | None = None, perm: torch.Tensor | 
     _lib.call("ss_rank", _lib.ptr(G), _lib.ptr(ids), n, _lib.ptr(perm), _lib.ptr(workspace), wsb,
               _lib.stream_ptr())
     return perm
+
+
+PACK_MODE = {"cut": 0, "skip": 1}
+
+
+class BatchPlan:
+    """Device result of ``pack_batch``: ``batch[:count]`` request indices in
+    priority order, projecting ``tokens`` KV tokens."""
+
+    def __init__(self, max_batch: int, device="cuda"):
+        self.batch = torch.empty(max_batch, dtype=torch.int64, device=device)
+        self.count = torch.zeros(1, dtype=torch.int32, device=device)
+        self.tokens = torch.zeros(1, dtype=torch.int64, device=device)
+
+    def host(self):
+        """(batch int64 [count] numpy, tokens) after a synchronising read;
+        raises ValueError for a request that can never fit (SPEC.md engine
+        step errors: "request cannot fit")."""
+        n = int(self.count.item())
+        t = int(self.tokens.item())
+        if n < 0:
+            raise ValueError(f"request {t} cannot fit: I + 1 exceeds the KV capacity")
+        return self.batch[:n].cpu().numpy(), t
+
+
+def pack_batch(perm: torch.Tensor, input_len: torch.Tensor, g: torch.Tensor,
+               kv_capacity: int = 8192, max_batch: int = 64, mode: str = "cut",
+               out: BatchPlan | None = None, stream=None) -> BatchPlan:
+    """Engine batch formation over the ranked list (SPEC.md:470 step 3,
+    defaults K = 8192, B = 64 from SPEC.md:501): admit requests in ``perm``
+    order while sum(I + g + 1) <= K and count <= B.  ``mode`` "cut" stops at
+    the first request that does not fit, "skip" passes over it.  Async on the
+    device (graph-capturable); ``BatchPlan.host()`` reads the result."""
+    if mode not in PACK_MODE:
+        raise ValueError(f"mode must be one of {sorted(PACK_MODE)}, got {mode!r}")
+    n = perm.numel()
+    if out is None:
+        out = BatchPlan(max_batch, perm.device)
+    elif out.batch.numel() < max_batch:
+        raise ValueError("BatchPlan smaller than max_batch")
+    _lib.call("ss_pack_batch", _lib.ptr(perm), _lib.ptr(input_len), _lib.ptr(g), n,
+              int(kv_capacity), int(max_batch), PACK_MODE[mode], _lib.ptr(out.batch),
+              _lib.ptr(out.count), _lib.ptr(out.tokens), _lib.stream_ptr(stream))
+    return out
 
 
 class RequestTable:

@@ -361,7 +361,8 @@ def test_refresh_bit_exact(cuda):
     assert (dG == -1.0).all() and int(ref_flag.sum()) == 0
 
 
-def test_c5_replay_rolling_inserts_bit_exact(cuda):
+@pytest.mark.parametrize("kv,mode", [(None, "cut"), (12_000, "cut"), (12_000, "skip")])
+def test_c5_replay_rolling_inserts_bit_exact(cuda, kv, mode):
     """BASELINE configs[4] at test scale: trace replay with rolling bank inserts
     (completions evict the oldest records), admission predict, bucket
     refreshes and a full re-rank every round -- G and the order bit-exact vs an
@@ -420,19 +421,25 @@ def test_c5_replay_rolling_inserts_bit_exact(cuda):
                 s["bucket"] = s["g"] // 200
         G = np.array([st[int(i)]["G"] for i in act])
         perm = O.rank(G, act)
-        running = [int(act[p]) for p in perm[:B]]
-        expected.append((act, G, perm))
+        if kv is None:
+            running = [int(act[p]) for p in perm[:B]]
+        else:
+            b, _ = O.pack_batch(perm, [st[int(i)]["I"] for i in act],
+                                [st[int(i)]["g"] for i in act], kv, B, mode)
+            running = [int(act[i]) for i in b]
+        expected.append((act, G, perm, running))
         del head
 
     got = []
     stats = replay(w, tr, cfg, A, TOK, B, max_active=2048, rounds=R,
-                   on_round=lambda r, info: got.append(info))
-    assert stats.completed > 50 and stats.refreshed > 20
+                   on_round=lambda r, info: got.append(info), kv_capacity=kv, pack_mode=mode)
+    assert stats.completed > (50 if kv is None else 0) and stats.refreshed > (20 if kv is None else 0)
     assert len(got) == len(expected)
-    for (act, G, perm), info in zip(expected, got):
+    for (act, G, perm, running), info in zip(expected, got):
         assert np.array_equal(info["active_ids"], act)
         assert np.array_equal(info["G"], G)
         assert np.array_equal(info["perm"], perm)
+        assert info["running"] == running
 
 
 def test_c3_refresh_storm_full_size(cuda):
@@ -519,3 +526,60 @@ def test_sharded_round_world1_equals_single_gpu(cuda):
         assert torch.equal(G1, G0) and torch.equal(p1, p0)
     finally:
         dist.destroy_process_group()
+
+
+# ------------------------------------------- batch formation --
+@pytest.mark.parametrize("mode", ["cut", "skip"])
+@pytest.mark.parametrize("n,K,B", [(0, 8192, 64), (1, 8192, 64), (7, 20, 3), (1024, 8192, 64),
+                                   (3000, 60_000, 2000), (5000, 8192, 4096),
+                                   (200_000, 8192, 64), (200_000, 1 << 40, 5000)])
+def test_pack_batch_bit_exact(cuda, mode, n, K, B):
+    from paper_2603_07917_b200.scheduler import pack_batch
+    rng = np.random.default_rng(n + B)
+    Imax = min(4096, K - 1)
+    I = rng.integers(1, Imax + 1, n).astype(np.int32)
+    running = rng.random(n) < 0.4
+    g = np.where(running, rng.integers(0, 2049, n), 0).astype(np.int32)
+    perm = rng.permutation(n).astype(np.int64)
+    plan = pack_batch(_t(perm), _t(I), _t(g), K, B, mode)
+    batch, tokens = plan.host()
+    ref, ref_tokens = O.pack_batch(perm, I, g, K, B, mode)
+    assert batch.tolist() == ref and tokens == ref_tokens
+
+
+def test_pack_batch_cannot_fit(cuda):
+    from paper_2603_07917_b200.scheduler import pack_batch
+    I = np.array([5, 9000, 7, 9001], np.int32)
+    plan = pack_batch(_t(np.arange(4)), _t(I), _t(np.zeros(4, np.int32)), 8192, 64)
+    with pytest.raises(ValueError, match="request 1 cannot fit"):
+        plan.host()
+
+
+def test_trace_to_replay(cuda, tmp_path):
+    """Generated JSONL trace -> GPU feature-hash embedding (bit-exact vs the
+    reference hash) -> replay with KV-packed batches."""
+    from paper_2603_07917_b200.history import DEFAULT_SALT, HistoryWindow
+    from paper_2603_07917_b200.replay import replay
+    from paper_2603_07917_b200.scheduler import RoundConfig
+    from paper_2603_07917_b200.trace import (ClusterSpec, LengthLaw, WorkloadConfig,
+                                             generate_trace, load_trace, save_trace,
+                                             to_replay_trace)
+    rng = np.random.default_rng(5)
+    cl = tuple(ClusterSpec(tuple(int(x) for x in rng.integers(0, 50_000, 40)), 6,
+                           LengthLaw("lognormal", (float(rng.uniform(3, 6)), 0.5)))
+               for _ in range(12))
+    reqs = generate_trace(WorkloadConfig(lam=10.0, n_requests=1200, clusters=cl, seed=2))
+    f = tmp_path / "t.jsonl"
+    save_trace(reqs, str(f))
+    tr = to_replay_trace(load_trace(str(f)), dim=384)
+    ref = np.stack([O.embed_accumulate(r.prompt_tokens, DEFAULT_SALT, 384) for r in reqs[:50]])
+    assert np.array_equal(tr.emb[:50], ref.astype(np.int8))
+    w = HistoryWindow(400, 384)
+    w.push(tr.emb[:400], tr.true_len[:400], tr.inv[:400])
+    cfg = RoundConfig(k=16, theta=0.8, min_matches=5, max_len=2048, nbins=64)
+    batches = []
+    st = replay(w, tr, cfg, 50, 32, 64, max_active=1024, rounds=20,
+                on_round=lambda r, info: batches.append(info["running"]), kv_capacity=8192,
+                pack_mode="skip")
+    assert st.rounds == 20 and st.admitted == 1000
+    assert all(sum(tr.input_len[i] for i in b) <= 8192 for b in batches)

@@ -169,3 +169,24 @@ def test_rank_examples():
     assert list(O.rank(G, [0, 1])) == [1, 0]
     # ties -> id order
     assert list(O.rank([3.0, 3.0, 1.0], [7, 2, 9])) == [2, 1, 0]
+
+
+# ------------------------------------------- batch formation --
+def test_pack_batch_spec_examples():
+    from oracle import sagesched_oracle as O
+    # K = I1 + 1 exactly, two identical pending requests -> strictly serial
+    # (SPEC engine example "capacity forces serialization")
+    assert O.pack_batch([0, 1], [10, 10], [0, 0], 11, 64) == ([0], 11)
+    # count limit B
+    assert O.pack_batch(range(5), [1] * 5, [0] * 5, 100, 3) == ([0, 1, 2], 6)
+    # running requests project I + g + 1
+    assert O.pack_batch([1, 0], [5, 5], [0, 10], 100, 64) == ([1, 0], 16 + 6)
+    # cut vs skip: the big request blocks the cut scan, the skip scan passes it
+    # (request 1 is a running one whose KV grew to I + g = 35)
+    I, g = [3, 5, 4], [0, 30, 0]
+    assert O.pack_batch([0, 1, 2], I, g, 20, 64, "cut") == ([0], 4)
+    assert O.pack_batch([0, 1, 2], I, g, 20, 64, "skip") == ([0, 2], 9)
+    # a request with I + 1 > K can never run
+    with pytest.raises(ValueError, match="cannot fit"):
+        O.pack_batch([0], [20], [0], 20, 64)
+    assert O.pack_batch([], [], [], 8192, 64) == ([], 0)
