@@ -813,30 +813,98 @@ int launch_merge_finish(const uint64_t* partials, int nlists, int64_t nq, int k,
 }
 
 // ---------------------------------------------------------------------------
-// refresh: warp per running request (SPEC.md:345-353 cadence).
+// refresh (SPEC.md:345-353 cadence): RF_GL = 8 lanes per request, four
+// requests per warp, so the prefix scans are 3 shuffle steps and a ~50-point
+// law fills the lanes.  Same arithmetic, in the same order, as
+// warp_gittins_exact / oracle gittins_points:
+//   survivors  D_k > A2 c_k (a suffix: bin means increase with the bin)
+//   T = sum of surviving c;  C_k, P_k inclusive prefix sums over survivors
+//   r_k = (0.5 P_k + s_k (T - C_k)) / C_k,  s_k = 0.5 d_k / c_k,  G = min r_k
+//   no survivor -> cost(I, g + bucket) - cost(I, g)
+// Loops run to the warp's largest law, masked per group, so every shuffle
+// is warp-converged.
 // ---------------------------------------------------------------------------
+constexpr int RF_GL = 8;
+
+__device__ __forceinline__ long long grp_incl_scan_i64(long long v, int gl) {
+#pragma unroll
+  for (int o = 1; o < RF_GL; o <<= 1) {
+    const long long t = __shfl_up_sync(0xffffffffu, v, o, RF_GL);
+    if (gl >= o) v += t;
+  }
+  return v;
+}
+__device__ __forceinline__ long long grp_sum_i64(long long v) {
+#pragma unroll
+  for (int o = RF_GL / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
 __global__ void __launch_bounds__(256)
 k_refresh(int64_t n, const int32_t* __restrict__ I, const int32_t* __restrict__ g_new,
           int32_t* __restrict__ bucket_io, int bucket_size, const int32_t* __restrict__ npts,
           const int32_t* __restrict__ pcnt, const int64_t* __restrict__ pD, int P,
           double* __restrict__ G_io, uint8_t* __restrict__ refreshed, int force) {
-  const int lane = threadIdx.x & 31;
-  const int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (i >= n) return;
-  const int g = g_new[i];
+  const int lane = threadIdx.x & 31, gl = lane & (RF_GL - 1);
+  const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / RF_GL;
+  const bool live = i < n;
+  const int g = live ? g_new[i] : 0;
   const int nb = g / bucket_size;
-  const bool due = force || nb > bucket_io[i];
-  if (due) {
-    const long long Ii = I[i];
-    const long long A2 = (long long)g * g + 2 * Ii * g;
-    double v = warp_gittins_exact(pcnt + i * P, pD + i * P, npts[i], A2, (int)Ii, g, bucket_size,
-                                  lane);
-    if (lane == 0) {
+  const bool due = live && (force || nb > bucket_io[i]);
+  const int np = due ? npts[i] : 0;
+  int npmax = np;
+#pragma unroll
+  for (int o = 16; o >= RF_GL; o >>= 1) npmax = max(npmax, __shfl_xor_sync(0xffffffffu, npmax, o));
+  const long long Ii = live ? I[i] : 0;
+  const long long A2 = (long long)g * g + 2 * Ii * g;
+  const int32_t* c = pcnt + (live ? i : 0) * (int64_t)P;
+  const int64_t* D = pD + (live ? i : 0) * (int64_t)P;
+  // pass 1: total surviving count
+  long long T = 0;
+  for (int b = 0; b < npmax; b += RF_GL) {
+    const int k = b + gl;
+    if (k < np) {
+      const long long ck = c[k];
+      if (D[k] > A2 * ck) T += ck;
+    }
+  }
+  T = grp_sum_i64(T);
+  // pass 2: prefix sums and the ratio at every surviving point
+  long long Cc = 0, Pc = 0;
+  double best = INFINITY;
+  for (int b = 0; b < npmax; b += RF_GL) {
+    const int k = b + gl;
+    long long ck = 0, dk = 0;
+    if (k < np) {
+      const long long cv = c[k];
+      const long long dv = D[k] - A2 * cv;
+      if (dv > 0) { ck = cv; dk = dv; }
+    }
+    const long long C = grp_incl_scan_i64(ck, gl) + Cc;
+    const long long Pp = grp_incl_scan_i64(dk, gl) + Pc;
+    if (ck > 0) {
+      const double sk = __ddiv_rn(__dmul_rn((double)dk, 0.5), (double)ck);
+      const double num = __dadd_rn(__dmul_rn((double)Pp, 0.5), __dmul_rn(sk, (double)(T - C)));
+      best = fmin(best, __ddiv_rn(num, (double)C));
+    }
+    Cc = __shfl_sync(0xffffffffu, C, RF_GL - 1, RF_GL);
+    Pc = __shfl_sync(0xffffffffu, Pp, RF_GL - 1, RF_GL);
+  }
+#pragma unroll
+  for (int o = RF_GL / 2; o > 0; o >>= 1) best = fmin(best, __shfl_xor_sync(0xffffffffu, best, o));
+  if (gl == 0 && live) {
+    if (due) {
+      double v = best;
+      if (T == 0) {  // outlived every predicted length
+        const long long gb = (long long)g + bucket_size;
+        v = __dadd_rn(__dmul_rn((double)(gb * gb - (long long)g * g), 0.5),
+                      __dmul_rn((double)Ii, (double)bucket_size));
+      }
       G_io[i] = v;
       bucket_io[i] = nb;
     }
+    if (refreshed) refreshed[i] = due ? 1 : 0;
   }
-  if (lane == 0 && refreshed) refreshed[i] = due ? 1 : 0;
 }
 
 int launch_refresh(int64_t n, const int32_t* I, const int32_t* g_new, int32_t* bucket_io,
@@ -844,8 +912,9 @@ int launch_refresh(int64_t n, const int32_t* I, const int32_t* g_new, int32_t* b
                    int P, double* G_io, uint8_t* refreshed, int force, cudaStream_t st) {
   if (n <= 0) return SS_OK;
   count_launch();
-  k_refresh<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(n, I, g_new, bucket_io, bucket_size, npts,
-                                                      pcnt, pD, P, G_io, refreshed, force);
+  const int64_t per_block = 256 / RF_GL;
+  k_refresh<<<(unsigned)((n + per_block - 1) / per_block), 256, 0, st>>>(
+      n, I, g_new, bucket_io, bucket_size, npts, pcnt, pD, P, G_io, refreshed, force);
   SS_LAUNCH_CHECK();
   return SS_OK;
 }

@@ -3,10 +3,9 @@
 // assigned in arrival order).  Equivalently descending north-star index 1/G.
 //
 //   n <= 4096 : one CTA, bitonic sort of (orderable64(G), id, index) in smem
-//   n  > 4096 : LSD radix sort, 8-bit digits: 4 passes over the low 32 bits of
-//               id, then 8 passes over orderable64(G); each pass is
-//               histogram -> exclusive scan -> stable scatter (warp match_any
-//               ranking), so ties keep id order.
+//   n <= 8192 : rank by counting (8 lanes per request)
+//   n  > 8192 : onesweep LSD radix sort (see below), stable, ties keep id
+//               order.
 #include "ss_common.cuh"
 #include "ss_internal.h"
 
@@ -99,150 +98,271 @@ k_rank_count(const double* __restrict__ G, const int64_t* __restrict__ ids, int 
 }
 
 // ---------------------------------------------------------------- radix ----
+// n > 8192: onesweep LSD radix sort of (id, orderable64(G)) -- 16 passes of
+// 8-bit digits over the 128-bit key (id digits first, then G digits), stable,
+// so the result is ascending (G, id).
+//   1. k_os_init   one read of G/ids: key/id/index arrays + all 16 digit
+//                  histograms (block-private smem, then global atomics)
+//   2. k_os_scan   per-pass exclusive digit offsets; a pass whose digit is
+//                  constant over all keys is marked trivial and skipped (the
+//                  high id bytes and the sign/exponent byte of G usually are),
+//                  with the ping-pong parity of every pass resolved here
+//   3. k_os_pass   x16: tiles of 2048 keys claimed in order, warp-striped
+//                  match_any ranks, per-digit decoupled look-back across tiles
+//                  (flag in the top 2 bits of a 32-bit status word), one
+//                  stable scatter -- no separate histogram/scan launches
+//   4. k_os_out    perm = final index array
 constexpr int RT_THREADS = 256;
 constexpr int RT_ITEMS = 8;
 constexpr int RT_TILE = RT_THREADS * RT_ITEMS;
+constexpr int OS_PASSES = 16;
+constexpr int OS_SMEM = RT_TILE * (8 + 8 + 4);
+constexpr uint32_t OS_AGG = 1u << 30, OS_PRE = 2u << 30, OS_VAL = (1u << 30) - 1;
 
-__global__ void k_rank_init(const double* __restrict__ G, const int64_t* __restrict__ ids,
-                            int64_t n, uint64_t* __restrict__ key, uint32_t* __restrict__ id32,
-                            uint32_t* __restrict__ idx) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  key[i] = f64_order(G[i]);
-  id32[i] = ids ? (uint32_t)ids[i] : (uint32_t)i;
-  idx[i] = (uint32_t)i;
+struct OsMeta {
+  uint32_t trivial[OS_PASSES];
+  uint32_t src[OS_PASSES + 1];  // source buffer of each pass; src[16] = final
+};
+
+__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed(uint32_t* p, uint32_t v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
 }
 
-__device__ __forceinline__ int digit_of(uint64_t key, uint32_t id, int pass) {
-  return pass < 4 ? (int)((id >> (8 * pass)) & 255u) : (int)((key >> (8 * (pass - 4))) & 255ull);
+__device__ __forceinline__ int os_digit(uint64_t key, uint64_t id, int pass) {
+  return pass < 8 ? (int)((id >> (8 * pass)) & 255u) : (int)((key >> (8 * (pass - 8))) & 255u);
 }
 
 __global__ void __launch_bounds__(RT_THREADS)
-k_radix_hist(const uint64_t* __restrict__ key, const uint32_t* __restrict__ id32, int64_t n,
-             int pass, int nblocks, uint32_t* __restrict__ bhist) {
-  __shared__ uint32_t h[256];
-  h[threadIdx.x] = 0;
+k_os_init(const double* __restrict__ G, const int64_t* __restrict__ ids, int64_t n,
+          uint64_t* __restrict__ key, uint64_t* __restrict__ idk, uint32_t* __restrict__ idx,
+          uint32_t* __restrict__ ghist, uint32_t* __restrict__ unsorted) {
+  __shared__ uint32_t h[OS_PASSES][256];
+  __shared__ int s_uns;
+  if (threadIdx.x == 0) s_uns = 0;
+  for (int i = threadIdx.x; i < OS_PASSES * 256; i += RT_THREADS) (&h[0][0])[i] = 0;
   __syncthreads();
-  const int lane = threadIdx.x & 31;
   const int64_t base = (int64_t)blockIdx.x * RT_TILE;
   for (int it = 0; it < RT_ITEMS; ++it) {
-    int64_t i = base + (int64_t)it * RT_THREADS + threadIdx.x;
-    bool live = i < n;
-    int d = live ? digit_of(key[i], id32[i], pass) : 0;
-    unsigned am = __ballot_sync(0xffffffffu, live);
-    if (live) {
-      unsigned peers = __match_any_sync(am, d);
-      if ((peers & ((1u << lane) - 1u)) == 0u) atomicAdd(&h[d], __popc(peers));
-    }
+    const int64_t i = base + (int64_t)it * RT_THREADS + threadIdx.x;
+    if (i >= n) break;
+    const uint64_t k = f64_order(G[i]);
+    // signed id -> order-preserving unsigned
+    const uint64_t d = (uint64_t)(ids ? ids[i] : i) ^ 0x8000000000000000ull;
+    key[i] = k;
+    idk[i] = d;
+    idx[i] = (uint32_t)i;
+    // ids already ascending in input order -> the id passes are no-ops for a
+    // stable sort (detected here, applied in k_os_scan)
+    if (ids && i > 0 && ids[i - 1] > ids[i]) s_uns = 1;
+#pragma unroll
+    for (int p = 0; p < OS_PASSES; ++p) atomicAdd(&h[p][os_digit(k, d, p)], 1u);
   }
   __syncthreads();
-  bhist[threadIdx.x * nblocks + blockIdx.x] = h[threadIdx.x];  // digit-major
+  for (int i = threadIdx.x; i < OS_PASSES * 256; i += RT_THREADS) {
+    const uint32_t c = (&h[0][0])[i];
+    if (c) atomicAdd(&ghist[i], c);
+  }
+  if (threadIdx.x == 0 && s_uns) atomicOr(unsorted, 1u);
 }
 
-// exclusive scan of 256*nblocks counters (digit-major) in one CTA
-__global__ void __launch_bounds__(1024)
-k_radix_scan(uint32_t* __restrict__ bhist, int total) {
-  __shared__ uint32_t s_warp[32];
-  __shared__ uint32_t s_carry;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) s_carry = 0;
+// one CTA: ghist[p][d] -> exclusive offsets in place; trivial passes; parities
+__global__ void __launch_bounds__(256)
+k_os_scan(uint32_t* __restrict__ ghist, int64_t n, const uint32_t* __restrict__ unsorted,
+          OsMeta* __restrict__ meta) {
+  __shared__ uint32_t s_warp[OS_PASSES][8];
+  __shared__ int s_triv[OS_PASSES];
+  const int d = threadIdx.x, lane = d & 31, warp = d >> 5;
+  uint32_t hv[OS_PASSES];
+#pragma unroll
+  for (int p = 0; p < OS_PASSES; ++p) hv[p] = ghist[p * 256 + d];  // all loads in flight
+  if (d < OS_PASSES) s_triv[d] = 0;
   __syncthreads();
-  for (int b0 = 0; b0 < total; b0 += 1024) {
-    int i = b0 + threadIdx.x;
-    uint32_t v = i < total ? bhist[i] : 0;
+#pragma unroll
+  for (int p = 0; p < OS_PASSES; ++p) {
+    const uint32_t v = hv[p];
+    if ((int64_t)v == n) s_triv[p] = 1;  // one digit holds every key
     uint32_t x = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      uint32_t t = __shfl_up_sync(0xffffffffu, x, o);
+      const uint32_t t = __shfl_up_sync(0xffffffffu, x, o);
       if (lane >= o) x += t;
     }
-    if (lane == 31) s_warp[warp] = x;
-    __syncthreads();
-    if (warp == 0) {
-      uint32_t y = s_warp[lane];
+    if (lane == 31) s_warp[p][warp] = x;
+    hv[p] = x - v;
+  }
+  __syncthreads();
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        uint32_t t = __shfl_up_sync(0xffffffffu, y, o);
-        if (lane >= o) y += t;
-      }
-      s_warp[lane] = y;
+  for (int p = 0; p < OS_PASSES; ++p) {
+    uint32_t pre = 0;
+    for (int w = 0; w < warp; ++w) pre += s_warp[p][w];
+    ghist[p * 256 + d] = pre + hv[p];
+  }
+  if (d == 0) {
+    // ids already ascending in input order: the stable key passes alone
+    // produce (G, id) order, so the id passes are skipped
+    const bool ids_sorted = *unsorted == 0u;
+    uint32_t par = 0;
+    for (int p = 0; p < OS_PASSES; ++p) {
+      const int triv = s_triv[p] || (p < 8 && ids_sorted);
+      meta->trivial[p] = (uint32_t)triv;
+      meta->src[p] = par;
+      if (!triv) par ^= 1u;
     }
-    __syncthreads();
-    uint32_t pre = (warp ? s_warp[warp - 1] : 0) + s_carry;
-    if (i < total) bhist[i] = pre + x - v;
-    __syncthreads();
-    if (threadIdx.x == 1023) s_carry = pre + x;
-    __syncthreads();
+    meta->src[OS_PASSES] = par;
   }
 }
 
 __global__ void __launch_bounds__(RT_THREADS)
-k_radix_scatter(const uint64_t* __restrict__ key, const uint32_t* __restrict__ id32,
-                const uint32_t* __restrict__ idx, int64_t n, int pass, int nblocks,
-                const uint32_t* __restrict__ offs, uint64_t* __restrict__ okey,
-                uint32_t* __restrict__ oid, uint32_t* __restrict__ oidx) {
+k_os_pass(uint64_t* __restrict__ key0, uint64_t* __restrict__ key1, uint64_t* __restrict__ id0,
+          uint64_t* __restrict__ id1, uint32_t* __restrict__ ix0, uint32_t* __restrict__ ix1,
+          int64_t n, int pass, const uint32_t* __restrict__ gofs, uint32_t* __restrict__ status,
+          uint32_t* __restrict__ tile_ctr, const OsMeta* __restrict__ meta) {
+  if (meta->trivial[pass]) return;
   __shared__ uint32_t cnt[RT_THREADS / 32][256];
+  __shared__ uint32_t s_excl[256];   // global offset of the tile's run of each digit
+  __shared__ uint32_t s_tstart[256]; // start of each digit's run inside the tile
+  __shared__ uint32_t s_wsum[RT_THREADS / 32];
+  __shared__ int s_tile;
+  extern __shared__ __align__(16) unsigned char os_smem[];
+  uint64_t* skey = reinterpret_cast<uint64_t*>(os_smem);  // tile sorted by digit
+  uint64_t* sidk = skey + RT_TILE;
+  uint32_t* six = reinterpret_cast<uint32_t*>(sidk + RT_TILE);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool flip = meta->src[pass] != 0;
+  const uint64_t* key = flip ? key1 : key0;
+  const uint64_t* idk = flip ? id1 : id0;
+  const uint32_t* idx = flip ? ix1 : ix0;
+  uint64_t* okey = flip ? key0 : key1;
+  uint64_t* oid = flip ? id0 : id1;
+  uint32_t* oidx = flip ? ix0 : ix1;
+  if (threadIdx.x == 0) s_tile = (int)atomicAdd(tile_ctr, 1u);
   for (int d = lane; d < 256; d += 32) cnt[warp][d] = 0;
-  __syncwarp();
-  const int64_t base = (int64_t)blockIdx.x * RT_TILE + (int64_t)warp * (RT_TILE / 8);
-  uint64_t k_[RT_ITEMS];
-  uint32_t id_[RT_ITEMS], ix_[RT_ITEMS], rk[RT_ITEMS];
+  __syncthreads();
+  const int tile = s_tile;
+  const int64_t base = (int64_t)tile * RT_TILE + (int64_t)warp * (RT_TILE / 8);
+  uint64_t k_[RT_ITEMS], d_[RT_ITEMS];
+  uint32_t ix_[RT_ITEMS], rk[RT_ITEMS];
   int dg[RT_ITEMS];
 #pragma unroll
   for (int it = 0; it < RT_ITEMS; ++it) {
-    int64_t i = base + it * 32 + lane;
-    bool live = i < n;
+    const int64_t i = base + it * 32 + lane;
+    const bool live = i < n;
     k_[it] = live ? key[i] : 0;
-    id_[it] = live ? id32[i] : 0;
+    d_[it] = live ? idk[i] : 0;
     ix_[it] = live ? idx[i] : 0;
-    int d = live ? digit_of(k_[it], id_[it], pass) : 0;
+  }
+  const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+  for (int it = 0; it < RT_ITEMS; ++it) {
+    const int64_t i = base + it * 32 + lane;
+    const bool live = i < n;
+    const int d = os_digit(k_[it], d_[it], pass);
     dg[it] = live ? d : -1;
-    unsigned am = __ballot_sync(0xffffffffu, live);
+    const unsigned am = __ballot_sync(0xffffffffu, live);
     uint32_t r = 0;
     if (live) {
-      unsigned peers = __match_any_sync(am, d);
-      uint32_t before = cnt[warp][d];
-      r = before + __popc(peers & ((1u << lane) - 1u));
+      const unsigned peers = __match_any_sync(am, d);
+      const uint32_t before = cnt[warp][d];
+      r = before + __popc(peers & lt);
       __syncwarp(am);
-      if ((peers & ((1u << lane) - 1u)) == 0u) cnt[warp][d] = before + __popc(peers);
+      if ((peers & lt) == 0u) cnt[warp][d] = before + __popc(peers);
     }
     __syncwarp();
     rk[it] = r;
   }
   __syncthreads();
-  // per-digit exclusive scan across warps -> cnt[w][d] becomes warp offset
+  // per digit: warp offsets within the tile, tile count, look-back
   {
-    const int d = threadIdx.x;  // 256 threads, 256 digits
+    const int d = threadIdx.x;
     uint32_t run = 0;
 #pragma unroll
     for (int w = 0; w < RT_THREADS / 32; ++w) {
-      uint32_t c = cnt[w][d];
+      const uint32_t c = cnt[w][d];
       cnt[w][d] = run;
       run += c;
     }
+    uint32_t* st = status + (size_t)tile * 256 + d;
+    if (tile == 0) {
+      st_relaxed(st, OS_PRE | run);
+      s_excl[d] = 0;
+    } else {
+      st_relaxed(st, OS_AGG | run);
+      // look back 8 predecessors per round trip (independent loads in flight)
+      uint32_t excl = 0;
+      bool found = false;
+      for (int t0 = tile - 1; t0 >= 0 && !found; t0 -= 8) {
+        uint32_t v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          v[u] = (t0 - u >= 0) ? ld_relaxed(status + (size_t)(t0 - u) * 256 + d) : OS_PRE;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (found) break;
+          while ((v[u] & ~OS_VAL) == 0u) v[u] = ld_relaxed(status + (size_t)(t0 - u) * 256 + d);
+          if (t0 - u >= 0) excl += v[u] & OS_VAL;
+          if (v[u] & OS_PRE) found = true;
+        }
+      }
+      st_relaxed(st, OS_PRE | (excl + run));
+      s_excl[d] = excl;
+    }
+    // exclusive scan of the tile counts over digits -> run starts in the tile
+    uint32_t x = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += t;
+    }
+    if (lane == 31) s_wsum[warp] = x;
+    __syncthreads();
+    uint32_t pre = 0;
+    for (int w = 0; w < warp; ++w) pre += s_wsum[w];
+    s_tstart[d] = pre + x - run;
+    s_excl[d] += gofs[pass * 256 + d];
   }
   __syncthreads();
+  // stage the tile in digit order, then write each digit's run contiguously
 #pragma unroll
   for (int it = 0; it < RT_ITEMS; ++it) {
     if (dg[it] < 0) continue;
-    int d = dg[it];
-    uint32_t pos = offs[d * nblocks + blockIdx.x] + cnt[warp][d] + rk[it];
-    okey[pos] = k_[it];
-    oid[pos] = id_[it];
-    oidx[pos] = ix_[it];
+    const int d = dg[it];
+    const uint32_t lp = s_tstart[d] + cnt[warp][d] + rk[it];
+    skey[lp] = k_[it];
+    sidk[lp] = d_[it];
+    six[lp] = ix_[it];
+  }
+  __syncthreads();
+  const int tn = (int)min((int64_t)RT_TILE, n - (int64_t)tile * RT_TILE);
+  for (int j = threadIdx.x; j < tn; j += RT_THREADS) {
+    const uint64_t kk = skey[j], dd = sidk[j];
+    const int d = os_digit(kk, dd, pass);
+    const uint32_t pos = s_excl[d] + (uint32_t)j - s_tstart[d];
+    okey[pos] = kk;
+    oid[pos] = dd;
+    oidx[pos] = six[j];
   }
 }
 
-__global__ void k_rank_out(const uint32_t* __restrict__ idx, int64_t n, int64_t* __restrict__ perm) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) perm[i] = idx[i];
+__global__ void k_os_out(const uint32_t* __restrict__ ix0, const uint32_t* __restrict__ ix1,
+                         int64_t n, const OsMeta* __restrict__ meta, int64_t* __restrict__ perm) {
+  const uint32_t* ix = meta->src[OS_PASSES] ? ix1 : ix0;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) perm[i] = ix[i];
+}
+
+static size_t os_zeroed_bytes(int64_t ntiles) {
+  return ((size_t)OS_PASSES * 256 + (size_t)OS_PASSES * ntiles * 256 + OS_PASSES + 1) * 4;
 }
 
 int64_t rank_workspace_bytes(int64_t n) {
   if (n <= SMALL_SORT_MAX) return 256;
-  int64_t nblocks = (n + RT_TILE - 1) / RT_TILE;
-  return 2 * n * (8 + 4 + 4) + 256 * nblocks * 4 + 1024;
+  const int64_t ntiles = (n + RT_TILE - 1) / RT_TILE;
+  return 2 * n * (8 + 8 + 4) + (int64_t)os_zeroed_bytes(ntiles) + (int64_t)sizeof(OsMeta) + 1024;
 }
 
 int launch_rank(const double* G, const int64_t* ids, int64_t n, int64_t* perm, void* ws,
@@ -265,40 +385,44 @@ int launch_rank(const double* G, const int64_t* ids, int64_t n, int64_t* perm, v
     SS_LAUNCH_CHECK();
     return SS_OK;
   }
-  if (n > 0x7fffffffLL) return set_error(SS_ERR_UNSUPPORTED, "rank n too large");
+  if (n >= (int64_t)OS_VAL) return set_error(SS_ERR_UNSUPPORTED, "rank n too large");
   if (ws_bytes < rank_workspace_bytes(n))
     return set_error(SS_ERR_ARG, "rank workspace too small (%lld < %lld)", (long long)ws_bytes,
                      (long long)rank_workspace_bytes(n));
-  const int nblocks = (int)((n + RT_TILE - 1) / RT_TILE);
+  const int ntiles = (int)((n + RT_TILE - 1) / RT_TILE);
   unsigned char* p = reinterpret_cast<unsigned char*>(ws);
-  uint64_t* key[2];
-  uint32_t* id[2];
-  uint32_t* ix[2];
-  key[0] = reinterpret_cast<uint64_t*>(p); p += n * 8;
-  key[1] = reinterpret_cast<uint64_t*>(p); p += n * 8;
-  id[0] = reinterpret_cast<uint32_t*>(p); p += n * 4;
-  id[1] = reinterpret_cast<uint32_t*>(p); p += n * 4;
-  ix[0] = reinterpret_cast<uint32_t*>(p); p += n * 4;
-  ix[1] = reinterpret_cast<uint32_t*>(p); p += n * 4;
-  uint32_t* bhist = reinterpret_cast<uint32_t*>(p);
+  uint64_t *key0, *key1, *id0, *id1;
+  uint32_t *ix0, *ix1;
+  key0 = reinterpret_cast<uint64_t*>(p); p += n * 8;
+  key1 = reinterpret_cast<uint64_t*>(p); p += n * 8;
+  id0 = reinterpret_cast<uint64_t*>(p); p += n * 8;
+  id1 = reinterpret_cast<uint64_t*>(p); p += n * 8;
+  ix0 = reinterpret_cast<uint32_t*>(p); p += n * 4;
+  ix1 = reinterpret_cast<uint32_t*>(p); p += n * 4;
+  p = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(p) + 255) & ~(uintptr_t)255);
+  uint32_t* ghist = reinterpret_cast<uint32_t*>(p);           // [16][256]
+  uint32_t* status = ghist + OS_PASSES * 256;                 // [16][ntiles][256]
+  uint32_t* tctr = status + (size_t)OS_PASSES * ntiles * 256;  // [16]
+  uint32_t* unsorted = tctr + OS_PASSES;                      // [1]
+  OsMeta* meta = reinterpret_cast<OsMeta*>(
+      (reinterpret_cast<uintptr_t>(unsorted + 1) + 15) & ~(uintptr_t)15);
+  SS_CUDA_TRY(cudaFuncSetAttribute(k_os_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, OS_SMEM));
+  SS_CUDA_TRY(cudaMemsetAsync(ghist, 0, os_zeroed_bytes(ntiles), st));
   count_launch();
-  k_rank_init<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(G, ids, n, key[0], id[0], ix[0]);
+  k_os_init<<<ntiles, RT_THREADS, 0, st>>>(G, ids, n, key0, id0, ix0, ghist, unsorted);
   SS_LAUNCH_CHECK();
-  int cur = 0;
-  for (int pass = 0; pass < 12; ++pass) {
-    if (pass < 4 && ids == nullptr) continue;  // identity ids: input already in id order
+  count_launch();
+  k_os_scan<<<1, 256, 0, st>>>(ghist, n, unsorted, meta);
+  SS_LAUNCH_CHECK();
+  for (int pass = 0; pass < OS_PASSES; ++pass) {
     count_launch();
-    k_radix_hist<<<nblocks, RT_THREADS, 0, st>>>(key[cur], id[cur], n, pass, nblocks, bhist);
-    count_launch();
-    k_radix_scan<<<1, 1024, 0, st>>>(bhist, 256 * nblocks);
-    count_launch();
-    k_radix_scatter<<<nblocks, RT_THREADS, 0, st>>>(key[cur], id[cur], ix[cur], n, pass, nblocks,
-                                                     bhist, key[cur ^ 1], id[cur ^ 1], ix[cur ^ 1]);
+    k_os_pass<<<ntiles, RT_THREADS, OS_SMEM, st>>>(key0, key1, id0, id1, ix0, ix1, n, pass, ghist,
+                                             status + (size_t)pass * ntiles * 256, tctr + pass,
+                                             meta);
     SS_LAUNCH_CHECK();
-    cur ^= 1;
   }
   count_launch();
-  k_rank_out<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(ix[cur], n, perm);
+  k_os_out<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(ix0, ix1, n, meta, perm);
   SS_LAUNCH_CHECK();
   return SS_OK;
 }

@@ -483,7 +483,7 @@ def test_c3_refresh_storm_full_size(cuda):
         assert Gh[i] == O.gittins_points(c, D, int(I[i]), int(g[i])), i
 
 
-@pytest.mark.parametrize("n", [1, 7, 1024, 4096, 4097, 200_000])
+@pytest.mark.parametrize("n", [1, 7, 1024, 4096, 4097, 8192, 8193, 20_000, 200_000, 1_000_003])
 def test_rank_bit_exact(cuda, n):
     from paper_2603_07917_b200.scheduler import rank
     rng = np.random.default_rng(n)
@@ -493,6 +493,22 @@ def test_rank_bit_exact(cuda, n):
     assert np.array_equal(perm, O.rank(G, ids))
     perm = rank(_t(G)).cpu().numpy()
     assert np.array_equal(perm, O.rank(G, np.arange(n)))
+    # ascending ids (the onesweep skips its id passes) with gaps
+    sids = np.cumsum(rng.integers(1, 5, n)).astype(np.int64)
+    perm = rank(_t(G), _t(sids)).cpu().numpy()
+    assert np.array_equal(perm, O.rank(G, sids))
+
+
+def test_rank_special_values(cuda):
+    """inf (no law yet), zero, wide exponent range, negative and > 2^32 ids."""
+    from paper_2603_07917_b200.scheduler import rank
+    rng = np.random.default_rng(9)
+    n = 50_000
+    G = rng.choice(np.array([np.inf, 0.0, 1e-300, 1e300, 2.0, 2.0, 5e3, 7.25]), n)
+    ids = rng.integers(-(1 << 40), 1 << 40, n).astype(np.int64)
+    ids[:10] = ids[10]  # duplicate ids: index order breaks the tie (stable)
+    perm = rank(_t(G), _t(ids)).cpu().numpy()
+    assert np.array_equal(perm, np.lexsort((np.arange(n), ids, G)))
 
 
 # ---------------------------------------------------- sharded round (N=1) ---
