@@ -269,7 +269,8 @@ k_topk_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUten
   uint64_t* empty = full + stages;
   uint64_t* tfull = empty + stages;
   uint64_t* tempty = tfull + 2;
-  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* mdone = tempty + 2;
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(mdone + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = (CG == 2) ? cluster_rank() : 0u;
@@ -292,6 +293,7 @@ k_topk_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUten
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], 4 * CG);  // one arrive per epilogue warp of the pair
     }
+    mbar_init(mdone, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 1) tmem_alloc512<CG>(s_tmem);
@@ -342,8 +344,10 @@ k_topk_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUten
       int it = 0;
       for (int t = 0; t < ntiles; ++t) {
         const int acc = t & 1;
-        if constexpr (CG == 2) mbar_wait_cluster(&tempty[acc], ((t >> 1) & 1) ^ 1);
-        else mbar_wait(&tempty[acc], ((t >> 1) & 1) ^ 1);
+        if (!(dbg & 64)) {  // debug bit 64: MMA issue alone, no epilogue hand-off
+          if constexpr (CG == 2) mbar_wait_cluster(&tempty[acc], ((t >> 1) & 1) ^ 1);
+          else mbar_wait(&tempty[acc], ((t >> 1) & 1) ^ 1);
+        }
         tc_fence_after();
         const uint32_t d = tmem + acc * tc::BN;
         for (int kb = 0; kb < nkb; ++kb, ++it) {
@@ -359,6 +363,10 @@ k_topk_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUten
           tc_commit<CG>(&empty[s]);  // frees the B stage (in both CTAs) once these MMAs retire
         }
         tc_commit<CG>(&tfull[acc]);  // accumulator ready for the epilogue(s)
+      }
+      if (dbg & 64) {  // nobody drains: wait for the last MMAs before teardown
+        tc_commit<CG>(mdone);
+        mbar_wait(mdone, 0);
       }
     }
   } else {
@@ -390,11 +398,12 @@ k_topk_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUten
         for (int u = 0; u < 8; ++u) pre[u] = (r0 + u < n_rows) ? inv[r0 + u] : NaNf;
       }
     };
-    if (ntiles > 0) fetch_iw(0);
+    const int ntiles_epi = (dbg & 64) ? 0 : ntiles;
+    if (ntiles_epi > 0) fetch_iw(0);
     // conservative s-domain filter: admits every row whose exact key can reach
     // the current k-th best (or theta while the heap fills)
     float thr = (iq == iq) ? s_threshold(theta, iq) : INFINITY;
-    for (int t = 0; t < ntiles; ++t) {
+    for (int t = 0; t < ntiles_epi; ++t) {
       const int acc = t & 1;
       const int64_t row0 = (tile0 + t) * tc::BN;
       float* ciw = wiw + (t & 1) * tc::BN;

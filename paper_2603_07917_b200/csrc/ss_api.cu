@@ -94,6 +94,11 @@ struct ss_bank {
   size_t ws_bytes = 0;
   uint32_t* gthr = nullptr;  // per-query shared k-th-key bound for the top-k slices
   int64_t gthr_cap = 0;
+  // side stream of the fused round: the fallback histogram runs concurrently
+  // with the similarity kernel (fork/join by events; captured as two graph
+  // branches when the caller's stream is being captured)
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
 // grow-on-demand (call once outside CUDA-graph capture); nullptr on failure
@@ -241,6 +246,9 @@ int ss_bank_create(ss_bank_t** out, int32_t device, int64_t capacity, int32_t di
   else if ((e = cudaMalloc(&h->seq, (size_t)capacity * 8)) != cudaSuccess) fail(e);
   else if ((e = cudaMalloc(&h->len_cnt, 65536 * 4)) != cudaSuccess) fail(e);
   else if ((e = cudaMalloc(&h->d_err, sizeof(int))) != cudaSuccess) fail(e);
+  else if ((e = cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking)) != cudaSuccess) fail(e);
+  else if ((e = cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming)) != cudaSuccess) fail(e);
+  else if ((e = cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming)) != cudaSuccess) fail(e);
   if (rc == SS_OK) {
     cudaMemset(h->emb, 0, (size_t)capacity * dim);
     cudaMemset(h->inv, 0xff, (size_t)capacity * 4);  // NaN: never matches
@@ -270,6 +278,9 @@ int ss_bank_destroy(ss_bank_t* h) {
   cudaFree(h->d_err);
   cudaFree(h->ws);
   cudaFree(h->gthr);
+  if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+  if (h->ev_join) cudaEventDestroy(h->ev_join);
+  if (h->side) cudaStreamDestroy(h->side);
   delete h;
   return SS_OK;
 }
@@ -505,10 +516,16 @@ static int round_impl(ss_bank* h, const int8_t* q, const float* q_inv, const int
   int slices = 1;
   if (int rc = topk_plan(h, a, algo, slices)) return rc;
   uint64_t* partials = reinterpret_cast<uint64_t*>((char*)h->ws + base + L.end);
-  int rc = (algo == SS_ALGO_TCGEN05) ? launch_topk_tc(a, partials, slices, st)
-                                     : launch_topk_scan(a, partials, slices, st);
+  // fork: the window's fallback law (1 CTA) overlaps the similarity kernel,
+  // which leaves SMs free (slices x query tiles <= the SM count)
+  SS_CUDA_TRY(cudaEventRecord(h->ev_fork, st));
+  SS_CUDA_TRY(cudaStreamWaitEvent(h->side, h->ev_fork, 0));
+  int rc = launch_fallback_hist(h->len_cnt, max_len, nbins, fb, fb + nbins, fb + 2 * nbins, h->side);
   if (rc) return rc;
-  rc = launch_fallback_hist(h->len_cnt, max_len, nbins, fb, fb + nbins, fb + 2 * nbins, st);
+  SS_CUDA_TRY(cudaEventRecord(h->ev_join, h->side));
+  rc = (algo == SS_ALGO_TCGEN05) ? launch_topk_tc(a, partials, slices, st)
+                                 : launch_topk_scan(a, partials, slices, st);
+  SS_CUDA_TRY(cudaStreamWaitEvent(st, h->ev_join, 0));  // join before any early return
   if (rc) return rc;
   rc = launch_merge_finish(partials, slices, nq, k, h->lens, h->head, h->gcap, h->slot_offset, comp,
                            len, min_matches, max_len, nbins, input_len, fb, fb + nbins,
