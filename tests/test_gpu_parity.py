@@ -276,6 +276,52 @@ def test_round_c1_bit_exact(cuda, algo, nbins, theta):
     assert np.array_equal(Gh, Gr) and np.array_equal(ph, O.rank(Gr, ids))
 
 
+def test_round_host_graph_replay(cuda):
+    """The plugin call with pinned host buffers: calls 1-2 run eagerly, the
+    repeat is captured and later calls replay one graph (H2D + round + D2H).
+    New buffer contents and a bank push (head moves) must be honoured."""
+    from paper_2603_07917_b200.history import HistoryWindow
+    from paper_2603_07917_b200.scheduler import RoundConfig, SageScheduler
+    n, nq, k, nbins = 10_000, 300, 32, 64
+    emb, lens, _, _ = O.make_bank(n + 500 + 2 * nq, 384, 100, 13)
+    w = HistoryWindow(12_000, 384)
+    w.push(emb[:n], lens[:n])
+    qa, qb = emb[n + 500:n + 500 + nq], emb[n + 500 + nq:]
+    rng = np.random.default_rng(4)
+    I = rng.integers(1, 4097, nq).astype(np.int32)
+    ids = np.arange(nq, dtype=np.int64)
+    s = SageScheduler(w, RoundConfig(k=k, theta=0.8, min_matches=20, max_len=2048, nbins=nbins))
+
+    def pin(a):
+        return torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+
+    hq, hqi, hI, hids = pin(qa), pin(O.inv_norm(qa)), pin(I), pin(ids)
+    G = torch.empty(nq, dtype=torch.float64).pin_memory().numpy()
+    perm = torch.empty(nq, dtype=torch.int64).pin_memory().numpy()
+
+    def expect(q, nb):
+        be, bl = emb[:nb], lens[:nb]
+        keys = O.scores(q, O.inv_norm(q), be, O.inv_norm(be))
+        ref = O.predict_round(keys, np.arange(nb), bl, I, k, 0.8, 20, 2048, nbins, window_lens=bl)
+        Gr = np.array([r["G"] for r in ref])
+        return Gr, O.rank(Gr, ids)
+
+    Ga, pa = expect(qa, n)
+    Gb, pb = expect(qb, n)
+    for it in range(5):
+        q = qb if it == 3 else qa
+        hq[:] = q
+        hqi[:] = O.inv_norm(q)
+        s.schedule_round_host(hq, hqi, hI, hids, G, perm)
+        Gr, pr = (Gb, pb) if it == 3 else (Ga, pa)
+        assert np.array_equal(G, Gr) and np.array_equal(perm, pr), it
+    w.push(emb[n:n + 500], lens[n:n + 500])
+    Gc, pc = expect(qa, n + 500)
+    for it in range(3):
+        s.schedule_round_host(hq, hqi, hI, hids, G, perm)
+        assert np.array_equal(G, Gc) and np.array_equal(perm, pc), it
+
+
 def test_round_fallback_and_cold_start(cuda):
     from paper_2603_07917_b200 import _lib
     from paper_2603_07917_b200.history import HistoryWindow
