@@ -258,7 +258,7 @@ int ss_bank_create(ss_bank_t** out, int32_t device, int64_t capacity, int32_t di
   };
   cudaError_t e;
   if ((e = cudaMalloc(&h->emb, (size_t)capacity * dim)) != cudaSuccess) fail(e);
-  else if ((e = cudaMalloc(&h->inv, (size_t)capacity * 4)) != cudaSuccess) fail(e);
+  else if ((e = cudaMalloc(&h->inv, ((size_t)capacity + 256) * 4)) != cudaSuccess) fail(e);
   else if ((e = cudaMalloc(&h->lens, (size_t)capacity * 4)) != cudaSuccess) fail(e);
   else if ((e = cudaMalloc(&h->seq, (size_t)capacity * 8)) != cudaSuccess) fail(e);
   else if ((e = cudaMalloc(&h->len_cnt, 65536 * 4)) != cudaSuccess) fail(e);
@@ -268,7 +268,7 @@ int ss_bank_create(ss_bank_t** out, int32_t device, int64_t capacity, int32_t di
   else if ((e = cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming)) != cudaSuccess) fail(e);
   if (rc == SS_OK) {
     cudaMemset(h->emb, 0, (size_t)capacity * dim);
-    cudaMemset(h->inv, 0xff, (size_t)capacity * 4);  // NaN: never matches
+    cudaMemset(h->inv, 0xff, ((size_t)capacity + 256) * 4);  // NaN: never matches (+1 tile pad)
     cudaMemset(h->lens, 0, (size_t)capacity * 4);
     cudaMemset(h->seq, 0xff, (size_t)capacity * 8);  // -1: empty slot
     cudaMemset(h->len_cnt, 0, 65536 * 4);
@@ -390,6 +390,7 @@ static int topk_plan(ss_bank* h, const TopkArgs& a, int32_t& algo, int& slices) 
 static size_t topk_ws_need(ss_bank* h, int64_t nq, int32_t k, int32_t algo) {
   TopkArgs a{nullptr, nullptr, nq, h->emb, h->inv, h->cap, h->dim, k, 0.f, h->head, h->gcap,
              h->slot_offset};
+  a.inv_padded = true;  // the bank pads inv with one NaN tile
   int slices = 1;
   if (topk_plan(h, a, algo, slices)) return 0;
   return align_up((size_t)slices * nq * k * 8);
@@ -403,6 +404,7 @@ static int topk_impl(ss_bank* h, const int8_t* q, const float* q_inv, int64_t nq
   if (nq == 0) return SS_OK;
   TopkArgs a{q, q_inv, nq, h->emb, h->inv, h->cap, h->dim, k, theta, h->head, h->gcap,
              h->slot_offset};
+  a.inv_padded = true;  // the bank pads inv with one NaN tile
   a.gthr = gthr_reserve(h, nq);
   int slices = 1;
   if (int rc = topk_plan(h, a, algo, slices)) return rc;
@@ -429,6 +431,7 @@ int ss_topk_partials(ss_bank_t* h, const int8_t* q, const float* q_inv, int64_t 
   if (k < 1 || k > 256 || nq < 0) return set_error(SS_ERR_ARG, "topk_partials: bad k/nq");
   TopkArgs a{q, q_inv, nq, h->emb, h->inv, h->cap, h->dim, k, theta, h->head, h->gcap,
              h->slot_offset};
+  a.inv_padded = true;  // the bank pads inv with one NaN tile
   a.gthr = gthr_reserve(h, nq);
   int slices = 1;
   if (int rc = topk_plan(h, a, algo, slices)) return rc;
@@ -531,6 +534,7 @@ static int round_impl(ss_bank* h, const int8_t* q, const float* q_inv, const int
   if (k < 1 || k > 256) return set_error(SS_ERR_ARG, "k must lie in [1, 256], got %d", k);
   TopkArgs a{q, q_inv, nq, h->emb, h->inv, h->cap, h->dim, k, theta, h->head, h->gcap,
              h->slot_offset};
+  a.inv_padded = true;  // the bank pads inv with one NaN tile
   a.gthr = gthr_reserve(h, nq);
   int slices = 1;
   if (int rc = topk_plan(h, a, algo, slices)) return rc;

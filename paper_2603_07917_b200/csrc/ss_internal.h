@@ -48,6 +48,9 @@ struct TopkArgs {
   // key (orderable bits), shared by all slices so each slice filters with the
   // tightest threshold any slice has proven
   uint32_t* gthr = nullptr;  // [slices][nq], slices <= kMaxShareSlices
+  // inv is followed by at least one tile (256 floats) of NaN padding, so a
+  // whole tile's inverse norms may be bulk-copied (the bank allocates it so)
+  bool inv_padded = false;
 };
 constexpr int kMaxShareSlices = 160;
 int launch_topk_scan(const TopkArgs& a, uint64_t* partials, int n_slices, cudaStream_t st);
@@ -60,6 +63,9 @@ bool topk_tc_supported(const TopkArgs& a);
 bool topk_ts_supported(const TopkArgs& a);
 int topk_ts_lists(const TopkArgs& a, int device);
 int launch_topk_ts(const TopkArgs& a, uint64_t* partials, int n_lists, cudaStream_t st);
+// CTA-pair tcgen05 kernel with the 8-warp epilogue (k_topk_pair.cu)
+bool topk_pair_supported(const TopkArgs& a);
+int topk_pair_lists(const TopkArgs& a, int device);
 
 int launch_merge(const uint64_t* comp, const int32_t* len, int nlists, int64_t nq, int k,
                  uint64_t* out_comp, int32_t* out_len, const int32_t* bank_lens,

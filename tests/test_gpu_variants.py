@@ -1,0 +1,21 @@
+"""The opt-in stage-1 kernels (selected by SS_TC_* switches the library reads
+once per process) stay bit-exact: each runs in its own subprocess."""
+
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.parametrize("env", [{"SS_TC_PAIR": "1"}, {"SS_TC_TSN": "256"}, {"SS_TC_TS": "0"},
+                                 {"SS_TC_TS": "0", "SS_TC_CG": "2"}])
+def test_topk_variant_bit_exact(cuda, env):
+    e = dict(os.environ, **env)
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "check_topk_variant.py"),
+                        "30000", "600"], env=e, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
