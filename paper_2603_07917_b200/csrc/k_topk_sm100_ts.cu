@@ -33,6 +33,7 @@ constexpr int UK = 32;           // int8 K per MMA
 constexpr int EPI_WARPS = 8;
 constexpr int THREADS = 64 + EPI_WARPS * 32;
 constexpr int KMAX = 64;
+constexpr int ISLOTS = 4;  // inverse-norm ring (tiles)
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void bar_init(uint64_t* b, uint32_t n) {
@@ -57,6 +58,13 @@ __device__ __forceinline__ void tma2d(void* dst, const CUtensorMap* m, uint64_t*
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%3, %4}], [%2];\n" ::"r"(su32(dst)),
       "l"(m), "r"(su32(b)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          su32(dst)),
+      "l"(src), "r"(bytes), "r"(su32(b))
       : "memory");
 }
 __device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
@@ -111,6 +119,19 @@ __device__ __forceinline__ void wait_ld(int (&v)[32]) {
                :
                : "memory");
 }
+__device__ __forceinline__ void ld8_async(uint32_t taddr, int (&v)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+                 "=r"(v[7])
+               : "r"(taddr));
+}
+__device__ __forceinline__ void wait_ld8(int (&v)[8]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n"
+               : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]),
+                 "+r"(v[7])
+               :
+               : "memory");
+}
 __device__ __forceinline__ void st32(uint32_t taddr, const uint32_t (&v)[32]) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
@@ -145,9 +166,10 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
   constexpr int A_COL = NACC * BN;
   constexpr int B_STAGE = BN * BK;
   constexpr int HALF = BN / 2;     // columns per epilogue warp per tile
-  constexpr int CPW = HALF / 32;   // 32-column chunks per epilogue warp per tile
-  static_assert(HALF % 32 == 0 && (CPW == 3 || CPW == 4), "tile shape");
-  static_assert(A_COL + 128 <= 512, "TMEM columns");
+  constexpr int CPW = HALF / 32;   // full 32-column chunks per epilogue warp per tile
+  constexpr int TAIL = HALF % 32;  // + one 8-column chunk when BN = 208
+  static_assert((CPW == 3 || CPW == 4) && (TAIL == 0 || (TAIL == 8 && CPW == 3)), "tile shape");
+  static_assert(A_COL + 96 <= 512, "TMEM columns (dim <= 384 beside the accumulators)");
   constexpr uint32_t IDESC = idesc(BN);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
@@ -156,15 +178,17 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
   uint64_t* s_hroot = s_heap + (size_t)k * BM;                           // [128]
   int* s_hcnt = reinterpret_cast<int*>(s_hroot + BM);                    // [128]
   int* s_hlock = s_hcnt + BM;                                            // [128]
-  float* s_iw = reinterpret_cast<float*>(s_hlock + BM);                  // [8 warps][2][128]
-  float* s_ib = s_iw + EPI_WARPS * 2 * 128;                              // [8 warps][2][8]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(s_ib + EPI_WARPS * 2 * 8);
+  float* s_inv = reinterpret_cast<float*>(s_hlock + BM);                 // [ISLOTS][BN]
+  float* s_ib = s_inv + ISLOTS * 256;                                    // [8 warps][8]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(s_ib + EPI_WARPS * 8);
   uint64_t* a_full = bars;
   uint64_t* full = bars + 1;
   uint64_t* empty = full + stages;
   uint64_t* tfull = empty + stages;
   uint64_t* tempty = tfull + NACC;
-  uint64_t* mdone = tempty + NACC;
+  uint64_t* ifull = tempty + NACC;   // [ISLOTS] tile's inverse norms landed
+  uint64_t* iempty = ifull + ISLOTS; // [ISLOTS] consumed by every epilogue warp
+  uint64_t* mdone = iempty + ISLOTS;
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(mdone + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -179,6 +203,7 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
     bar_init(a_full, 4);
     for (int s = 0; s < stages; ++s) { bar_init(&full[s], 1); bar_init(&empty[s], 1); }
     for (int b = 0; b < NACC; ++b) { bar_init(&tfull[b], 1); bar_init(&tempty[b], EPI_WARPS); }
+    for (int b = 0; b < ISLOTS; ++b) { bar_init(&ifull[b], 1); bar_init(&iempty[b], EPI_WARPS); }
     bar_init(mdone, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -198,6 +223,15 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
       int it = 0;
       for (int t = 0; t < ntiles; ++t) {
         const int row0 = (int)((tile0 + t) * BN);
+        // the tile's BN inverse norms into the ring (the bank pads inv with
+        // one NaN tile, so the copy never leaves the allocation); the
+        // epilogue then issues no global loads in its tile loop
+        if (!(dbg & 64)) {
+          const int sl = t % ISLOTS;
+          bar_wait(&iempty[sl], ((t / ISLOTS) & 1) ^ 1);
+          bar_expect(&ifull[sl], BN * 4);
+          bulk_g2s(s_inv + sl * 256, inv + row0, BN * 4, &ifull[sl]);
+        }
         for (int kb = 0; kb < nkb; ++kb, ++it) {
           const int s = it % stages;
           bar_wait(&empty[s], ((it / stages) & 1) ^ 1);
@@ -270,89 +304,86 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
     }
     const float iq = (q < nq) ? q_inv[q] : __int_as_float(0x7fc00000);
     uint64_t* heap = s_heap + qrow;  // shared by the two column-half warps of this quarter
-    float* wib = s_ib + ew * 16;
-    float* wiw = s_iw + ew * 256;
-    const float NaNf = __int_as_float(0x7fc00000);
-    float pre[4];
-    auto fetch_iw = [&](int t) {
-      const int64_t r0 = (tile0 + t) * BN + grp * HALF + lane * 4;
-      if (lane * 4 >= HALF) {
-        pre[0] = pre[1] = pre[2] = pre[3] = NaNf;
-      } else if (r0 + 4 <= n_rows) {
-        const float4 a = __ldg(reinterpret_cast<const float4*>(inv + r0));
-        pre[0] = a.x; pre[1] = a.y; pre[2] = a.z; pre[3] = a.w;
-      } else {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) pre[u] = (r0 + u < n_rows) ? inv[r0 + u] : NaNf;
-      }
-    };
+    float* cib = s_ib + ew * 8;  // [max inv_w of chunk 0..3][min inv_w of chunk 0..3]
     if (dbg & 64) ntiles = 0;  // debug: MMA issue rate alone (no epilogue hand-off)
-    if (ntiles > 0) fetch_iw(0);
     float thr = (iq == iq) ? s_threshold(theta, iq) : INFINITY;
     for (int t = 0; t < ntiles; ++t) {
       const int64_t row0 = (tile0 + t) * BN + grp * HALF;  // first bank row of my columns
-      const int acc = t % NACC;
-      float* ciw = wiw + (t & 1) * 128;
-      float* cib = wib + (t & 1) * 8;  // [max inv_w of chunk 0..3][min inv_w of chunk 0..3]
-      reinterpret_cast<float4*>(ciw)[lane] = make_float4(pre[0], pre[1], pre[2], pre[3]);
+      const int acc = t % NACC, sl = t % ISLOTS;
+      const float* ciw = s_inv + sl * 256 + grp * HALF;
+      bar_wait(&ifull[sl], (t / ISLOTS) & 1);
       {
         // NaN (zero row / past the end) never passes the exact test: leave it
         // out of the bounds
-        float hi = fmaxf(fmaxf(fmaxf(pre[0], pre[1]), fmaxf(pre[2], pre[3])), 0.f);
-        float lo = fminf(fminf(fminf(pre[0], pre[1]), fminf(pre[2], pre[3])), INFINITY);
+        const float NaNf = __int_as_float(0x7fc00000);  // ignored by fmaxf / fminf
+        const float4 w4 = (lane * 4 < HALF) ? reinterpret_cast<const float4*>(ciw)[lane]
+                                            : make_float4(NaNf, NaNf, NaNf, NaNf);
+        float hi = fmaxf(fmaxf(fmaxf(w4.x, w4.y), fmaxf(w4.z, w4.w)), 0.f);
+        float lo = fminf(fminf(fminf(w4.x, w4.y), fminf(w4.z, w4.w)), INFINITY);
 #pragma unroll
         for (int o = 1; o < 8; o <<= 1) {
           hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
           lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
         }
-        if ((lane & 7) == 0 && (lane >> 3) < CPW) {
+        if ((lane & 7) == 0 && (lane >> 3) < CPW + (TAIL ? 1 : 0)) {
           cib[lane >> 3] = hi;
           cib[4 + (lane >> 3)] = lo;
         }
       }
       __syncwarp();
-      if (t + 1 < ntiles) fetch_iw(t + 1);
       bar_wait(&tfull[acc], (t / NACC) & 1);
       fence_after();
       const uint32_t tbase = tmem + lane_base + acc * BN + grp * HALF;
       if (dbg & 16) {
         fence_before();
         __syncwarp();
-        if (lane == 0) bar_arrive(&tempty[acc]);
+        if (lane == 0) { bar_arrive(&tempty[acc]); bar_arrive(&iempty[sl]); }
         continue;
       }
       // pull my 4 chunks into registers, then hand the accumulator back
-      int v0[32], v1[32], v2[32], v3[32];
+      int v0[32], v1[32], v2[32], v3[32], vt[8];
       ld32_async(tbase, v0);
       ld32_async(tbase + 32, v1);
       ld32_async(tbase + 64, v2);
       if constexpr (CPW == 4) ld32_async(tbase + 96, v3);
+      if constexpr (TAIL == 8) ld8_async(tbase + 96, vt);
       wait_ld(v0);
       wait_ld(v1);
       wait_ld(v2);
       if constexpr (CPW == 4) wait_ld(v3);
+      if constexpr (TAIL == 8) wait_ld8(vt);
       fence_before();
       __syncwarp();
       if (lane == 0) bar_arrive(&tempty[acc]);
-      if (dbg & 4) continue;
+      if (dbg & 4) {
+        if (lane == 0) bar_arrive(&iempty[sl]);
+        continue;
+      }
       // Filter: a chunk of 32 columns can only hold a score >= thr if
       // fl(fl(max dot) * (max inv_w)) >= thr (or the min inv_w when every dot
       // is negative) -- monotone rounding makes this a superset test, so the
       // exact per-column scores (one int->float conversion each, quarter rate)
       // are only computed for the rare chunks that pass it.
-      auto chunk = [&](const int (&v)[32], const int c) {
-        int m[11];
+      auto chunk = [&](const auto& v, const int c) {
+        constexpr int W = sizeof(v) / sizeof(v[0]);  // 32, or 8 for the N=208 tail
+        int md;
+        if constexpr (W == 32) {
+          int m[11];
 #pragma unroll
-        for (int j = 0; j < 10; ++j) m[j] = __vimax3_s32(v[3 * j], v[3 * j + 1], v[3 * j + 2]);
-        m[10] = max(v[30], v[31]);
-        const int md = __vimax3_s32(__vimax3_s32(m[0], m[1], m[2]), __vimax3_s32(m[3], m[4], m[5]),
-                                    __vimax3_s32(__vimax3_s32(m[6], m[7], m[8]), m[9], m[10]));
+          for (int j = 0; j < 10; ++j) m[j] = __vimax3_s32(v[3 * j], v[3 * j + 1], v[3 * j + 2]);
+          m[10] = max(v[30], v[31]);
+          md = __vimax3_s32(__vimax3_s32(m[0], m[1], m[2]), __vimax3_s32(m[3], m[4], m[5]),
+                            __vimax3_s32(__vimax3_s32(m[6], m[7], m[8]), m[9], m[10]));
+        } else {
+          md = __vimax3_s32(__vimax3_s32(v[0], v[1], v[2]), __vimax3_s32(v[3], v[4], v[5]),
+                            max(v[6], v[7]));
+        }
         const float bnd = __fmul_rn(__int2float_rn(md), md >= 0 ? cib[c] : cib[4 + c]);
         if (!(dbg & 1) && bnd >= thr) {
-          float s[32];
+          float s[W];
           const float4* iw4 = reinterpret_cast<const float4*>(ciw + c * 32);
 #pragma unroll
-          for (int j4 = 0; j4 < 8; ++j4) {
+          for (int j4 = 0; j4 < W / 4; ++j4) {
             const float4 w = iw4[j4];
             s[4 * j4 + 0] = __fmul_rn(__int2float_rn(v[4 * j4 + 0]), w.x);
             s[4 * j4 + 1] = __fmul_rn(__int2float_rn(v[4 * j4 + 1]), w.y);
@@ -362,11 +393,11 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
           const int64_t gbase = slot_offset + row0 + c * 32 - hmod;
           uint32_t mask = 0;
 #pragma unroll
-          for (int j = 0; j < 32; ++j) mask |= (s[j] >= thr ? 1u : 0u) << j;
+          for (int j = 0; j < W; ++j) mask |= (s[j] >= thr ? 1u : 0u) << j;
           if (!mask) return;
-          float sl[32];
+          float sl[W];
 #pragma unroll
-          for (int j = 0; j < 32; ++j) sl[j] = s[j];
+          for (int j = 0; j < W; ++j) sl[j] = s[j];
           // this query's heap is shared with the other column-half warp: take
           // its lock (one lock per thread at a time, never nested)
           while (atomicCAS(&s_hlock[qrow], 0, 1) != 0) {
@@ -401,7 +432,9 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
       chunk(v1, 1);
       chunk(v2, 2);
       if constexpr (CPW == 4) chunk(v3, 3);
+      if constexpr (TAIL == 8) chunk(vt, 3);
       __syncwarp();
+      if (lane == 0) bar_arrive(&iempty[sl]);  // this tile's inverse norms consumed
     }
     asm volatile("bar.sync 1, %0;\n" ::"n"(EPI_WARPS * 32) : "memory");  // both halves done
     if (grp == 0 && q < nq) {
@@ -433,15 +466,16 @@ static PFN_cuTensorMapEncodeTiled_v12000 ts_encode() {
 }
 
 static size_t ts_fixed_smem(int k) {
-  return (size_t)k * ts::BM * 8 + ts::BM * 16 + ts::EPI_WARPS * 2 * 136 * 4 + 512 + 1024;
+  return (size_t)k * ts::BM * 8 + ts::BM * 16 + ts::ISLOTS * 256 * 4 + ts::EPI_WARPS * 8 * 4 + 512 +
+         1024;
 }
 
 // Tile shape: BN = 192 rows with two TMEM accumulators (the MMA of the next
 // tile overlaps the drain of this one) or BN = 256 with one.  SS_TC_TSN=256
 // forces the single-accumulator form.
 static int ts_bn() {
-  static const int v = getenv("SS_TC_TSN") ? atoi(getenv("SS_TC_TSN")) : 192;
-  return v == 256 ? 256 : 192;
+  static const int v = getenv("SS_TC_TSN") ? atoi(getenv("SS_TC_TSN")) : 208;
+  return (v == 256 || v == 192) ? v : 208;
 }
 static int ts_stages(int k, int bn) {
   for (int s = 8; s >= 3; --s)
@@ -450,10 +484,11 @@ static int ts_stages(int k, int bn) {
 }
 
 bool topk_ts_supported(const TopkArgs& a) {
-  const int acols = ts_bn() == 256 ? 256 : 384;
+  const int acols = ts_bn() == 256 ? 256 : 2 * ts_bn();
   if (a.dim % ts::BK || a.dim % 128 || a.dim / 4 + acols > 512 || a.k < 1 || a.k > ts::KMAX)
     return false;
   if (a.n_rows >= (1LL << 31) || a.nq >= (1LL << 31)) return false;
+  if (!a.inv_padded) return false;  // tiles of inverse norms are bulk-copied whole
   return ts_stages(a.k, ts_bn()) >= 3;
 }
 
@@ -499,8 +534,11 @@ static int launch_ts_t(const TopkArgs& a, uint64_t* partials, int n_slices, cuda
 
 int launch_topk_ts(const TopkArgs& a, uint64_t* partials, int n_lists, cudaStream_t st) {
   if (n_lists < 1) return set_error(SS_ERR_ARG, "ts: no slices");
-  return ts_bn() == 256 ? launch_ts_t<256, 1>(a, partials, n_lists, st)
-                        : launch_ts_t<192, 2>(a, partials, n_lists, st);
+  switch (ts_bn()) {
+    case 256: return launch_ts_t<256, 1>(a, partials, n_lists, st);
+    case 192: return launch_ts_t<192, 2>(a, partials, n_lists, st);
+    default: return launch_ts_t<208, 2>(a, partials, n_lists, st);
+  }
 }
 
 }  // namespace ss
