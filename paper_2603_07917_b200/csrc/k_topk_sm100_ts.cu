@@ -48,9 +48,9 @@ __device__ __forceinline__ void bar_arrive(uint64_t* b) {
 }
 __device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity) {
   asm volatile(
-      "{\n.reg .pred p;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "{\n.reg .pred p;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
       "@!p bra W_%=;\n}\n" ::"r"(su32(b)),
-      "r"(parity)
+      "r"(parity), "r"(0x989680)  // suspend-time hint: sleep in the barrier, do not spin
       : "memory");
 }
 __device__ __forceinline__ void tma2d(void* dst, const CUtensorMap* m, uint64_t* b, int c0, int c1) {
