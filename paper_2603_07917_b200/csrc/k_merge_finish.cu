@@ -597,23 +597,36 @@ k_merge_finish_w(const uint64_t* __restrict__ partials, int nlists, int64_t nq, 
   int* whist = whist_all[warp];
   const unsigned lt = (1u << lane) - 1u;
 
-  // 1. load (all loads independent of each other: many in flight) + tau
-  if ((k & 31) == 0) {  // k multiple of 32: fixed per-list pattern, 8 lists' loads in flight
+  // 1. load every slice's list, dropping the zero padding on the fly (a list
+  // holds its candidates first, then zeros).  A full list (k candidates) is
+  // a min-heap with its minimum at entry 0 (every producer writes its heap
+  // array as is), so tau = max over full lists of entry 0 is a lower bound
+  // of the global k-th best; candidates below it are dropped afterwards.
+  int m1 = 0;
+  uint64_t tau = 1ull;
+  if ((k & 31) == 0) {  // k multiple of 32: 8 lists' loads in flight per batch
     const int per = k >> 5;
     const uint64_t* src0 = partials + q * k + lane;
     const int64_t lstride = nq * (int64_t)k;
-    int l = 0;
-    for (; l + 8 <= nlists; l += 8) {
+    for (int l0 = 0; l0 < nlists; l0 += 8) {
+      const int nl = min(8, nlists - l0);
+      uint64_t root[8];  // entry 0 of each list of the batch
       for (int jj = 0; jj < per; ++jj) {
         uint64_t v[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = __ldcs(src0 + (l + u) * lstride + jj * 32);
+        for (int u = 0; u < 8; ++u) v[u] = (u < nl) ? __ldcs(src0 + (l0 + u) * lstride + jj * 32) : 0ull;
 #pragma unroll
-        for (int u = 0; u < 8; ++u) cand[(l + u) * k + jj * 32 + lane] = v[u];
+        for (int u = 0; u < 8; ++u) {
+          const unsigned b = __ballot_sync(0xffffffffu, v[u] != 0ull);
+          if (v[u] != 0ull) cand[m1 + __popc(b & lt)] = v[u];
+          m1 += __popc(b);
+          if (jj == 0) root[u] = __shfl_sync(0xffffffffu, v[u], 0);
+          // entry k-1 present: the list is full, its root bounds the k-th best
+          if (jj == per - 1 && (b >> 31) && u < nl) tau = max(tau, root[u]);
+        }
+        __syncwarp();
       }
     }
-    for (; l < nlists; ++l)
-      for (int jj = 0; jj < per; ++jj) cand[l * k + jj * 32 + lane] = __ldcs(src0 + l * lstride + jj * 32);
   } else {
     int l = 0, j = lane;
     while (j >= k) { j -= k; ++l; }
@@ -622,26 +635,39 @@ k_merge_finish_w(const uint64_t* __restrict__ partials, int nlists, int64_t nq, 
       j += 32;
       while (j >= k) { j -= k; ++l; }
     }
+    __syncwarp();
+    for (int l2 = 0; l2 < nlists; ++l2) {
+      uint64_t mn = ~0ull;
+      for (int jx = lane; jx < k; jx += 32) mn = min(mn, cand[l2 * k + jx]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      if (mn != 0ull) tau = max(tau, mn);
+    }
+    for (int i0 = 0; i0 < M; i0 += 32) {
+      const int i = i0 + lane;
+      const uint64_t c = (i < M) ? cand[i] : 0ull;
+      const bool keep = c != 0ull;
+      const unsigned b = __ballot_sync(0xffffffffu, keep);
+      __syncwarp();
+      if (keep) cand[m1 + __popc(b & lt)] = c;
+      m1 += __popc(b);
+      __syncwarp();
+    }
   }
   __syncwarp();
-  uint64_t tau = 1ull;
-  for (int l = 0; l < nlists; ++l) {
-    uint64_t mn = ~0ull;
-    for (int j = lane; j < k; j += 32) mn = min(mn, cand[l * k + j]);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-    if (mn != 0ull) tau = max(tau, mn);
-  }
-  int m1 = 0;
-  for (int i0 = 0; i0 < M; i0 += 32) {
-    const int i = i0 + lane;
-    const uint64_t c = (i < M) ? cand[i] : 0ull;
-    const bool keep = c >= tau;
-    const unsigned b = __ballot_sync(0xffffffffu, keep);
-    __syncwarp();
-    if (keep) cand[m1 + __popc(b & lt)] = c;
-    m1 += __popc(b);
-    __syncwarp();
+  if (tau > 1ull) {  // drop candidates below the proven bound (in place, order kept)
+    int m2 = 0;
+    for (int i0 = 0; i0 < m1; i0 += 32) {
+      const int i = i0 + lane;
+      const uint64_t c = (i < m1) ? cand[i] : 0ull;
+      const bool keep = c >= tau;
+      const unsigned b = __ballot_sync(0xffffffffu, keep);
+      __syncwarp();
+      if (keep) cand[m2 + __popc(b & lt)] = c;
+      m2 += __popc(b);
+      __syncwarp();
+    }
+    m1 = m2;
   }
   // 2. k-th largest (unique composites): T such that |{c >= T}| = min(k, m1)
   uint64_t T = 1ull;
