@@ -371,14 +371,10 @@ bool topk_pair_supported(const TopkArgs& a) {
 }
 
 int topk_pair_lists(const TopkArgs& a, int device) {
-  const int sms = sm_count(device);
   int64_t qtiles = (a.nq + pr::BM - 1) / pr::BM;
   qtiles = (qtiles + 1) / 2 * 2;
   const int64_t tiles = (a.n_rows + pr::BN - 1) / pr::BN;
-  int64_t s = sms / qtiles;
-  if (s < 1) s = 1;
-  if (s > tiles) s = tiles;
-  return (int)s;
+  return pick_slices(qtiles, tiles, sm_count(device));
 }
 
 int launch_topk_pair(const TopkArgs& a, uint64_t* partials, int n_slices, cudaStream_t st,

@@ -494,13 +494,9 @@ bool topk_ts_supported(const TopkArgs& a) {
 
 // one partial list per CTA slice
 int topk_ts_lists(const TopkArgs& a, int device) {
-  int sms = sm_count(device);
-  int64_t qtiles = (a.nq + ts::BM - 1) / ts::BM;
-  int64_t tiles = (a.n_rows + ts_bn() - 1) / ts_bn();
-  int64_t s = sms / qtiles;
-  if (s < 1) s = 1;
-  if (s > tiles) s = tiles;
-  return (int)s;
+  const int64_t qtiles = (a.nq + ts::BM - 1) / ts::BM;
+  const int64_t tiles = (a.n_rows + ts_bn() - 1) / ts_bn();
+  return pick_slices(qtiles, tiles, sm_count(device));
 }
 
 template <int BN, int NACC>

@@ -5,6 +5,7 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <algorithm>
 #include <atomic>
 #include <mutex>
 #include <new>
@@ -36,6 +37,24 @@ int sm_count(int device) {
     cache[device] = v;
   }
   return cache[device];
+}
+
+int pick_slices(int64_t qtiles, int64_t tiles, int sms) {
+  if (qtiles < 1 || tiles < 1 || sms < 1) return 1;
+  int64_t lo = sms / qtiles;
+  if (lo < 1) lo = 1;
+  const int64_t hi = std::min<int64_t>(std::max<int64_t>(lo, 64), tiles);
+  if (lo >= tiles) return (int)tiles;
+  int64_t best = lo;
+  double best_eff = 0.0;
+  for (int64_t s = lo; s <= hi; ++s) {
+    const int64_t ctas = qtiles * s;
+    const int64_t waves = (ctas + sms - 1) / sms;
+    const double eff = (double)ctas / (double)(waves * sms);
+    if (eff >= 0.97) return (int)s;
+    if (eff > best_eff + 1e-9) { best_eff = eff; best = s; }
+  }
+  return (int)best;
 }
 
 // per-device sticky error flag for handle-less synchronous entry points

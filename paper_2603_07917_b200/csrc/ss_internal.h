@@ -9,6 +9,10 @@ namespace ss {
 void count_launch();
 int set_error(int code, const char* fmt, ...);
 int sm_count(int device);
+// bank slices per query tile for a grid of qtiles x slices CTAs (one CTA per
+// SM at a time): the fewest slices >= sms / qtiles whose grid fills its last
+// wave to >= 97% (or the best fill up to 64 slices), capped by the tile count
+int pick_slices(int64_t qtiles, int64_t tiles, int sms);
 
 int launch_match_pmfs(const float* sims, int64_t nq, int64_t nw, const int64_t* lens,
                       float theta, int64_t max_len, double* sup, double* mas,
