@@ -17,7 +17,7 @@ from __future__ import annotations
 import numpy as np
 import torch
 
-__all__ = ["centroids", "make_bank_device", "make_queries", "inv_norm_np"]
+__all__ = ["centroids", "make_bank_device", "make_queries", "inv_norm_np", "inv_norm_device"]
 
 
 def centroids(n_clusters: int, dim: int, seed: int) -> np.ndarray:
@@ -34,13 +34,18 @@ def _quantise(x: torch.Tensor) -> torch.Tensor:
 
 
 def make_bank_device(n: int, dim: int, n_clusters: int, seed: int, noise: float = 0.45,
-                     max_len: int = 2048, chunk: int = 1 << 18, device: str = "cuda"):
-    """(emb int8 [n, dim], lens int32 [n], cluster int64 [n]) on `device`."""
+                     max_len: int = 2048, chunk: int = 1 << 18, device: str = "cuda",
+                     member_seed: int | None = None):
+    """(emb int8 [n, dim], lens int32 [n], cluster int64 [n]) on `device`.
+
+    ``seed`` fixes the clusters (centroids and length laws); ``member_seed``
+    (default seed + 1) the members, so a trace drawn with another member seed
+    shares the bank's clusters."""
     cent, mu = centroids(n_clusters, dim, seed)
     cent_t = torch.as_tensor(cent, device=device)
     mu_t = torch.as_tensor(mu, device=device)
     g = torch.Generator(device=device)
-    g.manual_seed(seed + 1)
+    g.manual_seed(seed + 1 if member_seed is None else member_seed)
     emb = torch.empty((n, dim), dtype=torch.int8, device=device)
     lens = torch.empty(n, dtype=torch.int32, device=device)
     cl_all = torch.empty(n, dtype=torch.int64, device=device)
@@ -80,3 +85,11 @@ def make_queries(nq: int, dim: int, n_clusters: int, seed: int, qseed: int,
     I = rng.integers(1, max_input + 1, nq).astype(np.int32)
     ids = np.arange(nq, dtype=np.int64)
     return q, inv_norm_np(q), I, ids
+
+
+def inv_norm_device(emb: torch.Tensor) -> torch.Tensor:
+    """fp32 1/sqrt(sum x^2) on the device (IEEE sqrt and divide, as the bank
+    computes it); NaN for a zero row."""
+    ss = (emb.to(torch.int32) ** 2).sum(dim=1).to(torch.float32)
+    r = 1.0 / torch.sqrt(ss)
+    return torch.where(ss == 0, torch.full_like(r, float("nan")), r)

@@ -645,3 +645,45 @@ def test_trace_to_replay(cuda, tmp_path):
                 pack_mode="skip")
     assert st.rounds == 20 and st.admitted == 1000
     assert all(sum(tr.input_len[i] for i in b) <= 8192 for b in batches)
+
+
+@pytest.mark.parametrize("kv,mode", [(None, "cut"), (12_000, "skip")])
+def test_c5_device_replay_equals_host_replay(cuda, kv, mode):
+    """The device-resident replay (bench --config c5) reproduces the host
+    driver (checked above against the numpy replica) round by round."""
+    from paper_2603_07917_b200.history import HistoryWindow
+    from paper_2603_07917_b200.replay import Trace, replay
+    from paper_2603_07917_b200.replay_device import DeviceReplay, DeviceTrace
+    from paper_2603_07917_b200.scheduler import RoundConfig
+    cap, dim, ntr = 3000, 128, 2500
+    emb, lens, _, _ = O.make_bank(cap + ntr, dim, 40, 91)
+    rng = np.random.default_rng(92)
+    tr = Trace(emb=emb[cap:], inv=O.inv_norm(emb[cap:]),
+               input_len=rng.integers(1, 4097, ntr).astype(np.int32),
+               true_len=np.clip(lens[cap:], 1, 500).astype(np.int32))
+    cfg = RoundConfig(k=16, theta=0.8, min_matches=5, max_len=2048, nbins=64)
+    A, TOK, B, R, MAXA = 80, 48, 64, 40, 700
+    w1 = HistoryWindow(cap, dim)
+    w1.push(emb[:cap], lens[:cap])
+    host = []
+    replay(w1, tr, cfg, A, TOK, B, max_active=MAXA, rounds=R,
+           on_round=lambda r, info: host.append(info), kv_capacity=kv, pack_mode=mode)
+    w2 = HistoryWindow(cap, dim)
+    w2.push(emb[:cap], lens[:cap])
+    dr = DeviceReplay(w2, DeviceTrace.from_host(tr), cfg, A, TOK, B, MAXA, kv, mode)
+    dev = []
+    for _ in range(R):
+        out = dr.round()
+        if dr.n_act:
+            dev.append(dr.info(out["perm"]))
+    assert len(dev) == len(host) and dr.stats.completed > 50
+    assert dr.stats.refreshed > (20 if kv is None else 0)
+    for a, b in zip(host, dev):
+        assert np.array_equal(a["active_ids"], b["active_ids"])
+        assert np.array_equal(a["G"][:a["active_ids"].size], b["G"])
+        assert np.array_equal(a["perm"], b["perm"])
+        assert a["running"] == b["running"]
+    # the rings saw the same pushes in the same order
+    e1, i1, l1, s1 = w1.tensors()
+    e2, i2, l2, s2 = w2.tensors()
+    assert w1.head == w2.head and torch.equal(s1, s2) and torch.equal(l1, l2) and torch.equal(e1, e2)
