@@ -20,7 +20,7 @@ with every per-request array kept on the GPU:
     compaction.
 
 ``tests/test_gpu_parity.py`` checks it round by round against
-``replay.replay`` (itself checked against a numpy replica of the oracle).
+``replay.replay`` (itself checked against an independent numpy replica).
 """
 
 from __future__ import annotations
