@@ -116,15 +116,18 @@ def run_ours(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    if world > 1:
+    # SS_BENCH_SHARDED=1 runs the sharded (multi-GPU) round even at N = 1,
+    # under torchrun, so its code path can be exercised on one GPU
+    sharded = world > 1 or os.environ.get("SS_BENCH_SHARDED") == "1"
+    if sharded:
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     if _build.is_stale() and rank == 0:
         _build.build()
-    if world > 1:
+    if sharded:
         dist.barrier()
     _lib.load()
 
-    if world > 1:
+    if sharded:
         return run_sharded(args, world, rank, local)
     emb, lens, _ = make_bank_device(N_BANK, DIM, N_CLUSTERS, SEED)
     win = HistoryWindow(N_BANK, DIM)
@@ -254,8 +257,25 @@ def run_sharded(args, world, rank, local):
     sched.schedule_round(dq, dqi, dI, dids)
     torch.cuda.synchronize()
     per_round = _lib.launch_count() - c0
+    # the whole sharded round (NCCL collectives included) as one CUDA graph;
+    # eager rounds if this NCCL/driver combination cannot capture
+    graph = None
+    try:
+        graph, _ = sched.capture_round(dq, dqi, dI, dids)
+    except Exception as e:  # noqa: BLE001
+        print(f"sharded round not captured ({type(e).__name__}: {e}); timing eager rounds",
+              file=sys.stderr)
+        graph = None
+        torch.cuda.synchronize()
+
+    def one_round():
+        if graph is not None:
+            graph.replay()
+        else:
+            sched.schedule_round(dq, dqi, dI, dids)
+
     for _ in range(args.warmup):
-        sched.schedule_round(dq, dqi, dI, dids)
+        one_round()
     torch.cuda.synchronize()
     sampler = ClockSampler(local)
     with sampler:
@@ -265,7 +285,7 @@ def run_sharded(args, world, rank, local):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for _ in range(args.steps):
-            sched.schedule_round(dq, dqi, dI, dids)
+            one_round()
         e1.record()
         torch.cuda.synchronize()
         t1 = time.time()
@@ -316,6 +336,7 @@ def run_sharded(args, world, rank, local):
                        "nq_per_gpu": NQ, "k": K, "nbins": NBINS, "theta": THETA,
                        "similarity": algo_used, "n_slices": n_slices,
                        "parallelism": f"bank shard x{world} + NCCL all-gather/all-to-all/all-reduce",
+                       "graph": graph is not None,
                        "l2": "bank shard streamed from HBM each round"},
             "e2e": {"value": round(req * args.steps / (e2e_ms / 1e3), 1), "unit": "requests/s",
                     "h2d_bytes_per_step": int(world * (q.nbytes + qi.nbytes + I.nbytes + ids.nbytes)),
@@ -324,7 +345,7 @@ def run_sharded(args, world, rank, local):
             "roofline": {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak,
                          "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
                          "peak_source": "int8 dense = 2 x measured bf16 burst",
-                         "kernel": "k_topk_tc" if algo_used == "tcgen05" else "k_topk_scan",
+                         "kernel": topk_kernel_name(algo_used, world * NQ),
                          "kernel_ms": round(kern_ms, 4),
                          "kernel_share_of_step": round(kern_ms / (ms / args.steps), 3),
                          "traffic": None},

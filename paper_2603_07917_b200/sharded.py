@@ -123,13 +123,34 @@ class ShardedHistory:
 
 
 class ShardedScheduler:
-    """The scheduling round of SageScheduler, with stage 1 sharded."""
+    """The scheduling round of SageScheduler, with stage 1 sharded.
+
+    Round buffers are allocated once per queue size (so a round can be
+    captured in a CUDA graph, NCCL collectives included), and the window's
+    fallback histogram is all-reduced asynchronously while the queries are
+    gathered and scored."""
 
     def __init__(self, history: ShardedHistory, cfg):
         self.h = history
         self.cfg = cfg
         self.group = history.group
-        self._ws = None
+        self._bufs = {}
+
+    def _buffers(self, nq: int):
+        b = self._bufs.get(nq)
+        if b is None:
+            c, d, P = self.cfg, "cuda", self.cfg.nbins
+            b = dict(comp=torch.empty((nq, c.k), dtype=torch.int64, device=d),
+                     len=torch.empty((nq, c.k), dtype=torch.int32, device=d),
+                     npts=torch.zeros(nq, dtype=torch.int32, device=d),
+                     pbin=torch.zeros((nq, P), dtype=torch.int32, device=d),
+                     pcnt=torch.zeros((nq, P), dtype=torch.int32, device=d),
+                     pD=torch.zeros((nq, P), dtype=torch.int64, device=d),
+                     used_fb=torch.zeros(nq, dtype=torch.uint8, device=d),
+                     G=torch.empty(nq, dtype=torch.float64, device=d),
+                     perm=torch.empty(nq, dtype=torch.int64, device=d))
+            self._bufs[nq] = b
+        return b
 
     def schedule_round(self, q, q_inv, input_len, ids=None):
         from . import _lib
@@ -137,28 +158,39 @@ class ShardedScheduler:
 
         c = self.cfg
         nq = q.shape[0]
+        out = self._buffers(nq)
+        fb = self.h.window.fallback_hist(c.max_len, c.nbins)
+        fb_work = dist.all_reduce(fb, op=dist.ReduceOp.SUM, group=self.group,
+                                  async_op=True)                                # 5 (overlapped)
         q_all, qi_all = gather_queries(q, q_inv, self.group)                    # 1
         comp_all, len_all = self.h.window.topk(q_all, qi_all, c.k, c.theta, c.algo)  # 2
         comp_x, len_x = exchange_candidates(comp_all, len_all, self.group)      # 3
         world = comp_x.shape[0]
-        comp = torch.empty((nq, c.k), dtype=torch.int64, device="cuda")
-        ln = torch.empty((nq, c.k), dtype=torch.int32, device="cuda")
+        comp, ln = out["comp"], out["len"]
         _lib.call("ss_merge_topk", _lib.ptr(comp_x), _lib.ptr(len_x), world, nq, c.k,
                   _lib.ptr(comp), _lib.ptr(ln), _lib.stream_ptr())              # 4
-        fb = allreduce_hist(self.h.window.fallback_hist(c.max_len, c.nbins), self.group)  # 5
+        fb_work.wait()
         P = c.nbins
-        out = dict(npts=torch.zeros(nq, dtype=torch.int32, device="cuda"),
-                   pbin=torch.zeros((nq, P), dtype=torch.int32, device="cuda"),
-                   pcnt=torch.zeros((nq, P), dtype=torch.int32, device="cuda"),
-                   pD=torch.zeros((nq, P), dtype=torch.int64, device="cuda"),
-                   used_fb=torch.zeros(nq, dtype=torch.uint8, device="cuda"),
-                   G=torch.empty(nq, dtype=torch.float64, device="cuda"))
         I = torch.as_tensor(input_len, device="cuda").to(torch.int32)
         _lib.call("ss_finish", _lib.ptr(comp), _lib.ptr(ln), nq, c.k, c.min_matches, c.max_len,
                   c.nbins, _lib.ptr(I), _lib.ptr(fb[0]), _lib.ptr(fb[1]), _lib.ptr(fb[2]), P,
                   _lib.ptr(out["npts"]), _lib.ptr(out["pbin"]), _lib.ptr(out["pcnt"]),
                   _lib.ptr(out["pD"]), None, _lib.ptr(out["used_fb"]), _lib.ptr(out["G"]),
                   _lib.stream_ptr())                                            # 6
-        perm = _rank(out["G"], None if ids is None else torch.as_tensor(ids, device="cuda"))
-        out["comp"], out["len"] = comp, ln
+        perm = _rank(out["G"], None if ids is None else torch.as_tensor(ids, device="cuda"),
+                     out["perm"])
         return perm, out["G"], out
+
+    def capture_round(self, q, q_inv, input_len, ids=None, warmup: int = 2):
+        """CUDA-graph the sharded round (collectives included) for fixed input
+        buffers; returns (graph, (perm, G, out)).  Every rank must capture."""
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            for _ in range(warmup):
+                self.schedule_round(q, q_inv, input_len, ids)
+        torch.cuda.current_stream().wait_stream(s)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            res = self.schedule_round(q, q_inv, input_len, ids)
+        return g, res
