@@ -81,6 +81,15 @@ __device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a, uint64_t bdesc, u
       "r"(a), "l"(bdesc), "r"(idesc), "r"(acc)
       : "memory");
 }
+// D[tmem] (+)= A[smem] x B[smem]^T (the last K-block when A is split)
+__device__ __forceinline__ void mma_ss(uint32_t d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                       uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
+      : "memory");
+}
 // K-major, 128B swizzle: rows of 128 B, 8-row atoms 1024 B apart (SBO)
 __device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
   uint64_t d = 0;
@@ -132,6 +141,23 @@ __device__ __forceinline__ void wait_ld8(int (&v)[8]) {
                :
                : "memory");
 }
+__device__ __forceinline__ void ld16_async(uint32_t taddr, int (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];\n"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void wait_ld16(int (&v)[16]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n"
+               : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]),
+                 "+r"(v[7]), "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]), "+r"(v[12]),
+                 "+r"(v[13]), "+r"(v[14]), "+r"(v[15])
+               :
+               : "memory");
+}
 __device__ __forceinline__ void st32(uint32_t taddr, const uint32_t (&v)[32]) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
@@ -157,9 +183,13 @@ __device__ __noinline__ uint64_t heap_replace(uint64_t* heap, int k, uint64_t x)
 // BN bank rows per tile (UMMA N), NACC accumulators of BN columns in TMEM
 // (NACC = 2 lets the MMA of tile t+1 run while tile t is drained), A in
 // columns [NACC * BN, NACC * BN + dim / 4).
-template <int BN, int NACC>
+// ASPLIT: the last K-block of A lives in shared memory (TMA) instead of
+// TMEM, which frees 32 TMEM columns: two N=224 accumulators + 64 A columns
+// fill the 512 columns exactly.
+template <int BN, int NACC, bool ASPLIT>
 __global__ void __launch_bounds__(THREADS, 1)
-k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
+k_topk_ts(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmQ,
+          const int8_t* __restrict__ Q,
           const float* __restrict__ q_inv, int64_t nq, const float* __restrict__ inv, int64_t n_rows,
           int dim, int stages, int k, float theta, int64_t hmod, int64_t gcap, int64_t slot_offset,
           int64_t tiles_per_slice, uint64_t* __restrict__ partials, int dbg) {
@@ -167,14 +197,16 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
   constexpr int B_STAGE = BN * BK;
   constexpr int HALF = BN / 2;     // columns per epilogue warp per tile
   constexpr int CPW = HALF / 32;   // full 32-column chunks per epilogue warp per tile
-  constexpr int TAIL = HALF % 32;  // + one 8-column chunk when BN = 208
-  static_assert((CPW == 3 || CPW == 4) && (TAIL == 0 || (TAIL == 8 && CPW == 3)), "tile shape");
-  static_assert(A_COL + 96 <= 512, "TMEM columns (dim <= 384 beside the accumulators)");
+  constexpr int TAIL = HALF % 32;  // + one 8- or 16-column chunk (BN = 208 / 224)
+  static_assert((CPW == 3 || CPW == 4) && (TAIL == 0 || ((TAIL == 8 || TAIL == 16) && CPW == 3)),
+                "tile shape");
+  static_assert(A_COL + (ASPLIT ? 64 : 96) <= 512, "TMEM columns (dim 384 beside the accumulators)");
   constexpr uint32_t IDESC = idesc(BN);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sB = smem;                                                    // stages x 32 KB
-  uint64_t* s_heap = reinterpret_cast<uint64_t*>(sB + stages * B_STAGE);  // [k][128]
+  uint8_t* sA = sB + stages * B_STAGE;  // ASPLIT: the last K-block of A (16 KB, 1024-aligned)
+  uint64_t* s_heap = reinterpret_cast<uint64_t*>(sA + (ASPLIT ? BM * BK : 0));  // [k][128]
   uint64_t* s_hroot = s_heap + (size_t)k * BM;                           // [128]
   int* s_hcnt = reinterpret_cast<int*>(s_hroot + BM);                    // [128]
   int* s_hlock = s_hcnt + BM;                                            // [128]
@@ -200,7 +232,7 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
 
   if (threadIdx.x == 0) {
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmB) : "memory");
-    bar_init(a_full, 4);
+    bar_init(a_full, ASPLIT ? 5 : 4);  // 4 TMEM-writer warps (+ the TMA of the smem K-block)
     for (int s = 0; s < stages; ++s) { bar_init(&full[s], 1); bar_init(&empty[s], 1); }
     for (int b = 0; b < NACC; ++b) { bar_init(&tfull[b], 1); bar_init(&tempty[b], EPI_WARPS); }
     for (int b = 0; b < ISLOTS; ++b) { bar_init(&ifull[b], 1); bar_init(&iempty[b], EPI_WARPS); }
@@ -220,6 +252,10 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
   if (warp == 0) {
     // ------------------------------------------------------ TMA producer ---
     if (lane == 0 && ntiles > 0) {
+      if constexpr (ASPLIT) {
+        bar_expect(a_full, BM * BK);
+        tma2d(sA, &tmQ, a_full, (nkb - 1) * BK, qt * BM);
+      }
       int it = 0;
       for (int t = 0; t < ntiles; ++t) {
         const int row0 = (int)((tile0 + t) * BN);
@@ -262,11 +298,19 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
           const int s = it % stages;
           bar_wait(&full[s], (it / stages) & 1);
           fence_after();
+          if (ASPLIT && kb == nkb - 1) {
 #pragma unroll
-          for (int kk = 0; kk < BK / UK; ++kk)
-            if (!(dbg & 2))
-              mma_ts(dacc, tmem + A_COL + (kb * (BK / UK) + kk) * (UK / 4),
-                     desc_sw128(b_base + s * B_STAGE + kk * UK), IDESC, (kb | kk) != 0);
+            for (int kk = 0; kk < BK / UK; ++kk)
+              if (!(dbg & 2))
+                mma_ss(dacc, desc_sw128(su32(sA) + kk * UK),
+                       desc_sw128(b_base + s * B_STAGE + kk * UK), IDESC, (kb | kk) != 0);
+          } else {
+#pragma unroll
+            for (int kk = 0; kk < BK / UK; ++kk)
+              if (!(dbg & 2))
+                mma_ts(dacc, tmem + A_COL + (kb * (BK / UK) + kk) * (UK / 4),
+                       desc_sw128(b_base + s * B_STAGE + kk * UK), IDESC, (kb | kk) != 0);
+          }
           commit(&empty[s]);
         }
         commit(&tfull[acc]);
@@ -286,7 +330,7 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
     // group 0 writes this query's int8 vector into TMEM (A operand)
     if (grp == 0) {
-      const int ncol = dim / 4;
+      const int ncol = (ASPLIT ? dim - BK : dim) / 4;
       for (int c0 = 0; c0 < ncol; c0 += 32) {
         uint32_t v[32];
         const uint4* src = reinterpret_cast<const uint4*>(Q + q * dim) + c0 / 4;
@@ -341,17 +385,19 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
         continue;
       }
       // pull my 4 chunks into registers, then hand the accumulator back
-      int v0[32], v1[32], v2[32], v3[32], vt[8];
+      int v0[32], v1[32], v2[32], v3[32], vt[TAIL ? TAIL : 1];
       ld32_async(tbase, v0);
       ld32_async(tbase + 32, v1);
       ld32_async(tbase + 64, v2);
       if constexpr (CPW == 4) ld32_async(tbase + 96, v3);
       if constexpr (TAIL == 8) ld8_async(tbase + 96, vt);
+      if constexpr (TAIL == 16) ld16_async(tbase + 96, vt);
       wait_ld(v0);
       wait_ld(v1);
       wait_ld(v2);
       if constexpr (CPW == 4) wait_ld(v3);
       if constexpr (TAIL == 8) wait_ld8(vt);
+      if constexpr (TAIL == 16) wait_ld16(vt);
       fence_before();
       __syncwarp();
       if (lane == 0) bar_arrive(&tempty[acc]);
@@ -374,6 +420,11 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
           m[10] = max(v[30], v[31]);
           md = __vimax3_s32(__vimax3_s32(m[0], m[1], m[2]), __vimax3_s32(m[3], m[4], m[5]),
                             __vimax3_s32(__vimax3_s32(m[6], m[7], m[8]), m[9], m[10]));
+        } else if constexpr (W == 16) {
+          const int m0 = __vimax3_s32(v[0], v[1], v[2]), m1 = __vimax3_s32(v[3], v[4], v[5]);
+          const int m2 = __vimax3_s32(v[6], v[7], v[8]), m3 = __vimax3_s32(v[9], v[10], v[11]);
+          const int m4 = __vimax3_s32(v[12], v[13], v[14]);
+          md = __vimax3_s32(__vimax3_s32(m0, m1, m2), __vimax3_s32(m3, m4, v[15]), m0);
         } else {
           md = __vimax3_s32(__vimax3_s32(v[0], v[1], v[2]), __vimax3_s32(v[3], v[4], v[5]),
                             max(v[6], v[7]));
@@ -432,7 +483,7 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
       chunk(v1, 1);
       chunk(v2, 2);
       if constexpr (CPW == 4) chunk(v3, 3);
-      if constexpr (TAIL == 8) chunk(vt, 3);
+      if constexpr (TAIL != 0) chunk(vt, 3);
       __syncwarp();
       if (lane == 0) bar_arrive(&iempty[sl]);  // this tile's inverse norms consumed
     }
@@ -470,36 +521,45 @@ static size_t ts_fixed_smem(int k) {
          1024;
 }
 
-// Tile shape: BN = 192 rows with two TMEM accumulators (the MMA of the next
-// tile overlaps the drain of this one) or BN = 256 with one.  SS_TC_TSN=256
-// forces the single-accumulator form.
-static int ts_bn() {
+// Tile shape (bank rows per tile, accumulators): 208 x 2 with all of A in
+// TMEM (default: the widest double buffer that fits beside A), 224 x 2 with
+// the last K-block of A in shared memory (SS_TC_TSN=224; the SS-form MMA of
+// that K-block ran slower, 0.303 vs 0.297 ms MMA-only, 0.378 vs 0.373 ms end
+// to end), 192 x 2, or 256 x 1.
+static int ts_bn(const TopkArgs& a) {
   static const int v = getenv("SS_TC_TSN") ? atoi(getenv("SS_TC_TSN")) : 208;
-  return (v == 256 || v == 192) ? v : 208;
+  const int want = (v == 256 || v == 192 || v == 224) ? v : 208;
+  if (want == 224 && a.dim / 4 - 32 + 2 * 224 <= 512) return 224;
+  if (want >= 208 && want != 256 && a.dim / 4 + 2 * 208 <= 512) return 208;
+  if (want == 256) return 256;
+  return 192;
 }
+static size_t ts_smem_extra(int bn) { return bn == 224 ? (size_t)ts::BM * ts::BK : 0; }
 static int ts_stages(int k, int bn) {
   for (int s = 8; s >= 3; --s)
-    if (ts_fixed_smem(k) + (size_t)s * bn * ts::BK <= 227 * 1024) return s;
+    if (ts_fixed_smem(k) + ts_smem_extra(bn) + (size_t)s * bn * ts::BK <= 227 * 1024) return s;
   return 0;
 }
 
 bool topk_ts_supported(const TopkArgs& a) {
-  const int acols = ts_bn() == 256 ? 256 : 2 * ts_bn();
-  if (a.dim % ts::BK || a.dim % 128 || a.dim / 4 + acols > 512 || a.k < 1 || a.k > ts::KMAX)
+  const int bn = ts_bn(a);
+  const int acols = bn == 256 ? 256 : 2 * bn;
+  const int a_tmem = bn == 224 ? a.dim / 4 - 32 : a.dim / 4;
+  if (a.dim % ts::BK || a.dim % 128 || a_tmem + acols > 512 || a.k < 1 || a.k > ts::KMAX)
     return false;
   if (a.n_rows >= (1LL << 31) || a.nq >= (1LL << 31)) return false;
   if (!a.inv_padded) return false;  // tiles of inverse norms are bulk-copied whole
-  return ts_stages(a.k, ts_bn()) >= 3;
+  return ts_stages(a.k, ts_bn(a)) >= 3;
 }
 
 // one partial list per CTA slice
 int topk_ts_lists(const TopkArgs& a, int device) {
   const int64_t qtiles = (a.nq + ts::BM - 1) / ts::BM;
-  const int64_t tiles = (a.n_rows + ts_bn() - 1) / ts_bn();
+  const int64_t tiles = (a.n_rows + ts_bn(a) - 1) / ts_bn(a);
   return pick_slices(qtiles, tiles, sm_count(device));
 }
 
-template <int BN, int NACC>
+template <int BN, int NACC, bool ASPLIT>
 static int launch_ts_t(const TopkArgs& a, uint64_t* partials, int n_slices, cudaStream_t st) {
   auto enc = ts_encode();
   if (!enc) return set_error(SS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
@@ -512,17 +572,26 @@ static int launch_ts_t(const TopkArgs& a, uint64_t* partials, int n_slices, cuda
                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_error(SS_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  CUtensorMap mq = mb;  // queries (A) for the smem K-block of the split form
+  if (ASPLIT) {
+    cuuint64_t qdim[2] = {(cuuint64_t)a.dim, (cuuint64_t)a.nq};
+    cuuint32_t qbox[2] = {(cuuint32_t)ts::BK, (cuuint32_t)ts::BM};
+    r = enc(&mq, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(a.q), qdim, gstride, qbox,
+            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return set_error(SS_ERR_CUDA, "cuTensorMapEncodeTiled (q) failed (%d)", (int)r);
+  }
   const int stages = ts_stages(a.k, BN);
-  const size_t smem = ts_fixed_smem(a.k) + (size_t)stages * BN * ts::BK;
-  SS_CUDA_TRY(cudaFuncSetAttribute(ts::k_topk_ts<BN, NACC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)smem));
+  const size_t smem = ts_fixed_smem(a.k) + ts_smem_extra(BN) + (size_t)stages * BN * ts::BK;
+  SS_CUDA_TRY(cudaFuncSetAttribute(ts::k_topk_ts<BN, NACC, ASPLIT>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int64_t tiles = (a.n_rows + BN - 1) / BN;
   const int64_t tps = (tiles + n_slices - 1) / n_slices;
   dim3 grid((unsigned)((a.nq + ts::BM - 1) / ts::BM), (unsigned)n_slices);
   const char* dv = getenv("SS_TC_DEBUG");
   count_launch();
-  ts::k_topk_ts<BN, NACC><<<grid, ts::THREADS, smem, st>>>(
-      mb, a.q, a.q_inv, a.nq, a.inv, a.n_rows, a.dim, stages, a.k, a.theta, a.head % a.gcap, a.gcap,
+  ts::k_topk_ts<BN, NACC, ASPLIT><<<grid, ts::THREADS, smem, st>>>(
+      mb, mq, a.q, a.q_inv, a.nq, a.inv, a.n_rows, a.dim, stages, a.k, a.theta, a.head % a.gcap, a.gcap,
       a.slot_offset, tps, partials, dv ? atoi(dv) : 0);
   SS_LAUNCH_CHECK();
   return SS_OK;
@@ -530,10 +599,11 @@ static int launch_ts_t(const TopkArgs& a, uint64_t* partials, int n_slices, cuda
 
 int launch_topk_ts(const TopkArgs& a, uint64_t* partials, int n_lists, cudaStream_t st) {
   if (n_lists < 1) return set_error(SS_ERR_ARG, "ts: no slices");
-  switch (ts_bn()) {
-    case 256: return launch_ts_t<256, 1>(a, partials, n_lists, st);
-    case 192: return launch_ts_t<192, 2>(a, partials, n_lists, st);
-    default: return launch_ts_t<208, 2>(a, partials, n_lists, st);
+  switch (ts_bn(a)) {
+    case 256: return launch_ts_t<256, 1, false>(a, partials, n_lists, st);
+    case 192: return launch_ts_t<192, 2, false>(a, partials, n_lists, st);
+    case 208: return launch_ts_t<208, 2, false>(a, partials, n_lists, st);
+    default: return launch_ts_t<224, 2, true>(a, partials, n_lists, st);
   }
 }
 
