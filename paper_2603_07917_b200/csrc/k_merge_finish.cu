@@ -586,6 +586,7 @@ k_merge_finish_w(const uint64_t* __restrict__ partials, int nlists, int64_t nq, 
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t q = (int64_t)blockIdx.x * MFW_WARPS + warp;
+  pdl_wait();  // the similarity kernel's partial lists
   if (q >= nq) return;  // warp-uniform; no block barriers below
   const int M = nlists * k;
   unsigned char* base = smem + warp * warp_bytes;
@@ -814,10 +815,10 @@ int launch_merge_finish(const uint64_t* partials, int nlists, int64_t nq, int k,
         SS_CUDA_TRY(cudaFuncSetAttribute(k_merge_finish_w,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       count_launch();
-      k_merge_finish_w<<<(unsigned)((nq + MFW_WARPS - 1) / MFW_WARPS), MFW_WARPS * 32, smem, st>>>(
-          partials, nlists, nq, k, bank_lens, head, gcap, slot_offset, out_comp, out_len,
-          min_matches, max_len, nbins, I, fb_cnt, fb_sv, fb_sv2, P, npts, pbin, pcnt, pD, psv,
-          used_fb, G, wb);
+      SS_CUDA_TRY(pdl_launch(k_merge_finish_w, dim3((unsigned)((nq + MFW_WARPS - 1) / MFW_WARPS)),
+                             dim3(MFW_WARPS * 32), smem, st, partials, nlists, nq, k, bank_lens, head,
+                             gcap, slot_offset, out_comp, out_len, min_matches, max_len, nbins, I,
+                             fb_cnt, fb_sv, fb_sv2, P, npts, pbin, pcnt, pD, psv, used_fb, G, wb));
       SS_LAUNCH_CHECK();
       return SS_OK;
     }

@@ -67,6 +67,7 @@ constexpr int RC_LANES = 8;
 __global__ void __launch_bounds__(256)
 k_rank_count(const double* __restrict__ G, const int64_t* __restrict__ ids, int n,
              int64_t* __restrict__ perm) {
+  pdl_wait();  // G from the previous kernel
   __shared__ uint64_t sk[2048];
   __shared__ int64_t sid[2048];
   const int t = threadIdx.x & (RC_LANES - 1);
@@ -370,7 +371,8 @@ int launch_rank(const double* G, const int64_t* ids, int64_t n, int64_t* perm, v
   if (n <= 0) return SS_OK;
   if (n <= COUNT_MAX) {
     count_launch();
-    k_rank_count<<<(unsigned)((n * RC_LANES + 255) / 256), 256, 0, st>>>(G, ids, (int)n, perm);
+    SS_CUDA_TRY(pdl_launch(k_rank_count, dim3((unsigned)((n * RC_LANES + 255) / 256)), dim3(256), 0,
+                           st, G, ids, (int)n, perm));
     SS_LAUNCH_CHECK();
     return SS_OK;
   }

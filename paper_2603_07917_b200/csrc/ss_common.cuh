@@ -95,6 +95,11 @@ __device__ __forceinline__ double warp_min_f64(double v) {
   return v;
 }
 
+// Programmatic dependent launch: a kernel launched with pdl_launch() may be
+// scheduled while its predecessor on the stream drains; it must call
+// pdl_wait() before touching anything the predecessor writes.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+
 }  // namespace ss
 
 // Internal launchers (host side), implemented per kernel file.

@@ -7,6 +7,25 @@
 namespace ss {
 
 void count_launch();
+
+// launch `kern` with the programmatic-stream-serialization attribute (PDL):
+// its launch overlaps the tail of the previous kernel on the stream; the
+// kernel calls pdl_wait() before reading that kernel's outputs
+template <typename... KArgs, typename... Args>
+inline cudaError_t pdl_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
 int set_error(int code, const char* fmt, ...);
 int sm_count(int device);
 // bank slices per query tile for a grid of qtiles x slices CTAs (one CTA per
