@@ -60,13 +60,14 @@ k_rank_small(const double* __restrict__ G, const int64_t* __restrict__ ids, int 
 // Keys are staged through shared memory in 1024-entry tiles.
 constexpr int COUNT_MAX = 8192;
 
-// 8 lanes per request: lane t of a group compares against j = t, t+8, ...
-// (L1-resident loads), then the group sums its partial ranks with shuffles.
-constexpr int RC_LANES = 8;
-
+// L lanes per request (32 up to 2048 requests, else 8): lane t of a group
+// compares against j = t, t+L, ... (shared-memory tiles), then the group sums
+// its partial ranks with shuffles.
+template <int L>
 __global__ void __launch_bounds__(256)
 k_rank_count(const double* __restrict__ G, const int64_t* __restrict__ ids, int n,
              int64_t* __restrict__ perm) {
+  constexpr int RC_LANES = L;
   pdl_wait();  // G from the previous kernel
   __shared__ uint64_t sk[2048];
   __shared__ int64_t sid[2048];
@@ -371,8 +372,12 @@ int launch_rank(const double* G, const int64_t* ids, int64_t n, int64_t* perm, v
   if (n <= 0) return SS_OK;
   if (n <= COUNT_MAX) {
     count_launch();
-    SS_CUDA_TRY(pdl_launch(k_rank_count, dim3((unsigned)((n * RC_LANES + 255) / 256)), dim3(256), 0,
-                           st, G, ids, (int)n, perm));
+    if (n <= 2048)
+      SS_CUDA_TRY(pdl_launch(k_rank_count<32>, dim3((unsigned)((n * 32 + 255) / 256)), dim3(256), 0,
+                             st, G, ids, (int)n, perm));
+    else
+      SS_CUDA_TRY(pdl_launch(k_rank_count<8>, dim3((unsigned)((n * 8 + 255) / 256)), dim3(256), 0,
+                             st, G, ids, (int)n, perm));
     SS_LAUNCH_CHECK();
     return SS_OK;
   }
