@@ -687,3 +687,15 @@ def test_c5_device_replay_equals_host_replay(cuda, kv, mode):
     e1, i1, l1, s1 = w1.tensors()
     e2, i2, l2, s2 = w2.tensors()
     assert w1.head == w2.head and torch.equal(s1, s2) and torch.equal(l1, l2) and torch.equal(e1, e2)
+
+
+@pytest.mark.parametrize("dim", [128, 256, 512])
+@pytest.mark.parametrize("nq", [64, 300])
+def test_topk_dims_bit_exact(cuda, dim, nq):
+    """Other embedding widths through the tcgen05 kernels (dim 512 leaves
+    room for only the N=192 double buffer beside A in TMEM)."""
+    w, be, bl, q, qi = _bank(12_000, dim, 60, 17, nq)
+    for theta, k in ((0.8, 64), (-1.0, 32)):
+        keys, seq, ref = _oracle_topk(w, be, q, qi, k, theta)
+        comp, ln = w.topk(q, qi, k, theta, "tcgen05")
+        _check_topk(w, comp, keys, seq, ref, k)
