@@ -186,13 +186,20 @@ __device__ __noinline__ uint64_t heap_replace(uint64_t* heap, int k, uint64_t x)
 // ASPLIT: the last K-block of A lives in shared memory (TMA) instead of
 // TMEM, which frees 32 TMEM columns: two N=224 accumulators + 64 A columns
 // fill the 512 columns exactly.
-template <int BN, int NACC, bool ASPLIT>
+// SHARE (pure top-k): every slice publishes the R-th best key it keeps per
+// query (gslots[slice][q], R = ceil(k / slices)); each tile, every slice
+// filters with the minimum over all slices' published keys -- once every
+// slice has published, the union of their top-R holds >= k rows at or above
+// that minimum, so it bounds the global k-th key from below.  Slots that are
+// still 0 make the minimum 0 (no bound).
+template <int BN, int NACC, bool ASPLIT, bool SHARE = false>
 __global__ void __launch_bounds__(THREADS, 1)
 k_topk_ts(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmQ,
           const int8_t* __restrict__ Q,
           const float* __restrict__ q_inv, int64_t nq, const float* __restrict__ inv, int64_t n_rows,
           int dim, int stages, int k, float theta, int64_t hmod, int64_t gcap, int64_t slot_offset,
-          int64_t tiles_per_slice, uint64_t* __restrict__ partials, int dbg) {
+          int64_t tiles_per_slice, uint64_t* __restrict__ partials, int dbg,
+          uint32_t* __restrict__ gslots = nullptr, int rshare = 0) {
   constexpr int A_COL = NACC * BN;
   constexpr int B_STAGE = BN * BK;
   constexpr int HALF = BN / 2;     // columns per epilogue warp per tile
@@ -222,6 +229,8 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUten
   uint64_t* iempty = ifull + ISLOTS; // [ISLOTS] consumed by every epilogue warp
   uint64_t* mdone = iempty + ISLOTS;
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(mdone + 1);
+  // SHARE: this slice's top-R keys per query, after everything else
+  uint32_t* s_rtop = s_tmem + 4;  // [128][4]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int qt = blockIdx.x, slice = blockIdx.y;
@@ -240,6 +249,8 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUten
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   for (int i = threadIdx.x; i < BM; i += blockDim.x) { s_hcnt[i] = 0; s_hroot[i] = 0; s_hlock[i] = 0; }
+  if constexpr (SHARE)
+    for (int i = threadIdx.x; i < BM * 4; i += blockDim.x) s_rtop[i] = 0u;
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(su32(s_tmem)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
@@ -355,6 +366,15 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUten
       const int64_t row0 = (tile0 + t) * BN + grp * HALF;  // first bank row of my columns
       const int acc = t % NACC, sl = t % ISLOTS;
       const float* ciw = s_inv + sl * 256 + grp * HALF;
+      if constexpr (SHARE) {
+        // minimum over the slices' published R-th best keys (independent
+        // loads; their latency overlaps the wait for this tile's MMA)
+        if (q < nq) {
+          uint32_t m = ~0u;
+          for (int s2 = 0; s2 < (int)gridDim.y; ++s2) m = min(m, __ldcg(gslots + (int64_t)s2 * nq + q));
+          if (m != 0u && m != ~0u) thr = fmaxf(thr, s_threshold(f32_unorder(m), iq));
+        }
+      }
       bar_wait(&ifull[sl], (t / ISLOTS) & 1);
       {
         // NaN (zero row / past the end) never passes the exact test: leave it
@@ -456,6 +476,8 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUten
           __threadfence_block();
           int hcnt = s_hcnt[qrow];
           uint64_t hroot = s_hroot[qrow];
+          uint32_t rth0 = 0u;
+          if constexpr (SHARE) rth0 = s_rtop[qrow * 4 + rshare - 1];
           while (mask) {
             const int j = __ffs(mask) - 1;
             mask &= mask - 1;
@@ -464,19 +486,36 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUten
               int64_t rel = gbase + j;
               if (rel < 0) rel += gcap;
               const uint64_t comp = make_comp(key, (uint32_t)rel);
+              bool kept = true;
               if (hcnt < k) {
                 heap[hcnt * BM] = comp;
                 if (++hcnt == k) hroot = heapify(heap, k);
               } else if (comp > hroot) {
                 hroot = heap_replace(heap, k, comp);
+              } else {
+                kept = false;
+              }
+              if constexpr (SHARE) {
+                if (kept) {  // this slice's top-R keys, descending
+                  uint32_t x = f32_order(key);
+                  for (int i = 0; i < rshare; ++i) {
+                    const uint32_t cur = s_rtop[qrow * 4 + i];
+                    if (x > cur) { s_rtop[qrow * 4 + i] = x; x = cur; }
+                  }
+                }
               }
             }
           }
+          uint32_t rth1 = 0u;
+          if constexpr (SHARE) rth1 = s_rtop[qrow * 4 + rshare - 1];
           s_hcnt[qrow] = hcnt;
           s_hroot[qrow] = hroot;
           __threadfence_block();
           atomicExch(&s_hlock[qrow], 0);
           if (hcnt >= k) thr = fmaxf(thr, s_threshold(comp_key(hroot), iq));
+          if constexpr (SHARE) {
+            if (rth1 != rth0) __stcg(gslots + (int64_t)slice * nq + q, rth1);  // publish
+          }
         }
       };
       chunk(v0, 0);
@@ -561,6 +600,12 @@ int topk_ts_lists(const TopkArgs& a, int device) {
 
 template <int BN, int NACC, bool ASPLIT>
 static int launch_ts_t(const TopkArgs& a, uint64_t* partials, int n_slices, cudaStream_t st) {
+  // pure top-k: share per-slice bounds (see k_topk_ts SHARE)
+  int rshare = 0;
+  if (a.gslots && a.theta <= 0.f && n_slices >= 2 && n_slices <= kMaxShareSlices) {
+    const int R = (a.k + n_slices - 1) / n_slices;
+    if (R <= 4) rshare = R;
+  }
   auto enc = ts_encode();
   if (!enc) return set_error(SS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   CUtensorMap mb;
@@ -582,17 +627,20 @@ static int launch_ts_t(const TopkArgs& a, uint64_t* partials, int n_slices, cuda
     if (r != CUDA_SUCCESS) return set_error(SS_ERR_CUDA, "cuTensorMapEncodeTiled (q) failed (%d)", (int)r);
   }
   const int stages = ts_stages(a.k, BN);
-  const size_t smem = ts_fixed_smem(a.k) + ts_smem_extra(BN) + (size_t)stages * BN * ts::BK;
-  SS_CUDA_TRY(cudaFuncSetAttribute(ts::k_topk_ts<BN, NACC, ASPLIT>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const size_t smem = ts_fixed_smem(a.k) + ts_smem_extra(BN) + (size_t)stages * BN * ts::BK +
+                      (rshare ? ts::BM * 16 : 0);
+  auto kern = rshare ? ts::k_topk_ts<BN, NACC, ASPLIT, true> : ts::k_topk_ts<BN, NACC, ASPLIT, false>;
+  SS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (rshare)
+    SS_CUDA_TRY(cudaMemsetAsync(a.gslots, 0, (size_t)n_slices * a.nq * sizeof(uint32_t), st));
   const int64_t tiles = (a.n_rows + BN - 1) / BN;
   const int64_t tps = (tiles + n_slices - 1) / n_slices;
   dim3 grid((unsigned)((a.nq + ts::BM - 1) / ts::BM), (unsigned)n_slices);
   const char* dv = getenv("SS_TC_DEBUG");
   count_launch();
-  ts::k_topk_ts<BN, NACC, ASPLIT><<<grid, ts::THREADS, smem, st>>>(
+  kern<<<grid, ts::THREADS, smem, st>>>(
       mb, mq, a.q, a.q_inv, a.nq, a.inv, a.n_rows, a.dim, stages, a.k, a.theta, a.head % a.gcap, a.gcap,
-      a.slot_offset, tps, partials, dv ? atoi(dv) : 0);
+      a.slot_offset, tps, partials, dv ? atoi(dv) : 0, a.gslots, rshare);
   SS_LAUNCH_CHECK();
   return SS_OK;
 }

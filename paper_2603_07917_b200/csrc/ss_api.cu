@@ -113,6 +113,8 @@ struct ss_bank {
   size_t ws_bytes = 0;
   uint32_t* gthr = nullptr;  // per-query shared k-th-key bound for the top-k slices
   int64_t gthr_cap = 0;
+  uint32_t* gslots = nullptr;  // TS kernel pure top-k: per-slice published bounds
+  int64_t gslots_cap = 0;
   // side stream of the fused round: the fallback histogram runs concurrently
   // with the similarity kernel (fork/join by events; captured as two graph
   // branches when the caller's stream is being captured)
@@ -157,6 +159,25 @@ static uint32_t* gthr_reserve(ss_bank* h, int64_t nq) {
   }
   h->gthr_cap = want;
   return h->gthr;
+}
+
+// per-slice published bounds for the TS kernel in pure top-k mode (theta <=
+// 0); SS_TC_SHARE=0 disables.  Grow-on-demand outside graph capture, like the
+// workspace; nullptr simply disables the sharing.
+static uint32_t* gslots_reserve(ss_bank* h, int64_t nq, float theta) {
+  static const bool off = getenv("SS_TC_SHARE") && atoi(getenv("SS_TC_SHARE")) == 0;
+  if (off || !(theta <= 0.f)) return nullptr;
+  const int64_t need = nq * kMaxShareSlices;
+  if (need <= h->gslots_cap) return h->gslots;
+  if (h->gslots) cudaFree(h->gslots);
+  h->gslots = nullptr;
+  h->gslots_cap = 0;
+  if (cudaMalloc(&h->gslots, (size_t)need * sizeof(uint32_t)) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  h->gslots_cap = need;
+  return h->gslots;
 }
 
 static int ws_reserve(ss_bank* h, size_t bytes) {
@@ -314,6 +335,7 @@ int ss_bank_destroy(ss_bank_t* h) {
   cudaFree(h->d_err);
   cudaFree(h->ws);
   cudaFree(h->gthr);
+  cudaFree(h->gslots);
   if (h->host_exec) cudaGraphExecDestroy(h->host_exec);
   if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
@@ -425,6 +447,7 @@ static int topk_impl(ss_bank* h, const int8_t* q, const float* q_inv, int64_t nq
              h->slot_offset};
   a.inv_padded = true;  // the bank pads inv with one NaN tile
   a.gthr = gthr_reserve(h, nq);
+  a.gslots = gslots_reserve(h, nq, theta);
   int slices = 1;
   if (int rc = topk_plan(h, a, algo, slices)) return rc;
   size_t need = ws_offset + align_up((size_t)slices * nq * k * 8);
@@ -452,6 +475,7 @@ int ss_topk_partials(ss_bank_t* h, const int8_t* q, const float* q_inv, int64_t 
              h->slot_offset};
   a.inv_padded = true;  // the bank pads inv with one NaN tile
   a.gthr = gthr_reserve(h, nq);
+  a.gslots = gslots_reserve(h, nq, theta);
   int slices = 1;
   if (int rc = topk_plan(h, a, algo, slices)) return rc;
   if (slices > max_slices) slices = max_slices;
@@ -555,6 +579,7 @@ static int round_impl(ss_bank* h, const int8_t* q, const float* q_inv, const int
              h->slot_offset};
   a.inv_padded = true;  // the bank pads inv with one NaN tile
   a.gthr = gthr_reserve(h, nq);
+  a.gslots = gslots_reserve(h, nq, theta);
   int slices = 1;
   if (int rc = topk_plan(h, a, algo, slices)) return rc;
   uint64_t* partials = reinterpret_cast<uint64_t*>((char*)h->ws + base + L.end);

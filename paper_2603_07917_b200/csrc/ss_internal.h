@@ -74,6 +74,11 @@ struct TopkArgs {
   // inv is followed by at least one tile (256 floats) of NaN padding, so a
   // whole tile's inverse norms may be bulk-copied (the bank allocates it so)
   bool inv_padded = false;
+  // optional [kMaxShareSlices][nq] scratch for the TS kernel's pure top-k
+  // mode: every slice publishes the R-th best key it holds per query, and
+  // every slice filters with the minimum over slices (a lower bound of the
+  // global k-th key once all have published)
+  uint32_t* gslots = nullptr;
 };
 constexpr int kMaxShareSlices = 160;
 int launch_topk_scan(const TopkArgs& a, uint64_t* partials, int n_slices, cudaStream_t st);
