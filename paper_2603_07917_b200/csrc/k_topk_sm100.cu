@@ -176,7 +176,6 @@ k_topk_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUten
     // per-query heap state in registers (see topk_heap.cuh for the invariant)
     int hcnt = 0;
     uint32_t rtop[4] = {0u, 0u, 0u, 0u};  // this slice's best R keys (orderable), descending
-    uint32_t bnd_next = 0u;
     uint64_t hroot = 0;
     uint64_t* heap = s_heap + qrow;
     float* wiw = s_iw + ew * 2 * tc::BN;  // double-buffered per warp
@@ -211,15 +210,18 @@ k_topk_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUten
       }
       __syncwarp();
       if (t + 1 < ntiles) fetch_iw(t + 1);  // overlaps this tile's epilogue
-      // cross-slice bound: every slice publishes the R-th best key it has seen
-      // (R = ceil(k / slices)); once all have, the union holds >= k rows at or
-      // above the minimum of those, so the global k-th key is >= it
-      // (maintained by the publishers in gmin[q]; loaded one tile ahead)
-      const uint32_t bnd = bnd_next;
-      if (rshare && q < nq && t + 1 < ntiles) bnd_next = __ldcg(grth + q);
+      // cross-slice bound (pure top-k): every slice publishes the R-th best
+      // key it has kept (R = ceil(k / slices)) in grth[slice][q]; once all
+      // have, the union holds >= k rows at or above the minimum of those, so
+      // the global k-th key is >= it.  Independent loads, overlapping the
+      // wait for this tile's MMA; a 0 slot (not yet published) means no bound.
+      if (rshare && q < nq) {
+        uint32_t m = ~0u;
+        for (int s2 = 0; s2 < (int)gridDim.y; ++s2) m = min(m, __ldcg(grth + (int64_t)s2 * nq + q));
+        if (m != 0u && m != ~0u) thr = fmaxf(thr, s_threshold(f32_unorder(m), iq));
+      }
       mbar_wait(&tfull[acc], (t >> 1) & 1);
       tc_fence_after();
-      if (bnd) thr = fmaxf(thr, s_threshold(f32_unorder(bnd), iq));
       const uint32_t tbase = tmem + ((uint32_t)(quarter * 32) << 16) + acc * tc::BN;
       auto chunk = [&](const int (&v)[32], const int c) {
         if (dbg & 4) return;  // debug: TMEM drain only
@@ -274,14 +276,7 @@ k_topk_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUten
                     }
                   }
                   const uint32_t now = rth();
-                  if (now != old) {  // publish, then refresh gmin[q] = min over slices
-                    uint32_t* slots = grth + nq;  // [slices][nq] after gmin[nq]
-                    __stcg(slots + (int64_t)slice * nq + q, now);
-                    uint32_t m = ~0u;
-                    for (int s2 = 0; s2 < (int)gridDim.y; ++s2)
-                      m = min(m, __ldcg(slots + (int64_t)s2 * nq + q));
-                    if (m) atomicMax(grth + q, m);
-                  }
+                  if (now != old) __stcg(grth + (int64_t)slice * nq + q, now);  // publish
                 }
                 int64_t rel = gbase + j;
                 if (rel < 0) rel += gcap;
@@ -487,17 +482,22 @@ static int launch_cg(const TopkArgs& a, uint64_t* partials, int n_slices, cudaSt
   const int dbg = env_int("SS_TC_DEBUG", 0) | (tc_prefetch() << 8);
   // cross-slice bound sharing: R = ceil(k / slices) <= 4 so every slice
   // tracks its best R keys in registers (needs >= 16 slices at k = 64)
+  // cross-slice bound sharing, opt-in (SS_TC_GTHR=1: a.gthr, slots after
+  // gmin[nq]).  Not used for pure top-k here: with ~148 slices the bound is
+  // each slice's best key (R = 1), too weak to pay for reading 148 slots per
+  // tile (theta=-1, nq=8: 0.65 vs 0.52 ms); the TS kernel shares instead.
+  uint32_t* slots = a.gthr ? a.gthr + a.nq : nullptr;
   int rshare = 0;
-  if (a.gthr && n_slices >= 2 && n_slices <= kMaxShareSlices) {
+  if (slots && n_slices >= 2 && n_slices <= kMaxShareSlices) {
     const int R = (a.k + n_slices - 1) / n_slices;
     if (R <= 4) rshare = R;
   }
   if (rshare)
-    SS_CUDA_TRY(cudaMemsetAsync(a.gthr, 0, (size_t)(n_slices + 1) * a.nq * sizeof(uint32_t), st));
+    SS_CUDA_TRY(cudaMemsetAsync(slots, 0, (size_t)n_slices * a.nq * sizeof(uint32_t), st));
   count_launch();
   SS_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_topk_tc<CG>, mq, mb, a.q_inv, a.nq, a.inv, a.n_rows,
                                  a.dim / tc::BK, stages, a.k, a.theta, a.head % a.gcap, a.gcap,
-                                 a.slot_offset, tps, partials, dbg, a.gthr, rshare));
+                                 a.slot_offset, tps, partials, dbg, slots, rshare));
   return SS_OK;
 }
 
