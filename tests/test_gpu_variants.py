@@ -14,7 +14,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 @pytest.mark.parametrize("env", [{"SS_TC_PAIR": "1"}, {"SS_TC_TSN": "256"}, {"SS_TC_TSN": "192"},
                                  {"SS_TC_TSN": "224"},
-                                 {"SS_TC_TS": "0"},
+                                 {"SS_TC_TS": "0"}, {"SS_TC_TS": "0", "SS_TC_GTHR": "1"},
+                                 {"SS_TC_SHARE": "0"},
                                  {"SS_TC_TS": "0", "SS_TC_CG": "2"}])
 def test_topk_variant_bit_exact(cuda, env):
     e = dict(os.environ, **env)
