@@ -360,12 +360,13 @@ def run_c5(args):
     """BASELINE configs[4] on one GPU: rolling trace replay against the c2
     bank (1M rows, pre-seeded), every round = completions pushed into the
     FIFO ring + arrivals predicted (stages 1-3) + bucket refreshes + full
-    re-rank + batch packing, all device-resident (replay_device.py)."""
+    re-rank + batch packing, all device-resident, one native C-ABI call per
+    round (ss_engine_round, csrc/k_engine.cu)."""
     import torch
 
     from paper_2603_07917_b200 import _build, _lib
     from paper_2603_07917_b200.history import HistoryWindow
-    from paper_2603_07917_b200.replay_device import DeviceReplay, DeviceTrace
+    from paper_2603_07917_b200.replay_device import DeviceTrace, NativeReplay
     from paper_2603_07917_b200.scheduler import RoundConfig
     from paper_2603_07917_b200.synthetic import inv_norm_device, make_bank_device
 
@@ -387,7 +388,7 @@ def run_c5(args):
                      torch.randint(1, 4097, (n_trace,), generator=g, device="cuda",
                                    dtype=torch.int32), tl)
     cfg = RoundConfig(k=K, theta=THETA, min_matches=MIN_MATCHES, max_len=MAX_LEN, nbins=NBINS)
-    dr = DeviceReplay(win, tr, cfg, A, TOK, B, MAXA)
+    dr = NativeReplay(win, tr, cfg, A, TOK, B, MAXA)  # one ss_engine_round call per round
     for _ in range(args.warmup):
         dr.round()
     torch.cuda.synchronize()
@@ -419,7 +420,8 @@ def run_c5(args):
                    "arrivals_per_round": A, "tokens_per_round": TOK, "batch": B, "k": K,
                    "nbins": NBINS, "theta": THETA,
                    "active_requests": [min(n_act), max(n_act)],
-                   "completions_pushed": dr.stats.completed, "refreshed": dr.stats.refreshed},
+                   "completions_pushed": dr.stats.completed,
+                   "driver": "native: one ss_engine_round C call per round"},
         "gpu_launches": int(_lib.launch_count() - c0), "clocks": clocks}), flush=True)
 
 

@@ -203,6 +203,33 @@ int ss_pack_batch(const int64_t* perm, const int32_t* input_len, const int32_t* 
                   int64_t* out_batch, int32_t* out_count, int64_t* out_tokens,
                   void* stream);
 
+/* -------------------------------------------------------- engine round -- */
+/* A GPU-resident table of active requests (ids ascending, two buffers for the
+ * stable compaction) and one C call per engine iteration (SPEC.md:462-470,
+ * scheduling state only): the last batch gains tokens_per_round tokens;
+ * requests reaching tr_true_len complete and enter the bank ring in batch
+ * order; up to max_arrivals trace requests from *next_id on
+ * are admitted and predicted (fused stages 1-3); bucket refreshes
+ * (SPEC.md:345-353); all active requests are ranked and the
+ * next batch packed (ss_pack_batch semantics, max_batch from the table).
+ * Trace arrays are device pointers indexed by request id (ids = arrival
+ * order).  Synchronises once (the completion count).  *next_id advances by
+ * the admitted count; *n_done_out / *n_admitted_out report the round. */
+typedef struct ss_table ss_table_t;
+int ss_table_create(ss_table_t** out, int32_t device, int64_t capacity, int32_t P,
+                    int32_t max_batch);
+int ss_table_destroy(ss_table_t* t);
+/* device pointers of the live buffer (rows [0, n_active)) for inspection */
+int ss_table_view(ss_table_t* t, int64_t* n_active, int32_t** input_len, int32_t** g,
+                  int64_t** ids, double** G, int32_t** npts, int64_t** perm,
+                  int64_t** run_ids, int32_t** batch_count);
+int ss_engine_round(ss_table_t* t, ss_bank_t* h, const int8_t* tr_emb, const float* tr_inv,
+                    const int32_t* tr_input_len, const int32_t* tr_true_len, int64_t tr_len,
+                    int64_t* next_id, int64_t max_arrivals, int32_t tokens_per_round,
+                    int32_t bucket_size, int64_t kv_capacity, int32_t mode, int32_t k,
+                    float theta, int32_t min_matches, int32_t max_len, int32_t nbins,
+                    int32_t algo, int64_t* n_done_out, int64_t* n_admitted_out, void* stream);
+
 /* ----------------------------------------------- fused scheduling round -- */
 /* One round for a batch of nq pending requests on a single-GPU bank:
  * ss_topk -> ss_bank_fallback_hist -> ss_finish -> ss_rank.  All device

@@ -49,6 +49,13 @@ SIGNATURES = {
     "ss_rank_workspace_bytes": (I64, [I64]),
     "ss_rank": (C.c_int, [P, P, I64, P, P, I64, P]),
     "ss_pack_batch": (C.c_int, [P, P, P, I64, I64, I32, I32, P, P, P, P]),
+    "ss_table_create": (C.c_int, [C.POINTER(P), I32, I64, I32, I32]),
+    "ss_table_destroy": (C.c_int, [P]),
+    "ss_table_view": (C.c_int, [P, C.POINTER(I64), C.POINTER(P), C.POINTER(P), C.POINTER(P),
+                                C.POINTER(P), C.POINTER(P), C.POINTER(P), C.POINTER(P),
+                                C.POINTER(P)]),
+    "ss_engine_round": (C.c_int, [P, P, P, P, P, P, I64, C.POINTER(I64), I64, I32, I32, I64, I32,
+                                  I32, F32, I32, I32, I32, I32, C.POINTER(I64), C.POINTER(I64), P]),
     "ss_schedule_round": (C.c_int, [P, P, P, P, P, I64, I32, F32, I32, I32, I32, I32, I32,
                                     P, P, P, P, P, P, P, P]),
     "ss_schedule_round_host": (C.c_int, [P, P, P, P, P, I64, I32, F32, I32, I32, I32, I32,

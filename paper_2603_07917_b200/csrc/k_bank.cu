@@ -19,17 +19,19 @@ k_bank_write(int8_t* __restrict__ emb, float* __restrict__ inv, int32_t* __restr
              const int8_t* __restrict__ src_emb, const float* __restrict__ src_inv,
              const int32_t* __restrict__ src_lens, const int64_t* __restrict__ src_seq,
              const int64_t* __restrict__ src_slot, int64_t n, int64_t first_seq,
-             int64_t capacity, int64_t skip, int* __restrict__ err) {
+             int64_t capacity, int64_t skip, int* __restrict__ err,
+             const int64_t* __restrict__ src_idx) {
   const int lane = threadIdx.x & 31;
   const int64_t r = skip + (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (r >= n) return;
+  const int64_t rs = src_idx ? src_idx[r] : r;  // source record (gather)
   const int64_t s = src_seq ? src_seq[r] : first_seq + r;
   const int64_t slot = src_slot ? src_slot[r] : s % capacity;
   if (slot < 0 || slot >= capacity) {
     if (lane == 0) atomicExch(err, SS_ERR_ARG);
     return;
   }
-  const int4* src = reinterpret_cast<const int4*>(src_emb + r * dim);
+  const int4* src = reinterpret_cast<const int4*>(src_emb + rs * dim);
   int4* dst = reinterpret_cast<int4*>(emb + slot * dim);
   int ss2 = 0;
   for (int w = lane; w < dim / 16; w += 32) {
@@ -42,7 +44,7 @@ k_bank_write(int8_t* __restrict__ emb, float* __restrict__ inv, int32_t* __restr
   for (int o = 16; o > 0; o >>= 1) ss2 += __shfl_xor_sync(0xffffffffu, ss2, o);
   if (lane == 0) {
     if (seq[slot] >= 0) atomicSub(&len_cnt[lens[slot] & 0xffff], 1);  // evicted record
-    int L = src_lens[r];
+    int L = src_lens[rs];
     if (L < 1 || L > 65535) {
       atomicExch(err, SS_ERR_RANGE);
       L = max(1, min(L, 65535));
@@ -51,7 +53,7 @@ k_bank_write(int8_t* __restrict__ emb, float* __restrict__ inv, int32_t* __restr
     lens[slot] = L;
     seq[slot] = s;
     float iv;
-    if (src_inv) iv = src_inv[r];
+    if (src_inv) iv = src_inv[rs];
     else iv = ss2 ? __fdiv_rn(1.0f, __fsqrt_rn((float)ss2)) : __int_as_float(0x7fc00000);
     inv[slot] = iv;
   }
@@ -61,13 +63,13 @@ int launch_bank_write(int8_t* emb, float* inv, int32_t* lens, int64_t* seq, int3
                       int dim, const int8_t* src_emb, const float* src_inv,
                       const int32_t* src_lens, const int64_t* src_seq, const int64_t* src_slot,
                       int64_t n, int64_t first_seq, int64_t capacity, int64_t skip, int* err,
-                      cudaStream_t st) {
+                      cudaStream_t st, const int64_t* src_idx) {
   int64_t m = n - skip;
   if (m <= 0) return SS_OK;
   count_launch();
   k_bank_write<<<(unsigned)((m + 7) / 8), 256, 0, st>>>(emb, inv, lens, seq, len_cnt, dim, src_emb,
                                                           src_inv, src_lens, src_seq, src_slot,
-                                                          n, first_seq, capacity, skip, err);
+                                                          n, first_seq, capacity, skip, err, src_idx);
   SS_LAUNCH_CHECK();
   return SS_OK;
 }

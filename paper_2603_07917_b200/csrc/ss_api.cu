@@ -560,7 +560,7 @@ static int round_impl(ss_bank* h, const int8_t* q, const float* q_inv, const int
                       const int64_t* ids, int64_t nq, int32_t k, float theta, int32_t min_matches,
                       int32_t max_len, int32_t nbins, int32_t algo, int32_t P, int32_t* npts,
                       int32_t* pbin, int32_t* pcnt, int64_t* pD, uint8_t* used_fb, double* G,
-                      int64_t* perm, size_t extra_front, cudaStream_t st) {
+                      int64_t* perm, size_t extra_front, cudaStream_t st, bool do_rank = true) {
   if (int rc = check_bins(max_len, nbins)) return rc;
   if (P < nbins) return set_error(SS_ERR_ARG, "P (%d) must be >= nbins (%d)", P, nbins);
   if (h->head <= 0) return set_error(SS_ERR_EMPTY, "cold start: the history window is empty");
@@ -598,8 +598,11 @@ static int round_impl(ss_bank* h, const int8_t* q, const float* q_inv, const int
                            len, min_matches, max_len, nbins, input_len, fb, fb + nbins,
                            fb + 2 * nbins, P, npts, pbin, pcnt, pD, nullptr, used_fb, G, st);
   if (rc) return rc;
+  if (!do_rank) return SS_OK;
   return launch_rank(G, ids, nq, perm, ws + L.rank, (int64_t)rank_workspace_bytes(nq), st);
 }
+
+
 
 int ss_schedule_round(ss_bank_t* h, const int8_t* q, const float* q_inv, const int32_t* input_len,
                       const int64_t* ids, int64_t nq, int32_t k, float theta, int32_t min_matches,
@@ -724,3 +727,27 @@ int ss_schedule_round_host(ss_bank_t* h, const int8_t* q_host, const float* q_in
 }
 
 }  // extern "C"
+
+namespace ss {
+int predict_into(ss_bank* h, const int8_t* q, const float* q_inv, const int32_t* input_len,
+                 int64_t nq, int32_t k, float theta, int32_t min_matches, int32_t max_len,
+                 int32_t nbins, int32_t algo, int32_t P, int32_t* npts, int32_t* pbin,
+                 int32_t* pcnt, int64_t* pD, uint8_t* used_fb, double* G, cudaStream_t st) {
+  return round_impl(h, q, q_inv, input_len, nullptr, nq, k, theta, min_matches, max_len, nbins,
+                    algo, P, npts, pbin, pcnt, pD, used_fb, G, nullptr, 0, st, false);
+}
+int bank_push_gather(ss_bank* h, const int8_t* src_emb, const float* src_inv,
+                     const int32_t* src_lens, const int64_t* src_idx, int64_t n, cudaStream_t st) {
+  if (h->gcap != h->cap || h->slot_offset != 0)
+    return set_error(SS_ERR_ARG, "push on a shard: use ss_bank_write with the global head");
+  if (n <= 0) return SS_OK;
+  const int64_t skip = n > h->cap ? n - h->cap : 0;
+  int rc = launch_bank_write(h->emb, h->inv, h->lens, h->seq, h->len_cnt, h->dim, src_emb, src_inv,
+                             src_lens, nullptr, nullptr, n, h->head, h->cap, skip, h->d_err, st,
+                             src_idx);
+  if (rc) return rc;
+  h->head += n;
+  return SS_OK;
+}
+}  // namespace ss
+

@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+struct ss_bank;  // the C-ABI bank handle (include/sagesched.h: ss_bank_t)
+
 namespace ss {
 
 void count_launch();
@@ -51,7 +53,7 @@ int launch_bank_write(int8_t* emb, float* inv, int32_t* lens, int64_t* seq, int3
                       int dim, const int8_t* src_emb, const float* src_inv,
                       const int32_t* src_lens, const int64_t* src_seq, const int64_t* src_slot,
                       int64_t n, int64_t first_seq, int64_t capacity, int64_t skip, int* err,
-                      cudaStream_t st);
+                      cudaStream_t st, const int64_t* src_idx = nullptr);
 int launch_fallback_hist(const int32_t* len_cnt, int max_len, int nbins, int64_t* cnt,
                          int64_t* sv, int64_t* sv2, cudaStream_t st);
 
@@ -115,6 +117,16 @@ int launch_refresh(int64_t n, const int32_t* I, const int32_t* g_new, int32_t* b
                    int bucket_size, const int32_t* npts, const int32_t* pcnt,
                    const int64_t* pD, int P, double* G_io, uint8_t* refreshed, int force,
                    cudaStream_t st);
+
+// fused stages 1-3 for a batch of pending requests into caller arrays (the
+// fused round without its rank), on bank h (ss_api.cu)
+int predict_into(ss_bank* h, const int8_t* q, const float* q_inv, const int32_t* input_len,
+                 int64_t nq, int32_t k, float theta, int32_t min_matches, int32_t max_len,
+                 int32_t nbins, int32_t algo, int32_t P, int32_t* npts, int32_t* pbin,
+                 int32_t* pcnt, int64_t* pD, uint8_t* used_fb, double* G, cudaStream_t st);
+// ring push of src rows src_idx[0..n) (gather) at the bank head (ss_api.cu)
+int bank_push_gather(::ss_bank* h, const int8_t* src_emb, const float* src_inv,
+                     const int32_t* src_lens, const int64_t* src_idx, int64_t n, cudaStream_t st);
 
 // batch formation (k_pack.cu)
 int launch_pack_batch(const int64_t* perm, const int32_t* I, const int32_t* g, int64_t n,

@@ -173,7 +173,7 @@ def _cuda_view(addr: int, dtype, shape, device: int) -> torch.Tensor:
         __cuda_array_interface__ = {
             "shape": tuple(shape),
             "typestr": {torch.int8: "|i1", torch.float32: "<f4", torch.int32: "<i4",
-                        torch.int64: "<i8"}[dtype],
+                        torch.int64: "<i8", torch.float64: "<f8"}[dtype],
             "data": (addr, False),
             "version": 3,
             "strides": None,

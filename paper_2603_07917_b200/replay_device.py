@@ -162,3 +162,80 @@ class DeviceReplay:
         n = self.n_act
         return dict(active_ids=self.table.ids[:n].cpu().numpy(), G=self.table.G[:n].cpu().numpy(),
                     perm=perm.cpu().numpy(), running=self.running())
+
+
+class NativeReplay:
+    """The same replay with each round a single C-ABI call (``ss_engine_round``,
+    csrc/k_engine.cu): progress, ring push, compaction, admission, refresh,
+    rank and packing all launched natively from one host call."""
+
+    def __init__(self, window: HistoryWindow, trace: DeviceTrace, cfg: RoundConfig,
+                 arrivals_per_round: int, tokens_per_round: int, batch_size: int,
+                 max_active: int, kv_capacity: int | None = None, pack_mode: str = "cut"):
+        import ctypes as C
+
+        from .scheduler import PACK_MODE
+
+        self._C = C
+        self.window, self.trace, self.cfg = window, trace, cfg
+        self.A, self.TOK, self.B = int(arrivals_per_round), int(tokens_per_round), int(batch_size)
+        self.K = (1 << 62) if kv_capacity is None else int(kv_capacity)
+        self.mode = PACK_MODE[pack_mode]
+        h = C.c_void_p()
+        _lib.call("ss_table_create", C.byref(h), torch.cuda.current_device(), int(max_active),
+                  cfg.nbins, self.B)
+        self._t = h
+        self._next = C.c_int64(0)
+        self.stats = ReplayStats()
+
+    def close(self):
+        if getattr(self, "_t", None) is not None and self._t.value:
+            _lib.lib().ss_table_destroy(self._t)
+            self._t = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def round(self) -> dict:
+        C, c, tr = self._C, self.cfg, self.trace
+        nd, na = C.c_int64(0), C.c_int64(0)
+        _lib.call("ss_engine_round", self._t, self.window.handle, _lib.ptr(tr.emb), _lib.ptr(tr.inv),
+                  _lib.ptr(tr.input_len), _lib.ptr(tr.true_len), len(tr), C.byref(self._next),
+                  self.A, self.TOK, c.bucket_size, self.K, self.mode, c.k,
+                  float(np.float32(c.theta)), c.min_matches, c.max_len, c.nbins, _lib.ALGO[c.algo],
+                  C.byref(nd), C.byref(na), _lib.stream_ptr())
+        self.stats.completed += nd.value
+        self.stats.admitted += na.value
+        n = self.n_act
+        if n:
+            self.stats.rounds += 1
+        return dict(n_active=n)
+
+    def _view(self):
+        C = self._C
+        n = C.c_int64(0)
+        ptrs = [C.c_void_p() for _ in range(8)]
+        _lib.call("ss_table_view", self._t, C.byref(n), *[C.byref(p) for p in ptrs])
+        return n.value, [p.value for p in ptrs]
+
+    @property
+    def n_act(self) -> int:
+        return self._view()[0]
+
+    def info(self, _=None) -> dict:
+        """Host copy of the round's state, in replay.replay's on_round format."""
+        from .history import _cuda_view
+
+        n, (pI, pg, pids, pG, pnp, pperm, prun, pcnt) = self._view()
+        dev = torch.cuda.current_device()
+        ids = _cuda_view(pids, torch.int64, (n,), dev).cpu().numpy()
+        G = _cuda_view(pG, torch.float64, (n,), dev).cpu().numpy()
+        perm = _cuda_view(pperm, torch.int64, (n,), dev).cpu().numpy()
+        cnt = int(_cuda_view(pcnt, torch.int32, (1,), dev).item())
+        if cnt < 0:
+            raise ValueError("request cannot fit: I + 1 exceeds the KV capacity")
+        run = _cuda_view(prun, torch.int64, (self.B,), dev)[:cnt].cpu().tolist()
+        return dict(active_ids=ids, G=G, perm=perm, running=run)

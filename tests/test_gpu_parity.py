@@ -699,3 +699,43 @@ def test_topk_dims_bit_exact(cuda, dim, nq):
         keys, seq, ref = _oracle_topk(w, be, q, qi, k, theta)
         comp, ln = w.topk(q, qi, k, theta, "tcgen05")
         _check_topk(w, comp, keys, seq, ref, k)
+
+
+@pytest.mark.parametrize("kv,mode", [(None, "cut"), (12_000, "skip")])
+def test_c5_native_engine_equals_device_replay(cuda, kv, mode):
+    """ss_engine_round (one native call per round) reproduces the torch-driven
+    device replay round by round, including the ring it leaves behind."""
+    from paper_2603_07917_b200.history import HistoryWindow
+    from paper_2603_07917_b200.replay import Trace
+    from paper_2603_07917_b200.replay_device import DeviceReplay, DeviceTrace, NativeReplay
+    from paper_2603_07917_b200.scheduler import RoundConfig
+    cap, dim, ntr = 3000, 128, 2500
+    emb, lens, _, _ = O.make_bank(cap + ntr, dim, 40, 93)
+    rng = np.random.default_rng(94)
+    tr = Trace(emb=emb[cap:], inv=O.inv_norm(emb[cap:]),
+               input_len=rng.integers(1, 4097, ntr).astype(np.int32),
+               true_len=np.clip(lens[cap:], 1, 500).astype(np.int32))
+    dtr = DeviceTrace.from_host(tr)
+    cfg = RoundConfig(k=16, theta=0.8, min_matches=5, max_len=2048, nbins=64)
+    A, TOK, B, R, MAXA = 80, 48, 64, 40, 700
+    w1 = HistoryWindow(cap, dim)
+    w1.push(emb[:cap], lens[:cap])
+    w2 = HistoryWindow(cap, dim)
+    w2.push(emb[:cap], lens[:cap])
+    ref = DeviceReplay(w1, dtr, cfg, A, TOK, B, MAXA, kv, mode)
+    nat = NativeReplay(w2, dtr, cfg, A, TOK, B, MAXA, kv, mode)
+    for r in range(R):
+        out = ref.round()
+        nat.round()
+        assert nat.n_act == ref.n_act, r
+        if ref.n_act:
+            a, b = ref.info(out["perm"]), nat.info()
+            assert np.array_equal(a["active_ids"], b["active_ids"]), r
+            assert np.array_equal(a["G"], b["G"]), r
+            assert np.array_equal(a["perm"], b["perm"]), r
+            assert a["running"] == b["running"], r
+    assert nat.stats.completed == ref.stats.completed > 50
+    e1, i1, l1, s1 = w1.tensors()
+    e2, i2, l2, s2 = w2.tensors()
+    assert w1.head == w2.head and torch.equal(s1, s2) and torch.equal(l1, l2) and torch.equal(e1, e2)
+    assert torch.equal(i1.view(torch.int32), i2.view(torch.int32))
