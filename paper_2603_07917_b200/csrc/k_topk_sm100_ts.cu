@@ -20,6 +20,8 @@
 #include <cudaTypedefs.h>
 #include <stdlib.h>
 
+#include <type_traits>
+
 #include "ss_common.cuh"
 #include "ss_internal.h"
 #include "topk_heap.cuh"
@@ -218,8 +220,8 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUten
   int* s_hcnt = reinterpret_cast<int*>(s_hroot + BM);                    // [128]
   int* s_hlock = s_hcnt + BM;                                            // [128]
   float* s_inv = reinterpret_cast<float*>(s_hlock + BM);                 // [ISLOTS][BN]
-  float* s_ib = s_inv + ISLOTS * 256;                                    // [8 warps][8]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(s_ib + EPI_WARPS * 8);
+  float* s_ib = s_inv + ISLOTS * 256;                                    // [8 warps][16]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(s_ib + EPI_WARPS * 16);
   uint64_t* a_full = bars;
   uint64_t* full = bars + 1;
   uint64_t* empty = full + stages;
@@ -359,7 +361,7 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUten
     }
     const float iq = (q < nq) ? q_inv[q] : __int_as_float(0x7fc00000);
     uint64_t* heap = s_heap + qrow;  // shared by the two column-half warps of this quarter
-    float* cib = s_ib + ew * 8;  // [max inv_w of chunk 0..3][min inv_w of chunk 0..3]
+    float* cib = s_ib + ew * 16;  // [max inv_w of half 0..7][min inv_w of half 0..7]
     if (dbg & 64) ntiles = 0;  // debug: MMA issue rate alone (no epilogue hand-off)
     float thr = (iq == iq) ? s_threshold(theta, iq) : INFINITY;
     for (int t = 0; t < ntiles; ++t) {
@@ -385,13 +387,13 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUten
         float hi = fmaxf(fmaxf(fmaxf(w4.x, w4.y), fmaxf(w4.z, w4.w)), 0.f);
         float lo = fminf(fminf(fminf(w4.x, w4.y), fminf(w4.z, w4.w)), INFINITY);
 #pragma unroll
-        for (int o = 1; o < 8; o <<= 1) {
+        for (int o = 1; o < 4; o <<= 1) {  // 4 lanes x 4 floats = one 16-column half
           hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
           lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
         }
-        if ((lane & 7) == 0 && (lane >> 3) < CPW + (TAIL ? 1 : 0)) {
-          cib[lane >> 3] = hi;
-          cib[4 + (lane >> 3)] = lo;
+        if ((lane & 3) == 0 && lane * 4 < HALF) {
+          cib[lane >> 2] = hi;
+          cib[8 + (lane >> 2)] = lo;
         }
       }
       __syncwarp();
@@ -430,45 +432,32 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUten
       // is negative) -- monotone rounding makes this a superset test, so the
       // exact per-column scores (one int->float conversion each, quarter rate)
       // are only computed for the rare chunks that pass it.
-      auto chunk = [&](const auto& v, const int c) {
-        constexpr int W = sizeof(v) / sizeof(v[0]);  // 32, or 8 for the N=208 tail
-        int md;
-        if constexpr (W == 32) {
-          int m[11];
+      // Filter per 16-column half: a half can only hold a score >= thr if
+      // fl(fl(max dot) * (max inv_w)) >= thr (or the min inv_w when every dot
+      // is negative) -- monotone rounding makes this a superset test, so the
+      // exact scores (one quarter-rate int->float conversion each) are only
+      // formed for the rare halves that pass it.
+      auto exact = [&](const auto& v, const int c, auto off_c, auto w_c) {
+        constexpr int OFF = decltype(off_c)::value;
+        constexpr int WW = decltype(w_c)::value;
+          float s[WW];
+          const float4* iw4 = reinterpret_cast<const float4*>(ciw + c * 32 + OFF);
 #pragma unroll
-          for (int j = 0; j < 10; ++j) m[j] = __vimax3_s32(v[3 * j], v[3 * j + 1], v[3 * j + 2]);
-          m[10] = max(v[30], v[31]);
-          md = __vimax3_s32(__vimax3_s32(m[0], m[1], m[2]), __vimax3_s32(m[3], m[4], m[5]),
-                            __vimax3_s32(__vimax3_s32(m[6], m[7], m[8]), m[9], m[10]));
-        } else if constexpr (W == 16) {
-          const int m0 = __vimax3_s32(v[0], v[1], v[2]), m1 = __vimax3_s32(v[3], v[4], v[5]);
-          const int m2 = __vimax3_s32(v[6], v[7], v[8]), m3 = __vimax3_s32(v[9], v[10], v[11]);
-          const int m4 = __vimax3_s32(v[12], v[13], v[14]);
-          md = __vimax3_s32(__vimax3_s32(m0, m1, m2), __vimax3_s32(m3, m4, v[15]), m0);
-        } else {
-          md = __vimax3_s32(__vimax3_s32(v[0], v[1], v[2]), __vimax3_s32(v[3], v[4], v[5]),
-                            max(v[6], v[7]));
-        }
-        const float bnd = __fmul_rn(__int2float_rn(md), md >= 0 ? cib[c] : cib[4 + c]);
-        if (!(dbg & 1) && bnd >= thr) {
-          float s[W];
-          const float4* iw4 = reinterpret_cast<const float4*>(ciw + c * 32);
-#pragma unroll
-          for (int j4 = 0; j4 < W / 4; ++j4) {
+          for (int j4 = 0; j4 < WW / 4; ++j4) {
             const float4 w = iw4[j4];
-            s[4 * j4 + 0] = __fmul_rn(__int2float_rn(v[4 * j4 + 0]), w.x);
-            s[4 * j4 + 1] = __fmul_rn(__int2float_rn(v[4 * j4 + 1]), w.y);
-            s[4 * j4 + 2] = __fmul_rn(__int2float_rn(v[4 * j4 + 2]), w.z);
-            s[4 * j4 + 3] = __fmul_rn(__int2float_rn(v[4 * j4 + 3]), w.w);
+            s[4 * j4 + 0] = __fmul_rn(__int2float_rn(v[OFF + 4 * j4 + 0]), w.x);
+            s[4 * j4 + 1] = __fmul_rn(__int2float_rn(v[OFF + 4 * j4 + 1]), w.y);
+            s[4 * j4 + 2] = __fmul_rn(__int2float_rn(v[OFF + 4 * j4 + 2]), w.z);
+            s[4 * j4 + 3] = __fmul_rn(__int2float_rn(v[OFF + 4 * j4 + 3]), w.w);
           }
-          const int64_t gbase = slot_offset + row0 + c * 32 - hmod;
+          const int64_t gbase = slot_offset + row0 + c * 32 + OFF - hmod;
           uint32_t mask = 0;
 #pragma unroll
-          for (int j = 0; j < W; ++j) mask |= (s[j] >= thr ? 1u : 0u) << j;
+          for (int j = 0; j < WW; ++j) mask |= (s[j] >= thr ? 1u : 0u) << j;
           if (!mask) return;
-          float sl[W];
+          float sl[WW];
 #pragma unroll
-          for (int j = 0; j < W; ++j) sl[j] = s[j];
+          for (int j = 0; j < WW; ++j) sl[j] = s[j];
           // this query's heap is shared with the other column-half warp: take
           // its lock (one lock per thread at a time, never nested)
           while (atomicCAS(&s_hlock[qrow], 0, 1) != 0) {
@@ -516,6 +505,46 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUten
           if constexpr (SHARE) {
             if (rth1 != rth0) __stcg(gslots + (int64_t)slice * nq + q, rth1);  // publish
           }
+      };
+      auto chunk = [&](const auto& v, const int c) {
+        constexpr int W = sizeof(v) / sizeof(v[0]);  // 32, or 8 for the N=208 tail
+        if constexpr (W == 32) {
+          const int a0 = __vimax3_s32(v[0], v[1], v[2]), a1 = __vimax3_s32(v[3], v[4], v[5]);
+          const int a2 = __vimax3_s32(v[6], v[7], v[8]), a3 = __vimax3_s32(v[9], v[10], v[11]);
+          const int a4 = __vimax3_s32(v[12], v[13], v[14]);
+          const int b0 = __vimax3_s32(v[16], v[17], v[18]), b1 = __vimax3_s32(v[19], v[20], v[21]);
+          const int b2 = __vimax3_s32(v[22], v[23], v[24]), b3 = __vimax3_s32(v[25], v[26], v[27]);
+          const int b4 = __vimax3_s32(v[28], v[29], v[30]);
+          const int mdl = __vimax3_s32(__vimax3_s32(a0, a1, a2), __vimax3_s32(a3, a4, v[15]), a0);
+          const int mdh = __vimax3_s32(__vimax3_s32(b0, b1, b2), __vimax3_s32(b3, b4, v[31]), b0);
+          const float bl = __fmul_rn(__int2float_rn(mdl), mdl >= 0 ? cib[2 * c] : cib[8 + 2 * c]);
+          const float bh =
+              __fmul_rn(__int2float_rn(mdh), mdh >= 0 ? cib[2 * c + 1] : cib[8 + 2 * c + 1]);
+          if constexpr (SHARE) {
+            // pure top-k: many chunks pass while the bounds rise -- one exact
+            // pass (and one heap lock) per 32 columns is cheaper there
+            if (!(dbg & 1) && fmaxf(bl, bh) >= thr)
+              exact(v, c, std::integral_constant<int, 0>(), std::integral_constant<int, 32>());
+          } else {
+            if (!(dbg & 1) && bl >= thr)
+              exact(v, c, std::integral_constant<int, 0>(), std::integral_constant<int, 16>());
+            if (!(dbg & 1) && bh >= thr)
+              exact(v, c, std::integral_constant<int, 16>(), std::integral_constant<int, 16>());
+          }
+        } else {  // the tail chunk: one half of 8 (BN = 208) or 16 (BN = 224) columns
+          int md;
+          if constexpr (W == 16) {
+            const int a0 = __vimax3_s32(v[0], v[1], v[2]), a1 = __vimax3_s32(v[3], v[4], v[5]);
+            const int a2 = __vimax3_s32(v[6], v[7], v[8]), a3 = __vimax3_s32(v[9], v[10], v[11]);
+            const int a4 = __vimax3_s32(v[12], v[13], v[14]);
+            md = __vimax3_s32(__vimax3_s32(a0, a1, a2), __vimax3_s32(a3, a4, v[15]), a0);
+          } else {
+            md = __vimax3_s32(__vimax3_s32(v[0], v[1], v[2]), __vimax3_s32(v[3], v[4], v[5]),
+                              max(v[6], v[7]));
+          }
+          const float bnd = __fmul_rn(__int2float_rn(md), md >= 0 ? cib[2 * c] : cib[8 + 2 * c]);
+          if (!(dbg & 1) && bnd >= thr)
+            exact(v, c, std::integral_constant<int, 0>(), std::integral_constant<int, W>());
         }
       };
       chunk(v0, 0);
@@ -556,7 +585,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 ts_encode() {
 }
 
 static size_t ts_fixed_smem(int k) {
-  return (size_t)k * ts::BM * 8 + ts::BM * 16 + ts::ISLOTS * 256 * 4 + ts::EPI_WARPS * 8 * 4 + 512 +
+  return (size_t)k * ts::BM * 8 + ts::BM * 16 + ts::ISLOTS * 256 * 4 + ts::EPI_WARPS * 16 * 4 + 512 +
          1024;
 }
 
