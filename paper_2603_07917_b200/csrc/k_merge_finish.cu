@@ -752,7 +752,23 @@ k_merge_finish_w(const uint64_t* __restrict__ partials, int nlists, int64_t nq, 
   const long long Iq = I[q];
   const int w = max_len / nbins;
   const bool fb = m < min_matches;
-  if (!fb) {
+  // <= k winners of length <= max_len: when k * max_len^2 < 2^32 the sums fit
+  // 32-bit shared-memory atomics (native adds instead of 64-bit CAS loops);
+  // they live in the first half of the 64-bit arrays' storage
+  const bool s32 = !fb && (long long)k * max_len * max_len < (1LL << 32);
+  uint32_t* sv32 = reinterpret_cast<uint32_t*>(f.h_sv);
+  uint32_t* sv2_32 = reinterpret_cast<uint32_t*>(f.h_sv2);
+  if (s32) {
+    for (int b = lane; b < nbins; b += 32) { f.h_cnt[b] = 0; sv32[b] = 0u; sv2_32[b] = 0u; }
+    __syncwarp();
+    for (int i = lane; i < m; i += 32) {
+      const int L = min(max(slen[i], 1), max_len);
+      const int b = (L - 1) / w;
+      atomicAdd(&f.h_cnt[b], 1);
+      atomicAdd(&sv32[b], (uint32_t)L);
+      atomicAdd(&sv2_32[b], (uint32_t)(L * L));
+    }
+  } else if (!fb) {
     for (int b = lane; b < nbins; b += 32) { f.h_cnt[b] = 0; f.h_sv[b] = 0; f.h_sv2[b] = 0; }
     __syncwarp();
     for (int i = lane; i < m; i += 32) {
@@ -778,14 +794,16 @@ k_merge_finish_w(const uint64_t* __restrict__ partials, int nlists, int64_t nq, 
     const unsigned bal = __ballot_sync(0xffffffffu, c > 0);
     if (c > 0) {
       const int pos = np + __popc(bal & lt);
-      const long long D = f.h_sv2[b] + 2 * Iq * f.h_sv[b];
+      const long long sv = s32 ? (long long)sv32[b] : f.h_sv[b];
+      const long long sv2 = s32 ? (long long)sv2_32[b] : f.h_sv2[b];
+      const long long D = sv2 + 2 * Iq * sv;
       f.l_c[pos] = c;
       f.l_D[pos] = D;
       if (pos < P) {
         pbin[q * P + pos] = b;
         pcnt[q * P + pos] = c;
         pD[q * P + pos] = D;
-        if (psv) psv[q * P + pos] = f.h_sv[b];
+        if (psv) psv[q * P + pos] = sv;
       }
     }
     np += __popc(bal);
