@@ -188,6 +188,67 @@ __device__ __noinline__ uint64_t heap_replace(uint64_t* heap, int k, uint64_t x)
 // ASPLIT: the last K-block of A lives in shared memory (TMA) instead of
 // TMEM, which frees 32 TMEM columns: two N=224 accumulators + 64 A columns
 // fill the 512 columns exactly.
+// The slow path of the pure-top-k (SHARE) filter, out of line: many chunks
+// pass there, and one copy of this code (instead of one per inlined chunk)
+// measured faster (1.29 vs 1.45 ms at c2, theta = -1); with a similarity
+// floor the path is rare and the call's register traffic makes it slower, so
+// the default instantiation keeps it inline.  Under the query's heap lock (the heap is shared with
+// the other column-half warp), insert the columns in `mask` whose exact key
+// passes theta; returns the tightened s-domain threshold.
+template <bool SHARE>
+__device__ __noinline__ float insert_locked(uint32_t mask, const float* sl, float iq, float theta,
+                                            int64_t gbase, int64_t gcap, uint64_t* heap, int k,
+                                            int* s_hlock, int* s_hcnt, uint64_t* s_hroot, int qrow,
+                                            uint32_t* s_rtop, int rshare, uint32_t* gslots,
+                                            int64_t slot_idx, float thr) {
+  while (atomicCAS(&s_hlock[qrow], 0, 1) != 0) {
+  }
+  __threadfence_block();
+  int hcnt = s_hcnt[qrow];
+  uint64_t hroot = s_hroot[qrow];
+  uint32_t rth0 = 0u;
+  if constexpr (SHARE) rth0 = s_rtop[qrow * 4 + rshare - 1];
+  while (mask) {
+    const int j = __ffs(mask) - 1;
+    mask &= mask - 1;
+    const float key = __fmul_rn(sl[j], iq);
+    if (key >= theta) {
+      int64_t rel = gbase + j;
+      if (rel < 0) rel += gcap;
+      const uint64_t comp = make_comp(key, (uint32_t)rel);
+      bool kept = true;
+      if (hcnt < k) {
+        heap[hcnt * BM] = comp;
+        if (++hcnt == k) hroot = heapify(heap, k);
+      } else if (comp > hroot) {
+        hroot = heap_replace(heap, k, comp);
+      } else {
+        kept = false;
+      }
+      if constexpr (SHARE) {
+        if (kept) {  // this slice's top-R keys, descending
+          uint32_t x = f32_order(key);
+          for (int i = 0; i < rshare; ++i) {
+            const uint32_t cur = s_rtop[qrow * 4 + i];
+            if (x > cur) { s_rtop[qrow * 4 + i] = x; x = cur; }
+          }
+        }
+      }
+    }
+  }
+  uint32_t rth1 = 0u;
+  if constexpr (SHARE) rth1 = s_rtop[qrow * 4 + rshare - 1];
+  s_hcnt[qrow] = hcnt;
+  s_hroot[qrow] = hroot;
+  __threadfence_block();
+  atomicExch(&s_hlock[qrow], 0);
+  if (hcnt >= k) thr = fmaxf(thr, s_threshold(comp_key(hroot), iq));
+  if constexpr (SHARE) {
+    if (rth1 != rth0) __stcg(gslots + slot_idx, rth1);  // publish
+  }
+  return thr;
+}
+
 // SHARE (pure top-k): every slice publishes the R-th best key it keeps per
 // query (gslots[slice][q], R = ceil(k / slices)); each tile, every slice
 // filters with the minimum over all slices' published keys -- once every
@@ -458,6 +519,12 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUten
           float sl[WW];
 #pragma unroll
           for (int j = 0; j < WW; ++j) sl[j] = s[j];
+          if constexpr (SHARE) {
+            thr = insert_locked<true>(mask, sl, iq, theta, gbase, gcap, heap, k, s_hlock, s_hcnt,
+                                      s_hroot, qrow, s_rtop, rshare, gslots,
+                                      (int64_t)slice * nq + q, thr);
+            return;
+          }
           // this query's heap is shared with the other column-half warp: take
           // its lock (one lock per thread at a time, never nested)
           while (atomicCAS(&s_hlock[qrow], 0, 1) != 0) {
