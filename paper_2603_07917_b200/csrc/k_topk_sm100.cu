@@ -49,7 +49,7 @@ k_topk_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUten
           const float* __restrict__ q_inv, int64_t nq, const float* __restrict__ inv,
           int64_t n_rows, int nkb, int stages, int k, float theta, int64_t hmod, int64_t gcap,
           int64_t slot_offset, int64_t tiles_per_slice, uint64_t* __restrict__ partials, int dbg,
-          uint32_t* __restrict__ grth, int rshare) {
+          uint32_t* __restrict__ grth, int rshare, int spread) {
   constexpr int BN_CTA = tc::BN / CG;          // B rows this CTA loads per tile
   constexpr int B_STAGE = BN_CTA * tc::BK;     // bytes per K-block stage per CTA
   extern __shared__ uint8_t smem_raw[];
@@ -171,7 +171,10 @@ k_topk_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUten
     const int ew = warp - tc::EPI_WARP0;        // 0..3
     const int quarter = warp & 3;               // TMEM lane quarter this warp may access
     const int qrow = quarter * 32 + lane;       // query row within the tile
-    const int64_t q = (int64_t)qt * tc::BM + qrow;
+    // spread (one query tile, nq <= 128): query i sits in TMEM row
+    // (i % 4) * 32 + i / 4, so a few queries occupy all four lane quarters and
+    // all four epilogue warps share the slow path (pure top-k)
+    const int64_t q = spread ? (int64_t)((qrow & 31) * 4 + (qrow >> 5)) : (int64_t)qt * tc::BM + qrow;
     const float iq = (q < nq) ? q_inv[q] : __int_as_float(0x7fc00000);
     // per-query heap state in registers (see topk_heap.cuh for the invariant)
     int hcnt = 0;
@@ -453,13 +456,37 @@ int topk_tc_slices(const TopkArgs& a, int device) {
   return (int)want;
 }
 
+// queries of a single tile copied to rows (i % 4) * 32 + i / 4 (see `spread`)
+__global__ void k_spread_queries(const int8_t* __restrict__ q, int64_t nq, int dim,
+                                 int8_t* __restrict__ out) {
+  const int i = blockIdx.x;
+  if (i >= nq) return;
+  const int r = (i & 3) * 32 + (i >> 2);
+  const int4* src = reinterpret_cast<const int4*>(q + (int64_t)i * dim);
+  int4* dst = reinterpret_cast<int4*>(out + (int64_t)r * dim);
+  for (int j = threadIdx.x; j < dim / 16; j += blockDim.x) dst[j] = src[j];
+}
+
 template <int CG>
 static int launch_cg(const TopkArgs& a, uint64_t* partials, int n_slices, cudaStream_t st) {
   const int stages = tc_stages(a.dim, a.k, CG);
   if (stages < 2) return set_error(SS_ERR_UNSUPPORTED, "tcgen05: not enough shared memory");
   const size_t smem = tc_fixed_smem(a.dim, a.k) + (size_t)stages * (tc::BN / CG) * tc::BK;
   CUtensorMap mq, mb;
-  if (int rc = make_map(&mq, a.q, a.nq, a.dim, tc::BM)) return rc;
+  // pure top-k on a single query tile: spread the queries over the four TMEM
+  // lane quarters so every epilogue warp shares the (then frequent) exact
+  // path (rows past nq in the scratch are never used: their query index maps
+  // >= nq).  With a similarity floor the exact path is rare and the extra
+  // copy launch would only cost time.
+  const int spread = (CG == 1 && a.nq <= tc::BM && a.qscratch && a.theta <= 0.f) ? 1 : 0;
+  if (spread) {
+    count_launch();
+    k_spread_queries<<<(unsigned)a.nq, 32, 0, st>>>(a.q, a.nq, a.dim, a.qscratch);
+    SS_LAUNCH_CHECK();
+    if (int rc = make_map(&mq, a.qscratch, tc::BM, a.dim, tc::BM)) return rc;
+  } else if (int rc = make_map(&mq, a.q, a.nq, a.dim, tc::BM)) {
+    return rc;
+  }
   if (int rc = make_map(&mb, a.emb, a.n_rows, a.dim, tc::BN / CG)) return rc;
   SS_CUDA_TRY(cudaFuncSetAttribute(k_topk_tc<CG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)smem));
@@ -497,7 +524,7 @@ static int launch_cg(const TopkArgs& a, uint64_t* partials, int n_slices, cudaSt
   count_launch();
   SS_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_topk_tc<CG>, mq, mb, a.q_inv, a.nq, a.inv, a.n_rows,
                                  a.dim / tc::BK, stages, a.k, a.theta, a.head % a.gcap, a.gcap,
-                                 a.slot_offset, tps, partials, dbg, slots, rshare));
+                                 a.slot_offset, tps, partials, dbg, slots, rshare, spread));
   return SS_OK;
 }
 

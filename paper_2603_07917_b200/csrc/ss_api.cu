@@ -115,6 +115,7 @@ struct ss_bank {
   int64_t gthr_cap = 0;
   uint32_t* gslots = nullptr;  // TS kernel pure top-k: per-slice published bounds
   int64_t gslots_cap = 0;
+  int8_t* qscratch = nullptr;  // 128 x dim: single-tile query spread (k_topk_tc)
   // side stream of the fused round: the fallback histogram runs concurrently
   // with the similarity kernel (fork/join by events; captured as two graph
   // branches when the caller's stream is being captured)
@@ -303,6 +304,7 @@ int ss_bank_create(ss_bank_t** out, int32_t device, int64_t capacity, int32_t di
   else if ((e = cudaMalloc(&h->seq, (size_t)capacity * 8)) != cudaSuccess) fail(e);
   else if ((e = cudaMalloc(&h->len_cnt, 65536 * 4)) != cudaSuccess) fail(e);
   else if ((e = cudaMalloc(&h->d_err, sizeof(int))) != cudaSuccess) fail(e);
+  else if ((e = cudaMalloc(&h->qscratch, (size_t)128 * dim)) != cudaSuccess) fail(e);
   else if ((e = cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking)) != cudaSuccess) fail(e);
   else if ((e = cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming)) != cudaSuccess) fail(e);
   else if ((e = cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming)) != cudaSuccess) fail(e);
@@ -336,6 +338,7 @@ int ss_bank_destroy(ss_bank_t* h) {
   cudaFree(h->ws);
   cudaFree(h->gthr);
   cudaFree(h->gslots);
+  cudaFree(h->qscratch);
   if (h->host_exec) cudaGraphExecDestroy(h->host_exec);
   if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
@@ -448,6 +451,7 @@ static int topk_impl(ss_bank* h, const int8_t* q, const float* q_inv, int64_t nq
   a.inv_padded = true;  // the bank pads inv with one NaN tile
   a.gthr = gthr_reserve(h, nq);
   a.gslots = gslots_reserve(h, nq, theta);
+  a.qscratch = h->qscratch;
   int slices = 1;
   if (int rc = topk_plan(h, a, algo, slices)) return rc;
   size_t need = ws_offset + align_up((size_t)slices * nq * k * 8);
@@ -476,6 +480,7 @@ int ss_topk_partials(ss_bank_t* h, const int8_t* q, const float* q_inv, int64_t 
   a.inv_padded = true;  // the bank pads inv with one NaN tile
   a.gthr = gthr_reserve(h, nq);
   a.gslots = gslots_reserve(h, nq, theta);
+  a.qscratch = h->qscratch;
   int slices = 1;
   if (int rc = topk_plan(h, a, algo, slices)) return rc;
   if (slices > max_slices) slices = max_slices;
@@ -580,6 +585,7 @@ static int round_impl(ss_bank* h, const int8_t* q, const float* q_inv, const int
   a.inv_padded = true;  // the bank pads inv with one NaN tile
   a.gthr = gthr_reserve(h, nq);
   a.gslots = gslots_reserve(h, nq, theta);
+  a.qscratch = h->qscratch;
   int slices = 1;
   if (int rc = topk_plan(h, a, algo, slices)) return rc;
   uint64_t* partials = reinterpret_cast<uint64_t*>((char*)h->ws + base + L.end);

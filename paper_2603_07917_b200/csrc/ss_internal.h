@@ -81,6 +81,9 @@ struct TopkArgs {
   // every slice filters with the minimum over slices (a lower bound of the
   // global k-th key once all have published)
   uint32_t* gslots = nullptr;
+  // optional 128 x dim scratch: a single query tile is re-laid out across the
+  // four TMEM lane quarters (k_topk_tc `spread`)
+  int8_t* qscratch = nullptr;
 };
 constexpr int kMaxShareSlices = 160;
 int launch_topk_scan(const TopkArgs& a, uint64_t* partials, int n_slices, cudaStream_t st);
