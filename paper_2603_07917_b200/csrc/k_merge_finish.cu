@@ -498,23 +498,6 @@ k_finish(const uint64_t* __restrict__ comp, const int32_t* __restrict__ len, int
              s_warp);
 }
 
-int launch_finish(const uint64_t* comp, const int32_t* len, int64_t nq, int k, int min_matches,
-                  int max_len, int nbins, const int32_t* I, const int64_t* fb_cnt,
-                  const int64_t* fb_sv, const int64_t* fb_sv2, int P, int32_t* npts,
-                  int32_t* pbin, int32_t* pcnt, int64_t* pD, int64_t* psv, uint8_t* used_fb,
-                  double* G, cudaStream_t st) {
-  if (nq <= 0) return SS_OK;
-  size_t smem = finish_smem(nbins);
-  if (smem > 200 * 1024) return set_error(SS_ERR_UNSUPPORTED, "nbins %d too large", nbins);
-  if (smem > 48 * 1024)
-    SS_CUDA_TRY(cudaFuncSetAttribute(k_finish, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  count_launch();
-  k_finish<<<(unsigned)nq, MF_THREADS, smem, st>>>(comp, len, nq, k, min_matches, max_len, nbins, I,
-                                                  fb_cnt, fb_sv, fb_sv2, P, npts, pbin, pcnt, pD,
-                                                  psv, used_fb, G);
-  SS_LAUNCH_CHECK();
-  return SS_OK;
-}
 
 // ---------------------------------------------------------------------------
 // merge + finish fused (single-GPU round): per request, select the global
@@ -566,6 +549,88 @@ k_merge_finish(const uint64_t* __restrict__ partials, int nlists, int64_t nq, in
 //      ballot compaction of the bins, exact integer Gittins (warp scan)
 // ---------------------------------------------------------------------------
 constexpr int MFW_WARPS = 4;
+
+// histogram of the m winners' lengths (or the fallback law) -> ascending
+// compaction of the non-empty bins into the sparse cost law -> exact Gittins;
+// one warp per request (shared by the fused merge+finish and k_finish_w)
+__device__ __forceinline__ void warp_finish_tail(
+    const int32_t* slen, int m, int64_t q, int k, int min_matches, int max_len, int nbins,
+    long long Iq_in, const int64_t* __restrict__ fb_cnt, const int64_t* __restrict__ fb_sv,
+    const int64_t* __restrict__ fb_sv2, int P, int32_t* __restrict__ npts,
+    int32_t* __restrict__ pbin, int32_t* __restrict__ pcnt, int64_t* __restrict__ pD,
+    int64_t* __restrict__ psv, uint8_t* __restrict__ used_fb, double* __restrict__ G,
+    FinishSmem f, int lane) {
+  const unsigned lt = (1u << lane) - 1u;
+  // 3b. histogram of the winners (or the fallback law)
+  const long long Iq = Iq_in;
+  const int w = max_len / nbins;
+  const bool fb = m < min_matches;  // SPEC.md:184
+  // <= k winners of length <= max_len: when k * max_len^2 < 2^32 the sums fit
+  // 32-bit shared-memory atomics (native adds instead of 64-bit CAS loops);
+  // they live in the first half of the 64-bit arrays' storage
+  const bool s32 = !fb && (long long)k * max_len * max_len < (1LL << 32);
+  uint32_t* sv32 = reinterpret_cast<uint32_t*>(f.h_sv);
+  uint32_t* sv2_32 = reinterpret_cast<uint32_t*>(f.h_sv2);
+  if (s32) {
+    for (int b = lane; b < nbins; b += 32) { f.h_cnt[b] = 0; sv32[b] = 0u; sv2_32[b] = 0u; }
+    __syncwarp();
+    for (int i = lane; i < m; i += 32) {
+      const int L = min(max(slen[i], 1), max_len);
+      const int b = (L - 1) / w;
+      atomicAdd(&f.h_cnt[b], 1);
+      atomicAdd(&sv32[b], (uint32_t)L);
+      atomicAdd(&sv2_32[b], (uint32_t)(L * L));
+    }
+  } else if (!fb) {
+    for (int b = lane; b < nbins; b += 32) { f.h_cnt[b] = 0; f.h_sv[b] = 0; f.h_sv2[b] = 0; }
+    __syncwarp();
+    for (int i = lane; i < m; i += 32) {
+      const int L = min(max(slen[i], 1), max_len);
+      const int b = (L - 1) / w;
+      atomicAdd(&f.h_cnt[b], 1);
+      atomicAdd(reinterpret_cast<unsigned long long*>(&f.h_sv[b]), (unsigned long long)L);
+      atomicAdd(reinterpret_cast<unsigned long long*>(&f.h_sv2[b]),
+                (unsigned long long)((long long)L * L));
+    }
+  } else {
+    for (int b = lane; b < nbins; b += 32) {
+      f.h_cnt[b] = (int32_t)fb_cnt[b];
+      f.h_sv[b] = fb_sv[b];
+      f.h_sv2[b] = fb_sv2[b];
+    }
+  }
+  __syncwarp();
+  int np = 0;
+  for (int b0 = 0; b0 < nbins; b0 += 32) {
+    const int b = b0 + lane;
+    const int c = (b < nbins) ? f.h_cnt[b] : 0;
+    const unsigned bal = __ballot_sync(0xffffffffu, c > 0);
+    if (c > 0) {
+      const int pos = np + __popc(bal & lt);
+      const long long sv = s32 ? (long long)sv32[b] : f.h_sv[b];
+      const long long sv2 = s32 ? (long long)sv2_32[b] : f.h_sv2[b];
+      const long long D = sv2 + 2 * Iq * sv;
+      f.l_c[pos] = c;
+      f.l_D[pos] = D;
+      if (pos < P) {
+        pbin[q * P + pos] = b;
+        pcnt[q * P + pos] = c;
+        pD[q * P + pos] = D;
+        if (psv) psv[q * P + pos] = sv;
+      }
+    }
+    np += __popc(bal);
+  }
+  __syncwarp();
+  const double g = (np > 0) ? warp_gittins_exact(f.l_c, f.l_D, np, 0, (int)Iq, 0, 0, lane) : INFINITY;
+  if (lane == 0) {
+    G[q] = g;
+    npts[q] = np;
+    if (used_fb) used_fb[q] = fb ? 1 : 0;
+  }
+}
+
+
 
 __device__ __forceinline__ int warp_sum_i32(int v) {
 #pragma unroll
@@ -748,73 +813,75 @@ k_merge_finish_w(const uint64_t* __restrict__ partials, int nlists, int64_t nq, 
     if (out_comp) out_comp[q * k + i] = (i < m) ? sel[i] : 0ull;
     if (out_len) out_len[q * k + i] = (i < m) ? slen[i] : 0;
   }
-  // 3b. histogram of the winners (or the fallback law)
-  const long long Iq = I[q];
-  const int w = max_len / nbins;
-  const bool fb = m < min_matches;  // SPEC.md:184
-  // <= k winners of length <= max_len: when k * max_len^2 < 2^32 the sums fit
-  // 32-bit shared-memory atomics (native adds instead of 64-bit CAS loops);
-  // they live in the first half of the 64-bit arrays' storage
-  const bool s32 = !fb && (long long)k * max_len * max_len < (1LL << 32);
-  uint32_t* sv32 = reinterpret_cast<uint32_t*>(f.h_sv);
-  uint32_t* sv2_32 = reinterpret_cast<uint32_t*>(f.h_sv2);
-  if (s32) {
-    for (int b = lane; b < nbins; b += 32) { f.h_cnt[b] = 0; sv32[b] = 0u; sv2_32[b] = 0u; }
-    __syncwarp();
-    for (int i = lane; i < m; i += 32) {
-      const int L = min(max(slen[i], 1), max_len);
-      const int b = (L - 1) / w;
-      atomicAdd(&f.h_cnt[b], 1);
-      atomicAdd(&sv32[b], (uint32_t)L);
-      atomicAdd(&sv2_32[b], (uint32_t)(L * L));
-    }
-  } else if (!fb) {
-    for (int b = lane; b < nbins; b += 32) { f.h_cnt[b] = 0; f.h_sv[b] = 0; f.h_sv2[b] = 0; }
-    __syncwarp();
-    for (int i = lane; i < m; i += 32) {
-      const int L = min(max(slen[i], 1), max_len);
-      const int b = (L - 1) / w;
-      atomicAdd(&f.h_cnt[b], 1);
-      atomicAdd(reinterpret_cast<unsigned long long*>(&f.h_sv[b]), (unsigned long long)L);
-      atomicAdd(reinterpret_cast<unsigned long long*>(&f.h_sv2[b]),
-                (unsigned long long)((long long)L * L));
-    }
-  } else {
-    for (int b = lane; b < nbins; b += 32) {
-      f.h_cnt[b] = (int32_t)fb_cnt[b];
-      f.h_sv[b] = fb_sv[b];
-      f.h_sv2[b] = fb_sv2[b];
-    }
+  warp_finish_tail(slen, m, q, k, min_matches, max_len, nbins, I[q], fb_cnt, fb_sv, fb_sv2, P, npts,
+                   pbin, pcnt, pD, psv, used_fb, G, f, lane);
+}
+
+// finish for neighbour lists already merged (ss_finish: the predictor API and
+// the multi-GPU round): one warp per request; the list's non-zero
+// composites and their lengths are compacted into per-warp smem, then the
+// shared tail (histogram -> cost law -> Gittins)
+__global__ void __launch_bounds__(MFW_WARPS * 32)
+k_finish_w(const uint64_t* __restrict__ comp, const int32_t* __restrict__ len, int64_t nq, int k,
+           int min_matches, int max_len, int nbins, const int32_t* __restrict__ I,
+           const int64_t* __restrict__ fb_cnt, const int64_t* __restrict__ fb_sv,
+           const int64_t* __restrict__ fb_sv2, int P, int32_t* __restrict__ npts,
+           int32_t* __restrict__ pbin, int32_t* __restrict__ pcnt, int64_t* __restrict__ pD,
+           int64_t* __restrict__ psv, uint8_t* __restrict__ used_fb, double* __restrict__ G,
+           size_t warp_bytes) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t q = (int64_t)blockIdx.x * MFW_WARPS + warp;
+  pdl_wait();
+  if (q >= nq) return;  // warp-uniform
+  unsigned char* base = smem + warp * warp_bytes;
+  int32_t* slen = reinterpret_cast<int32_t*>(base);  // [k]
+  FinishSmem f = carve_finish(base + (((size_t)k * 4 + 15) & ~(size_t)15), nbins);
+  const unsigned lt = (1u << lane) - 1u;
+  int m = 0;
+  for (int i0 = 0; i0 < k; i0 += 32) {
+    const int i = i0 + lane;
+    const bool nz = i < k && comp[q * k + i] != 0ull;
+    const unsigned b = __ballot_sync(0xffffffffu, nz);
+    if (nz) slen[m + __popc(b & lt)] = len[q * k + i];
+    m += __popc(b);
   }
   __syncwarp();
-  int np = 0;
-  for (int b0 = 0; b0 < nbins; b0 += 32) {
-    const int b = b0 + lane;
-    const int c = (b < nbins) ? f.h_cnt[b] : 0;
-    const unsigned bal = __ballot_sync(0xffffffffu, c > 0);
-    if (c > 0) {
-      const int pos = np + __popc(bal & lt);
-      const long long sv = s32 ? (long long)sv32[b] : f.h_sv[b];
-      const long long sv2 = s32 ? (long long)sv2_32[b] : f.h_sv2[b];
-      const long long D = sv2 + 2 * Iq * sv;
-      f.l_c[pos] = c;
-      f.l_D[pos] = D;
-      if (pos < P) {
-        pbin[q * P + pos] = b;
-        pcnt[q * P + pos] = c;
-        pD[q * P + pos] = D;
-        if (psv) psv[q * P + pos] = sv;
-      }
+  warp_finish_tail(slen, m, q, k, min_matches, max_len, nbins, I[q], fb_cnt, fb_sv, fb_sv2, P, npts,
+                   pbin, pcnt, pD, psv, used_fb, G, f, lane);
+}
+
+int launch_finish(const uint64_t* comp, const int32_t* len, int64_t nq, int k, int min_matches,
+                  int max_len, int nbins, const int32_t* I, const int64_t* fb_cnt,
+                  const int64_t* fb_sv, const int64_t* fb_sv2, int P, int32_t* npts,
+                  int32_t* pbin, int32_t* pcnt, int64_t* pD, int64_t* psv, uint8_t* used_fb,
+                  double* G, cudaStream_t st) {
+  if (nq <= 0) return SS_OK;
+  {
+    const size_t wb = (((size_t)k * 4 + 15) & ~(size_t)15) + ((finish_smem(nbins) + 15) & ~(size_t)15);
+    const size_t smem = wb * MFW_WARPS;
+    if (smem <= 200 * 1024) {
+      if (smem > 48 * 1024)
+        SS_CUDA_TRY(cudaFuncSetAttribute(k_finish_w, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem));
+      count_launch();
+      SS_CUDA_TRY(pdl_launch(k_finish_w, dim3((unsigned)((nq + MFW_WARPS - 1) / MFW_WARPS)),
+                             dim3(MFW_WARPS * 32), smem, st, comp, len, nq, k, min_matches, max_len,
+                             nbins, I, fb_cnt, fb_sv, fb_sv2, P, npts, pbin, pcnt, pD, psv, used_fb,
+                             G, wb));
+      return SS_OK;
     }
-    np += __popc(bal);
   }
-  __syncwarp();
-  const double g = (np > 0) ? warp_gittins_exact(f.l_c, f.l_D, np, 0, (int)Iq, 0, 0, lane) : INFINITY;
-  if (lane == 0) {
-    G[q] = g;
-    npts[q] = np;
-    if (used_fb) used_fb[q] = fb ? 1 : 0;
-  }
+  size_t smem = finish_smem(nbins);
+  if (smem > 200 * 1024) return set_error(SS_ERR_UNSUPPORTED, "nbins %d too large", nbins);
+  if (smem > 48 * 1024)
+    SS_CUDA_TRY(cudaFuncSetAttribute(k_finish, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  count_launch();
+  k_finish<<<(unsigned)nq, MF_THREADS, smem, st>>>(comp, len, nq, k, min_matches, max_len, nbins, I,
+                                                  fb_cnt, fb_sv, fb_sv2, P, npts, pbin, pcnt, pD,
+                                                  psv, used_fb, G);
+  SS_LAUNCH_CHECK();
+  return SS_OK;
 }
 
 int launch_merge_finish(const uint64_t* partials, int nlists, int64_t nq, int k,
