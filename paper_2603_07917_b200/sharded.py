@@ -135,6 +135,7 @@ class ShardedScheduler:
         self.cfg = cfg
         self.group = history.group
         self._bufs = {}
+        self._side = None
 
     def _buffers(self, nq: int):
         b = self._bufs.get(nq)
@@ -159,9 +160,15 @@ class ShardedScheduler:
         c = self.cfg
         nq = q.shape[0]
         out = self._buffers(nq)
-        fb = self.h.window.fallback_hist(c.max_len, c.nbins)
-        fb_work = dist.all_reduce(fb, op=dist.ReduceOp.SUM, group=self.group,
-                                  async_op=True)                                # 5 (overlapped)
+        # 5, overlapped: the window's fallback histogram and its all-reduce run
+        # on a side stream while the queries are gathered and scored
+        if self._side is None:
+            self._side = torch.cuda.Stream()
+        main = torch.cuda.current_stream()
+        self._side.wait_stream(main)
+        with torch.cuda.stream(self._side):
+            fb = self.h.window.fallback_hist(c.max_len, c.nbins, stream=self._side)
+            fb_work = dist.all_reduce(fb, op=dist.ReduceOp.SUM, group=self.group, async_op=True)
         q_all, qi_all = gather_queries(q, q_inv, self.group)                    # 1
         comp_all, len_all = self.h.window.topk(q_all, qi_all, c.k, c.theta, c.algo)  # 2
         comp_x, len_x = exchange_candidates(comp_all, len_all, self.group)      # 3
@@ -169,7 +176,9 @@ class ShardedScheduler:
         comp, ln = out["comp"], out["len"]
         _lib.call("ss_merge_topk", _lib.ptr(comp_x), _lib.ptr(len_x), world, nq, c.k,
                   _lib.ptr(comp), _lib.ptr(ln), _lib.stream_ptr())              # 4
-        fb_work.wait()
+        with torch.cuda.stream(self._side):
+            fb_work.wait()
+        main.wait_stream(self._side)
         P = c.nbins
         I = torch.as_tensor(input_len, device="cuda").to(torch.int32)
         _lib.call("ss_finish", _lib.ptr(comp), _lib.ptr(ln), nq, c.k, c.min_matches, c.max_len,
