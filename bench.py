@@ -252,7 +252,10 @@ def run_sharded(args, world, rank, local):
     dq, dqi, dI, dids = (torch.as_tensor(x, device="cuda") for x in (q, qi, I, ids))
     cfg = RoundConfig(k=K, theta=THETA, min_matches=MIN_MATCHES, max_len=MAX_LEN, nbins=NBINS,
                       algo=args.algo)
-    sched = ShardedScheduler(hist, cfg)
+    # SS_SHARD_EXCHANGE=p2p: fused merge + exchange over IPC-mapped peer
+    # buffers (ss_topk_scatter) instead of the candidate all_to_all
+    exchange = os.environ.get("SS_SHARD_EXCHANGE", "nccl")
+    sched = ShardedScheduler(hist, cfg, exchange=exchange)
     c0 = _lib.launch_count()
     sched.schedule_round(dq, dqi, dI, dids)
     torch.cuda.synchronize()
@@ -335,7 +338,9 @@ def run_sharded(args, world, rank, local):
                        f"1024-request queue per GPU", "bank_rows": N_BANK, "dim": DIM,
                        "nq_per_gpu": NQ, "k": K, "nbins": NBINS, "theta": THETA,
                        "similarity": algo_used, "n_slices": n_slices,
-                       "parallelism": f"bank shard x{world} + NCCL all-gather/all-to-all/all-reduce",
+                       "parallelism": f"bank shard x{world} + NCCL all-gather/all-reduce + "
+                                      + ("P2P fused merge-exchange" if exchange == "p2p"
+                                         else "NCCL all-to-all"),
                        "graph": graph is not None,
                        "l2": "bank shard streamed from HBM each round"},
             "e2e": {"value": round(req * args.steps / (e2e_ms / 1e3), 1), "unit": "requests/s",

@@ -149,6 +149,30 @@ int ss_topk_partials(ss_bank_t* h, const int8_t* q, const float* q_inv, int64_t 
 int ss_merge_topk(const uint64_t* comp, const int32_t* len, int32_t nlists,
                   int64_t nq, int32_t k, uint64_t* out_comp, int32_t* out_len,
                   void* stream);
+/* Fused merge + exchange of the multi-GPU round (SURVEY 8(e) stage 3,
+ * replacing the candidate all_to_all that follows the reference's per-process
+ * top-k, sagesched/predictor/_kernels.py:40 run per shard): the local top-k of
+ * nq = world * nq_local queries (rank-major: rows [r*nq_local, (r+1)*nq_local)
+ * are rank r's queue) against this rank's shard, whose merge kernel stores
+ * each merged row straight into the owner's receive buffer -- peer_comp_host[r]
+ * / peer_len_host[r] (device pointers, IPC-mapped for r != rank) laid out
+ * [world][nq_local][k] -- at row [rank][q % nq_local], as NVLink P2P stores.
+ * The caller orders the peers' reads after a barrier (e.g. a 1-element NCCL
+ * all_reduce) and then merges its receive buffer with ss_merge_topk.
+ * world <= 8 (one NVLink/NVSwitch node); nq % world == 0.  Async. */
+#define SS_IPC_HANDLE_BYTES 64
+int ss_topk_scatter(ss_bank_t* h, const int8_t* q, const float* q_inv, int64_t nq,
+                    int32_t k, float theta, int32_t algo, int32_t world, int32_t rank,
+                    uint64_t* const* peer_comp_host, int32_t* const* peer_len_host,
+                    void* stream);
+/* IPC-exportable device buffers for ss_topk_scatter: cudaMalloc'd (zeroed) on
+ * `device`, exported as a 64-byte handle, opened (peer-mapped) by the other
+ * ranks of the node.  Synchronous. */
+int ss_ipc_malloc(int32_t device, int64_t bytes, void** out);
+int ss_ipc_free(void* ptr);
+int ss_ipc_handle(const void* ptr, uint8_t* handle_host);
+int ss_ipc_open(const uint8_t* handle_host, void** out);
+int ss_ipc_close(void* ptr);
 /* decode composites: key f32, seq = head - capacity + rel, global slot. Async. */
 int ss_decode_topk(const uint64_t* comp, int64_t n, int64_t head, int64_t capacity,
                    float* out_key, int64_t* out_seq, int64_t* out_slot, void* stream);

@@ -43,6 +43,12 @@ SIGNATURES = {
     "ss_topk": (C.c_int, [P, P, P, I64, I32, F32, I32, P, P, P]),
     "ss_topk_partials": (C.c_int, [P, P, P, I64, I32, F32, I32, P, I32, C.POINTER(I32), P]),
     "ss_merge_topk": (C.c_int, [P, P, I32, I64, I32, P, P, P]),
+    "ss_topk_scatter": (C.c_int, [P, P, P, I64, I32, F32, I32, I32, I32, P, P, P]),
+    "ss_ipc_malloc": (C.c_int, [I32, I64, C.POINTER(P)]),
+    "ss_ipc_free": (C.c_int, [P]),
+    "ss_ipc_handle": (C.c_int, [P, P]),
+    "ss_ipc_open": (C.c_int, [P, C.POINTER(P)]),
+    "ss_ipc_close": (C.c_int, [P]),
     "ss_decode_topk": (C.c_int, [P, I64, I64, I64, P, P, P, P]),
     "ss_finish": (C.c_int, [P, P, I64, I32, I32, I32, I32, P, P, P, P, I32, P, P, P, P, P, P, P, P]),
     "ss_refresh": (C.c_int, [I64, P, P, P, I32, P, P, P, I32, P, P, I32, P]),

@@ -266,7 +266,7 @@ __global__ void __launch_bounds__(MF_THREADS)
 k_merge(const uint64_t* __restrict__ comp, const int32_t* __restrict__ len, int nlists,
         int64_t nq, int k, int kpad, uint64_t* __restrict__ out_comp,
         int32_t* __restrict__ out_len, const int32_t* __restrict__ bank_lens, int64_t head,
-        int64_t gcap, int64_t slot_offset) {
+        int64_t gcap, int64_t slot_offset, PeerOut po) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int M = nlists * k;
   uint64_t* cand = reinterpret_cast<uint64_t*>(smem);      // [M]
@@ -279,10 +279,21 @@ k_merge(const uint64_t* __restrict__ comp, const int32_t* __restrict__ len, int 
   load_candidates(comp, len, nlists, nq, k, q, cand, cpay, bank_lens, head, gcap, slot_offset);
   block_select_topk(cand, cpay, M, nlists, k, kpad, sel, spay, hist, s_misc);
   if (!len) resolve_lens(sel, spay, k, bank_lens, head, gcap, slot_offset);
-  for (int i = threadIdx.x; i < k; i += blockDim.x) {
-    out_comp[q * k + i] = sel[i];
-    out_len[q * k + i] = sel[i] ? spay[i] : 0;
+  int64_t row = q;
+  if (po.world > 0) {
+    // fused exchange: query q belongs to rank q / nq_local; its merged row is
+    // stored straight into that rank's receive buffer (NVLink P2P stores
+    // through the IPC-mapped pointer), at [this rank][q % nq_local]
+    const int owner = (int)(q / po.nq_local);
+    row = (int64_t)po.rank * po.nq_local + (q - (int64_t)owner * po.nq_local);
+    out_comp = po.comp[owner];
+    out_len = po.len[owner];
   }
+  for (int i = threadIdx.x; i < k; i += blockDim.x) {
+    out_comp[row * k + i] = sel[i];
+    out_len[row * k + i] = sel[i] ? spay[i] : 0;
+  }
+  if (po.world > 0) __threadfence_system();  // peer stores visible before the barrier
 }
 
 static size_t merge_smem(int nlists, int k, int kpad) {
@@ -291,7 +302,7 @@ static size_t merge_smem(int nlists, int k, int kpad) {
 
 int launch_merge(const uint64_t* comp, const int32_t* len, int nlists, int64_t nq, int k,
                  uint64_t* out_comp, int32_t* out_len, const int32_t* bank_lens, int64_t head,
-                 int64_t gcap, int64_t slot_offset, cudaStream_t st) {
+                 int64_t gcap, int64_t slot_offset, cudaStream_t st, const PeerOut* po) {
   if (nq <= 0) return SS_OK;
   int kpad = 1;
   while (kpad < k) kpad <<= 1;
@@ -301,7 +312,8 @@ int launch_merge(const uint64_t* comp, const int32_t* len, int nlists, int64_t n
   SS_CUDA_TRY(cudaFuncSetAttribute(k_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   count_launch();
   k_merge<<<(unsigned)nq, MF_THREADS, smem, st>>>(comp, len, nlists, nq, k, kpad, out_comp, out_len,
-                                                 bank_lens, head, gcap, slot_offset);
+                                                 bank_lens, head, gcap, slot_offset,
+                                                 po ? *po : PeerOut{});
   SS_LAUNCH_CHECK();
   return SS_OK;
 }

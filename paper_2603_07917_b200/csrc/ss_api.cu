@@ -442,7 +442,7 @@ static size_t topk_ws_need(ss_bank* h, int64_t nq, int32_t k, int32_t algo) {
 
 static int topk_impl(ss_bank* h, const int8_t* q, const float* q_inv, int64_t nq, int32_t k,
                      float theta, int32_t algo, uint64_t* out_comp, int32_t* out_len,
-                     size_t ws_offset, cudaStream_t st) {
+                     size_t ws_offset, cudaStream_t st, const PeerOut* po = nullptr) {
   if (k < 1 || k > 256) return set_error(SS_ERR_ARG, "k must lie in [1, 256], got %d", k);
   if (nq < 0) return set_error(SS_ERR_ARG, "nq < 0");
   if (nq == 0) return SS_OK;
@@ -461,13 +461,69 @@ static int topk_impl(ss_bank* h, const int8_t* q, const float* q_inv, int64_t nq
                                      : launch_topk_scan(a, partials, slices, st);
   if (rc) return rc;
   return launch_merge(partials, nullptr, slices, nq, k, out_comp, out_len, h->lens, h->head,
-                      h->gcap, h->slot_offset, st);
+                      h->gcap, h->slot_offset, st, po);
 }
 
 int ss_topk(ss_bank_t* h, const int8_t* q, const float* q_inv, int64_t nq, int32_t k, float theta,
             int32_t algo, uint64_t* out_comp, int32_t* out_len, void* stream) {
   if (!h || !out_comp || !out_len) return set_error(SS_ERR_ARG, "topk: null args");
   return topk_impl(h, q, q_inv, nq, k, theta, algo, out_comp, out_len, 0, (cudaStream_t)stream);
+}
+
+int ss_topk_scatter(ss_bank_t* h, const int8_t* q, const float* q_inv, int64_t nq, int32_t k,
+                    float theta, int32_t algo, int32_t world, int32_t rank,
+                    uint64_t* const* peer_comp_host, int32_t* const* peer_len_host,
+                    void* stream) {
+  if (!h || !peer_comp_host || !peer_len_host) return set_error(SS_ERR_ARG, "topk_scatter: null args");
+  if (world < 1 || world > SS_MAX_PEERS || rank < 0 || rank >= world || nq % world)
+    return set_error(SS_ERR_ARG, "topk_scatter: bad world/rank/nq (%d, %d, %lld)", world, rank,
+                     (long long)nq);
+  PeerOut po{};
+  po.world = world;
+  po.rank = rank;
+  po.nq_local = nq / world;
+  for (int r = 0; r < world; ++r) {
+    if (!peer_comp_host[r] || !peer_len_host[r])
+      return set_error(SS_ERR_ARG, "topk_scatter: null receive buffer of rank %d", r);
+    po.comp[r] = peer_comp_host[r];
+    po.len[r] = peer_len_host[r];
+  }
+  return topk_impl(h, q, q_inv, nq, k, theta, algo, nullptr, nullptr, 0, (cudaStream_t)stream, &po);
+}
+
+int ss_ipc_malloc(int32_t device, int64_t bytes, void** out) {
+  if (!out || bytes <= 0) return set_error(SS_ERR_ARG, "ipc_malloc: bad args");
+  SS_CUDA_TRY(cudaSetDevice(device));
+  SS_CUDA_TRY(cudaMalloc(out, (size_t)bytes));  // plain cudaMalloc: IPC-exportable
+  SS_CUDA_TRY(cudaMemset(*out, 0, (size_t)bytes));
+  return SS_OK;
+}
+
+int ss_ipc_free(void* ptr) {
+  if (ptr) SS_CUDA_TRY(cudaFree(ptr));
+  return SS_OK;
+}
+
+int ss_ipc_handle(const void* ptr, uint8_t* handle_host) {
+  if (!ptr || !handle_host) return set_error(SS_ERR_ARG, "ipc_handle: null args");
+  static_assert(sizeof(cudaIpcMemHandle_t) == SS_IPC_HANDLE_BYTES, "IPC handle size");
+  cudaIpcMemHandle_t hd;
+  SS_CUDA_TRY(cudaIpcGetMemHandle(&hd, const_cast<void*>(ptr)));
+  memcpy(handle_host, &hd, sizeof(hd));
+  return SS_OK;
+}
+
+int ss_ipc_open(const uint8_t* handle_host, void** out) {
+  if (!handle_host || !out) return set_error(SS_ERR_ARG, "ipc_open: null args");
+  cudaIpcMemHandle_t hd;
+  memcpy(&hd, handle_host, sizeof(hd));
+  SS_CUDA_TRY(cudaIpcOpenMemHandle(out, hd, cudaIpcMemLazyEnablePeerAccess));
+  return SS_OK;
+}
+
+int ss_ipc_close(void* ptr) {
+  if (ptr) SS_CUDA_TRY(cudaIpcCloseMemHandle(ptr));
+  return SS_OK;
 }
 
 int ss_topk_partials(ss_bank_t* h, const int8_t* q, const float* q_inv, int64_t nq, int32_t k,

@@ -100,9 +100,20 @@ int launch_topk_ts(const TopkArgs& a, uint64_t* partials, int n_lists, cudaStrea
 bool topk_pair_supported(const TopkArgs& a);
 int topk_pair_lists(const TopkArgs& a, int device);
 
+// Receive buffers of every rank for the fused merge + exchange (k_merge with
+// po.world > 0): rank r's [world][nq_local][k] rows, IPC-mapped into this process.
+#define SS_MAX_PEERS 8
+struct PeerOut {
+  uint64_t* comp[SS_MAX_PEERS];
+  int32_t* len[SS_MAX_PEERS];
+  int64_t nq_local;
+  int world;  // 0: plain local output
+  int rank;
+};
 int launch_merge(const uint64_t* comp, const int32_t* len, int nlists, int64_t nq, int k,
                  uint64_t* out_comp, int32_t* out_len, const int32_t* bank_lens,
-                 int64_t head, int64_t gcap, int64_t slot_offset, cudaStream_t st);
+                 int64_t head, int64_t gcap, int64_t slot_offset, cudaStream_t st,
+                 const PeerOut* po = nullptr);
 int launch_decode(const uint64_t* comp, int64_t n, int64_t head, int64_t capacity,
                   float* key, int64_t* seq, int64_t* slot, cudaStream_t st);
 int launch_finish(const uint64_t* comp, const int32_t* len, int64_t nq, int k,

@@ -19,6 +19,14 @@ Per round (only stage 1 is partitioned; stages 2-4 run on the queue owner):
   6. histogram -> cost -> Gittins (ss_finish) and rank (ss_rank) for the queue.
 Composites carry the global ring rank (slot - head) mod C, so tie-breaking by
 insertion_seq is identical to the single-GPU round.
+
+With ``exchange="p2p"`` stages 2 and 3 are one kernel sequence: the local
+merge kernel stores every merged row directly into its owner's receive buffer
+(``ss_topk_scatter``; the buffers are cudaMalloc'd, IPC-exported and mapped by
+every rank of the node, so the stores travel over NVLink), and a 1-element
+NCCL all_reduce is the barrier before the owners merge.  The next round's
+query all-gather orders the peers' reads of a receive buffer before it is
+overwritten, so one buffer per queue size suffices.
 """
 
 from __future__ import annotations
@@ -30,7 +38,7 @@ import torch
 import torch.distributed as dist
 
 __all__ = ["ShardPlan", "gather_queries", "exchange_candidates", "allreduce_hist",
-           "ShardedHistory", "ShardedScheduler"]
+           "ShardedHistory", "PeerExchange", "ShardedScheduler"]
 
 
 @dataclass(frozen=True)
@@ -122,6 +130,84 @@ class ShardedHistory:
         self.window.set_head(self.head)
 
 
+class PeerExchange:
+    """Receive buffers of the fused merge + exchange, mapped on every rank.
+
+    Per queue size nq: this rank's buffer comp u64 / len i32 [world, nq, k]
+    (allocated with ``ss_ipc_malloc``) and the device pointers of every rank's
+    buffer as seen from this process (``ss_ipc_open`` of the peers' handles).
+    Collective: every rank must call ``buffers`` with the same nq."""
+
+    def __init__(self, k: int, group=None):
+        self.k, self.group = int(k), group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self._bufs = {}
+        self.flag = None
+
+    def buffers(self, nq: int):
+        import ctypes as C
+
+        from . import _lib
+        from .history import _cuda_view
+
+        b = self._bufs.get(nq)
+        if b is not None:
+            return b
+        if self.flag is None:
+            self.flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+        dev = torch.cuda.current_device()
+        n = self.world * nq * self.k
+        own = [C.c_void_p(), C.c_void_p()]
+        _lib.call("ss_ipc_malloc", dev, n * 8, C.byref(own[0]))
+        _lib.call("ss_ipc_malloc", dev, n * 4, C.byref(own[1]))
+        hs = []
+        for p in own:
+            h = (C.c_uint8 * 64)()
+            _lib.call("ss_ipc_handle", p, h)
+            hs.append(bytes(h))
+        allh = [None] * self.world
+        dist.all_gather_object(allh, hs, group=self.group)
+        comp_t, len_t, opened = (C.c_void_p * self.world)(), (C.c_void_p * self.world)(), []
+        for r in range(self.world):
+            if r == self.rank:
+                comp_t[r], len_t[r] = own[0].value, own[1].value
+                continue
+            for j, tab in enumerate((comp_t, len_t)):
+                p = C.c_void_p()
+                _lib.call("ss_ipc_open", (C.c_uint8 * 64).from_buffer_copy(allh[r][j]), C.byref(p))
+                tab[r] = p.value
+                opened.append(p)
+        recv_c = _cuda_view(own[0].value, torch.int64, (self.world, nq, self.k), dev)
+        recv_l = _cuda_view(own[1].value, torch.int32, (self.world, nq, self.k), dev)
+        b = dict(own=own, opened=opened, comp_t=comp_t, len_t=len_t, recv_c=recv_c, recv_l=recv_l)
+        self._bufs[nq] = b
+        return b
+
+    def scatter_topk(self, window, q_all, qi_all, cfg):
+        """Local top-k of all ranks' queries, each merged row stored into its
+        owner's receive buffer; then the barrier.  -> (comp, len) [world, nq, k]."""
+        from . import _lib
+
+        nq = q_all.shape[0] // self.world
+        b = self.buffers(nq)
+        _lib.call("ss_topk_scatter", window.handle, _lib.ptr(q_all), _lib.ptr(qi_all),
+                  q_all.shape[0], self.k, float(np.float32(cfg.theta)), _lib.ALGO[cfg.algo],
+                  self.world, self.rank, b["comp_t"], b["len_t"], _lib.stream_ptr())
+        dist.all_reduce(self.flag, group=self.group)  # every shard's rows are stored
+        return b["recv_c"], b["recv_l"]
+
+    def close(self):
+        from . import _lib
+
+        for b in self._bufs.values():
+            for p in b["opened"]:
+                _lib.lib().ss_ipc_close(p)
+            for p in b["own"]:
+                _lib.lib().ss_ipc_free(p)
+        self._bufs = {}
+
+
 class ShardedScheduler:
     """The scheduling round of SageScheduler, with stage 1 sharded.
 
@@ -130,12 +216,15 @@ class ShardedScheduler:
     fallback histogram is all-reduced asynchronously while the queries are
     gathered and scored."""
 
-    def __init__(self, history: ShardedHistory, cfg):
+    def __init__(self, history: ShardedHistory, cfg, exchange: str = "nccl"):
+        if exchange not in ("nccl", "p2p"):
+            raise ValueError(f"exchange must be 'nccl' or 'p2p', got {exchange!r}")
         self.h = history
         self.cfg = cfg
         self.group = history.group
         self._bufs = {}
         self._side = None
+        self.peer = PeerExchange(cfg.k, self.group) if exchange == "p2p" else None
 
     def _buffers(self, nq: int):
         b = self._bufs.get(nq)
@@ -170,8 +259,11 @@ class ShardedScheduler:
             fb = self.h.window.fallback_hist(c.max_len, c.nbins, stream=self._side)
             fb_work = dist.all_reduce(fb, op=dist.ReduceOp.SUM, group=self.group, async_op=True)
         q_all, qi_all = gather_queries(q, q_inv, self.group)                    # 1
-        comp_all, len_all = self.h.window.topk(q_all, qi_all, c.k, c.theta, c.algo)  # 2
-        comp_x, len_x = exchange_candidates(comp_all, len_all, self.group)      # 3
+        if self.peer is not None:                                               # 2+3 fused
+            comp_x, len_x = self.peer.scatter_topk(self.h.window, q_all, qi_all, c)
+        else:
+            comp_all, len_all = self.h.window.topk(q_all, qi_all, c.k, c.theta, c.algo)  # 2
+            comp_x, len_x = exchange_candidates(comp_all, len_all, self.group)  # 3
         world = comp_x.shape[0]
         comp, ln = out["comp"], out["len"]
         _lib.call("ss_merge_topk", _lib.ptr(comp_x), _lib.ptr(len_x), world, nq, c.k,

@@ -558,10 +558,11 @@ def test_rank_special_values(cuda):
 
 
 # ---------------------------------------------------- sharded round (N=1) ---
-def test_sharded_round_world1_equals_single_gpu(cuda):
-    """The multi-GPU round (query all-gather, candidate all-to-all, merge,
-    histogram all-reduce) run as a 1-rank NCCL group equals the fused
-    single-GPU round bit for bit."""
+@pytest.mark.parametrize("exchange", ["nccl", "p2p"])
+def test_sharded_round_world1_equals_single_gpu(cuda, exchange):
+    """The multi-GPU round (query all-gather, candidate all-to-all or the fused
+    P2P merge + exchange, merge, histogram all-reduce) run as a 1-rank NCCL
+    group equals the fused single-GPU round bit for bit."""
     import socket
 
     import torch.distributed as dist
@@ -582,12 +583,97 @@ def test_sharded_round_world1_equals_single_gpu(cuda):
         q, qi = emb[n:], O.inv_norm(emb[n:])
         I = np.random.default_rng(0).integers(1, 4097, nq).astype(np.int32)
         ids = np.arange(nq)
-        p1, G1, _ = ShardedScheduler(sh, cfg).schedule_round(_t(q), _t(qi), _t(I), _t(ids))
+        ss = ShardedScheduler(sh, cfg, exchange=exchange)
+        p1, G1, _ = ss.schedule_round(_t(q), _t(qi), _t(I), _t(ids))
+        if ss.peer is not None:
+            p1, G1 = p1.clone(), G1.clone()
+            p1b, G1b, _ = ss.schedule_round(_t(q), _t(qi), _t(I), _t(ids))  # buffers reused
+            assert torch.equal(G1b, G1) and torch.equal(p1b, p1)
+            ss.peer.close()
         w, *_ = _bank(n, dim, 50, 9, nq)
         p0, G0, _ = SageScheduler(w, cfg).schedule_round(_t(q), _t(qi), _t(I), _t(ids))
         assert torch.equal(G1, G0) and torch.equal(p1, p0)
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_topk_scatter_shards_equal_single_bank(cuda, world):
+    """ss_topk_scatter addressing, all ranks simulated in one process: shard r
+    stores the merged rows of every rank's queries into that rank's receive
+    buffer at [r][q]; merging a receive buffer gives the single-bank top-k of
+    the owner's queries (lengths included), bit for bit."""
+    import ctypes as C
+
+    from paper_2603_07917_b200 import _lib
+    from paper_2603_07917_b200.history import HistoryWindow
+    from paper_2603_07917_b200.sharded import ShardPlan
+    n, dim, nq, k = 6_000, 384, 70, 16
+    emb, lens, _, _ = O.make_bank(n + world * nq, dim, 40, 5)
+    q = _t(emb[n:])
+    qi = _t(O.inv_norm(emb[n:]))
+    wins = []
+    for r in range(world):
+        plan = ShardPlan(n, world, r)
+        w = HistoryWindow(plan.local_capacity, dim, global_capacity=n, slot_offset=plan.slot_offset)
+        idx, seq, slot = plan.route(0, n)
+        w.write(_t(emb[idx]), _t(lens[idx]), _t(seq), _t(slot))
+        w.set_head(n)
+        wins.append(w)
+    recv_c = [torch.full((world, nq, k), -7, dtype=torch.int64, device="cuda") for _ in range(world)]
+    recv_l = [torch.full((world, nq, k), -7, dtype=torch.int32, device="cuda") for _ in range(world)]
+    tc = (C.c_void_p * world)(*[t.data_ptr() for t in recv_c])
+    tl = (C.c_void_p * world)(*[t.data_ptr() for t in recv_l])
+    for r, w in enumerate(wins):
+        _lib.call("ss_topk_scatter", w.handle, _lib.ptr(q), _lib.ptr(qi), world * nq, k, 0.5,
+                  _lib.ALGO["auto"], world, r, tc, tl, _lib.stream_ptr())
+    full, *_ = _bank(n, dim, 40, 5, world * nq)
+    c0, l0 = full.topk(q, qi, k, 0.5)
+    for r in range(world):
+        out_c = torch.empty((nq, k), dtype=torch.int64, device="cuda")
+        out_l = torch.empty((nq, k), dtype=torch.int32, device="cuda")
+        _lib.call("ss_merge_topk", _lib.ptr(recv_c[r]), _lib.ptr(recv_l[r]), world, nq, k,
+                  _lib.ptr(out_c), _lib.ptr(out_l), _lib.stream_ptr())
+        assert torch.equal(out_c, c0[r * nq:(r + 1) * nq])
+        assert torch.equal(out_l, l0[r * nq:(r + 1) * nq])
+    with pytest.raises(ValueError):
+        _lib.call("ss_topk_scatter", wins[0].handle, _lib.ptr(q), _lib.ptr(qi), world * nq - 1, k,
+                  0.5, 0, world, 0, tc, tl, _lib.stream_ptr())
+
+
+def test_ipc_buffer_cross_process(cuda, tmp_path):
+    """ss_ipc_malloc/handle in this process, ss_ipc_open + stores in another
+    (the mapping the P2P exchange uses between ranks of a node)."""
+    import ctypes as C
+    import subprocess
+    import sys
+
+    from paper_2603_07917_b200 import _lib
+    from paper_2603_07917_b200.history import _cuda_view
+    p = C.c_void_p()
+    _lib.call("ss_ipc_malloc", 0, 4096 * 8, C.byref(p))
+    try:
+        h = (C.c_uint8 * 64)()
+        _lib.call("ss_ipc_handle", p, h)
+        child = (
+            "import ctypes as C, torch\n"
+            "from paper_2603_07917_b200 import _lib\n"
+            "from paper_2603_07917_b200.history import _cuda_view\n"
+            "torch.cuda.init()\n"
+            f"h = (C.c_uint8 * 64).from_buffer_copy(bytes.fromhex('{bytes(h).hex()}'))\n"
+            "p = C.c_void_p()\n"
+            "_lib.call('ss_ipc_open', h, C.byref(p))\n"
+            "t = _cuda_view(p.value, torch.int64, (4096,), 0)\n"
+            "t.copy_(torch.arange(4096, device='cuda') * 3 + 1)\n"
+            "torch.cuda.synchronize()\n"
+            "_lib.call('ss_ipc_close', p)\n")
+        r = subprocess.run([sys.executable, "-c", child], cwd=str(__import__("pathlib").Path(__file__).resolve().parents[1]), capture_output=True,
+                           text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        got = _cuda_view(p.value, torch.int64, (4096,), 0).cpu()
+        assert torch.equal(got, torch.arange(4096) * 3 + 1)
+    finally:
+        _lib.call("ss_ipc_free", p)
 
 
 # ------------------------------------------- batch formation (SPEC.md:470) --
