@@ -1,0 +1,61 @@
+"""Worker of test_gpu_parity.test_sharded_p2p_two_ranks_one_gpu (not a test module).
+
+Two ranks share cuda:0 (gloo carries the control collectives: NCCL refuses two
+ranks on one device).  Each rank holds half of the ring and its own queue; the
+round uses the fused P2P merge + exchange, whose stores cross the process
+boundary through the IPC mapping.  Every rank checks its queue's Gittins
+indices and order against the single-GPU round over the whole bank.
+"""
+
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+from oracle import sagesched_oracle as O  # noqa: E402
+from paper_2603_07917_b200.history import HistoryWindow  # noqa: E402
+from paper_2603_07917_b200.scheduler import RoundConfig, SageScheduler  # noqa: E402
+from paper_2603_07917_b200.sharded import ShardedHistory, ShardedScheduler  # noqa: E402
+
+
+def main():
+    dist.init_process_group("gloo")
+    rank, world = dist.get_rank(), dist.get_world_size()
+    torch.cuda.set_device(0)
+    n, dim, nq = 12_000, 384, 96
+    emb, lens, _, _ = O.make_bank(n + world * nq, dim, 40, 3)
+    cfg = RoundConfig(k=32, theta=0.7, nbins=64)
+    sh = ShardedHistory(n, dim)
+    sh.push(torch.as_tensor(emb[:n], device="cuda"), torch.as_tensor(lens[:n], device="cuda"))
+    lo = n + rank * nq
+    q = torch.as_tensor(emb[lo:lo + nq], device="cuda")
+    qi = torch.as_tensor(O.inv_norm(emb[lo:lo + nq]), device="cuda")
+    I = torch.as_tensor(np.random.default_rng(rank).integers(1, 4097, nq).astype(np.int32),
+                        device="cuda")
+    ids = torch.arange(rank * nq, (rank + 1) * nq, device="cuda")
+    ss = ShardedScheduler(sh, cfg, exchange="p2p")
+    for _ in range(3):  # receive buffers reused across rounds
+        p1, G1, _ = ss.schedule_round(q, qi, I, ids)
+        torch.cuda.synchronize()
+        dist.barrier()
+    # the peer's shard really delivered rows into this rank's receive buffer
+    recv = ss.peer.buffers(nq)["recv_c"]
+    delivered = bool(recv[1 - rank].ne(0).any()) and bool(recv[rank].ne(0).any())
+    w = HistoryWindow(n, dim)
+    w.push(emb[:n], lens[:n])
+    p0, G0, _ = SageScheduler(w, cfg).schedule_round(q, qi, I, ids)
+    ok = delivered and torch.equal(G1, G0) and torch.equal(p1, p0)
+    ss.peer.close()
+    dist.barrier()
+    dist.destroy_process_group()
+    if not ok:
+        print(f"rank {rank}: sharded P2P round differs from the single-GPU round", file=sys.stderr)
+        sys.exit(1)
+
+
+if __name__ == "__main__":
+    main()

@@ -641,6 +641,24 @@ def test_topk_scatter_shards_equal_single_bank(cuda, world):
                   0.5, 0, world, 0, tc, tl, _lib.stream_ptr())
 
 
+def test_sharded_p2p_two_ranks_one_gpu(cuda):
+    """World-2 round with the fused P2P merge + exchange, both ranks on cuda:0
+    (tests/_p2p_worker.py): each rank's result equals the single-GPU round."""
+    import pathlib
+    import socket
+    import subprocess
+    import sys
+    root = pathlib.Path(__file__).resolve().parents[1]
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        "--nproc-per-node=2", "--master-addr=127.0.0.1", f"--master-port={port}",
+                        str(root / "tests" / "_p2p_worker.py")], cwd=str(root),
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, (r.stdout[-2000:], r.stderr[-4000:])
+
+
 def test_ipc_buffer_cross_process(cuda, tmp_path):
     """ss_ipc_malloc/handle in this process, ss_ipc_open + stores in another
     (the mapping the P2P exchange uses between ranks of a node)."""
