@@ -20,6 +20,7 @@
 #include <cudaTypedefs.h>
 #include <stdlib.h>
 
+#include <algorithm>
 #include <type_traits>
 
 #include "ss_common.cuh"
@@ -62,6 +63,25 @@ __device__ __forceinline__ void tma2d(void* dst, const CUtensorMap* m, uint64_t*
       "l"(m), "r"(su32(b)), "r"(c0), "r"(c1)
       : "memory");
 }
+// the same box, multicast into the same smem offset of every CTA in `mask`
+// (each destination CTA's barrier at `b`'s offset receives the byte count)
+__device__ __forceinline__ void tma2d_mc(void* dst, const CUtensorMap* m, uint64_t* b, int c0, int c1,
+                                         uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%3, %4}], [%2], %5;\n" ::"r"(su32(dst)),
+      "l"(m), "r"(su32(b)), "r"(c0), "r"(c1), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::
+                   : "memory");
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
@@ -74,6 +94,14 @@ __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::aft
 __device__ __forceinline__ void commit(uint64_t* b) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(su32(b))
                : "memory");
+}
+// arrive on the barrier at `b`'s offset in every CTA of `mask` when this
+// thread's MMAs complete
+__device__ __forceinline__ void commit_mc(uint64_t* b, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;\n" ::"r"(su32(b)), "h"(mask)
+      : "memory");
 }
 // D[tmem] (+)= A[tmem] x B[smem]^T
 __device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
@@ -185,9 +213,10 @@ __device__ __noinline__ uint64_t heap_replace(uint64_t* heap, int k, uint64_t x)
 // BN bank rows per tile (UMMA N), NACC accumulators of BN columns in TMEM
 // (NACC = 2 lets the MMA of tile t+1 run while tile t is drained), A in
 // columns [NACC * BN, NACC * BN + dim / 4).
-// ASPLIT: the last K-block of A lives in shared memory (TMA) instead of
+// ASPLIT = 1: the last K-block of A lives in shared memory (TMA) instead of
 // TMEM, which frees 32 TMEM columns: two N=224 accumulators + 64 A columns
-// fill the 512 columns exactly.
+// fill the 512 columns exactly.  ASPLIT = 2: all of A in shared memory
+// (SS-form MMA), so two N=256 accumulators fill TMEM.
 // The slow path of the pure-top-k (SHARE) filter, out of line: many chunks
 // pass there, and one copy of this code (instead of one per inlined chunk)
 // measured faster (1.29 vs 1.45 ms at c2, theta = -1); with a similarity
@@ -255,14 +284,14 @@ __device__ __noinline__ float insert_locked(uint32_t mask, const float* sl, floa
 // slice has published, the union of their top-R holds >= k rows at or above
 // that minimum, so it bounds the global k-th key from below.  Slots that are
 // still 0 make the minimum 0 (no bound).
-template <int BN, int NACC, bool ASPLIT, bool SHARE = false>
+template <int BN, int NACC, int ASPLIT, bool SHARE = false>
 __global__ void __launch_bounds__(THREADS, 1)
 k_topk_ts(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmQ,
           const int8_t* __restrict__ Q,
           const float* __restrict__ q_inv, int64_t nq, const float* __restrict__ inv, int64_t n_rows,
           int dim, int stages, int k, float theta, int64_t hmod, int64_t gcap, int64_t slot_offset,
           int64_t tiles_per_slice, uint64_t* __restrict__ partials, int dbg,
-          uint32_t* __restrict__ gslots = nullptr, int rshare = 0) {
+          uint32_t* __restrict__ gslots = nullptr, int rshare = 0, int mc = 0) {
   constexpr int A_COL = NACC * BN;
   constexpr int B_STAGE = BN * BK;
   constexpr int HALF = BN / 2;     // columns per epilogue warp per tile
@@ -270,13 +299,16 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUten
   constexpr int TAIL = HALF % 32;  // + one 8- or 16-column chunk (BN = 208 / 224)
   static_assert((CPW == 3 || CPW == 4) && (TAIL == 0 || ((TAIL == 8 || TAIL == 16) && CPW == 3)),
                 "tile shape");
-  static_assert(A_COL + (ASPLIT ? 64 : 96) <= 512, "TMEM columns (dim 384 beside the accumulators)");
+  constexpr bool A_ALL = ASPLIT == 2, A_LAST = ASPLIT == 1;
+  static_assert(A_ALL || A_COL + (A_LAST ? 64 : 96) <= 512,
+                "TMEM columns (dim 384 beside the accumulators)");
   constexpr uint32_t IDESC = idesc(BN);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sB = smem;                                                    // stages x 32 KB
   uint8_t* sA = sB + stages * B_STAGE;  // ASPLIT: the last K-block of A (16 KB, 1024-aligned)
-  uint64_t* s_heap = reinterpret_cast<uint64_t*>(sA + (ASPLIT ? BM * BK : 0));  // [k][128]
+  uint64_t* s_heap =
+      reinterpret_cast<uint64_t*>(sA + (A_ALL ? BM * dim : A_LAST ? BM * BK : 0));  // [k][128]
   uint64_t* s_hroot = s_heap + (size_t)k * BM;                           // [128]
   int* s_hcnt = reinterpret_cast<int*>(s_hroot + BM);                    // [128]
   int* s_hlock = s_hcnt + BM;                                            // [128]
@@ -304,8 +336,10 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUten
 
   if (threadIdx.x == 0) {
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmB) : "memory");
-    bar_init(a_full, ASPLIT ? 5 : 4);  // 4 TMEM-writer warps (+ the TMA of the smem K-block)
-    for (int s = 0; s < stages; ++s) { bar_init(&full[s], 1); bar_init(&empty[s], 1); }
+    // 4 TMEM-writer warps (+ the TMA of the smem K-block); A_ALL: the TMA alone
+    bar_init(a_full, A_ALL ? 1 : A_LAST ? 5 : 4);
+    // mc: a slot is refilled (for both CTAs of the pair) once both MMAs freed it
+    for (int s = 0; s < stages; ++s) { bar_init(&full[s], 1); bar_init(&empty[s], mc ? 2 : 1); }
     for (int b = 0; b < NACC; ++b) { bar_init(&tfull[b], 1); bar_init(&tempty[b], EPI_WARPS); }
     for (int b = 0; b < ISLOTS; ++b) { bar_init(&ifull[b], 1); bar_init(&iempty[b], EPI_WARPS); }
     bar_init(mdone, 1);
@@ -320,15 +354,20 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUten
   }
   fence_before();
   __syncthreads();
+  if (mc) cluster_sync();  // the peer's barriers are initialised before any multicast
   fence_after();
   const uint32_t tmem = *s_tmem;
 
   if (warp == 0) {
     // ------------------------------------------------------ TMA producer ---
     if (lane == 0 && ntiles > 0) {
-      if constexpr (ASPLIT) {
+      if constexpr (A_LAST) {
         bar_expect(a_full, BM * BK);
         tma2d(sA, &tmQ, a_full, (nkb - 1) * BK, qt * BM);
+      }
+      if constexpr (A_ALL) {
+        bar_expect(a_full, BM * dim);
+        for (int kb = 0; kb < nkb; ++kb) tma2d(sA + kb * BM * BK, &tmQ, a_full, kb * BK, qt * BM);
       }
       int it = 0;
       for (int t = 0; t < ntiles; ++t) {
@@ -350,7 +389,16 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUten
             continue;
           }
           bar_expect(&full[s], B_STAGE);
-          tma2d(sB + s * B_STAGE, &tmB, &full[s], kb * BK, row0);
+          if (mc) {
+            // cluster pair = two query tiles of one slice: each CTA fetches half
+            // of the bank tile's rows and multicasts it into both CTAs' slot,
+            // halving the L2 -> SM traffic of the tile
+            const uint32_t cr = cluster_rank();
+            tma2d_mc(sB + s * B_STAGE + cr * (B_STAGE / 2), &tmB, &full[s], kb * BK,
+                     row0 + (int)cr * (BN / 2), (uint16_t)3);
+          } else {
+            tma2d(sB + s * B_STAGE, &tmB, &full[s], kb * BK, row0);
+          }
         }
       }
       for (int i = max(0, it - stages); i < it; ++i) bar_wait(&empty[i % stages], (i / stages) & 1);
@@ -372,11 +420,11 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUten
           const int s = it % stages;
           bar_wait(&full[s], (it / stages) & 1);
           fence_after();
-          if (ASPLIT && kb == nkb - 1) {
+          if (A_ALL || (A_LAST && kb == nkb - 1)) {
 #pragma unroll
             for (int kk = 0; kk < BK / UK; ++kk)
               if (!(dbg & 2))
-                mma_ss(dacc, desc_sw128(su32(sA) + kk * UK),
+                mma_ss(dacc, desc_sw128(su32(sA) + (A_ALL ? kb * BM * BK : 0) + kk * UK),
                        desc_sw128(b_base + s * B_STAGE + kk * UK), IDESC, (kb | kk) != 0);
           } else {
 #pragma unroll
@@ -385,7 +433,10 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUten
                 mma_ts(dacc, tmem + A_COL + (kb * (BK / UK) + kk) * (UK / 4),
                        desc_sw128(b_base + s * B_STAGE + kk * UK), IDESC, (kb | kk) != 0);
           }
-          commit(&empty[s]);
+          if (mc)
+            commit_mc(&empty[s], (uint16_t)3);
+          else
+            commit(&empty[s]);
         }
         commit(&tfull[acc]);
       }
@@ -403,8 +454,8 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUten
     const int64_t q = (int64_t)qt * BM + qrow;
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
     // group 0 writes this query's int8 vector into TMEM (A operand)
-    if (grp == 0) {
-      const int ncol = (ASPLIT ? dim - BK : dim) / 4;
+    if (grp == 0 && !A_ALL) {
+      const int ncol = (A_LAST ? dim - BK : dim) / 4;
       for (int c0 = 0; c0 < ncol; c0 += 32) {
         uint32_t v[32];
         const uint4* src = reinterpret_cast<const uint4*>(Q + q * dim) + c0 / 4;
@@ -631,6 +682,7 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUten
   }
   fence_before();
   __syncthreads();
+  if (mc) cluster_sync();  // no multicast / remote arrive targets an exited CTA
   if (warp == 1) {
     fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
@@ -660,41 +712,105 @@ static size_t ts_fixed_smem(int k) {
 // TMEM (default: the widest double buffer that fits beside A), 224 x 2 with
 // the last K-block of A in shared memory (SS_TC_TSN=224; the SS-form MMA of
 // that K-block ran slower, 0.303 vs 0.297 ms MMA-only, 0.378 vs 0.373 ms end
-// to end), 192 x 2, or 256 x 1.
+// to end), 192 x 2, 256 x 1, or (code 512) 256 x 2 with all of A in shared
+// memory (SS-form MMA, SS_TC_TSN=512).
 static int ts_bn(const TopkArgs& a) {
   static const int v = getenv("SS_TC_TSN") ? atoi(getenv("SS_TC_TSN")) : 208;
-  const int want = (v == 256 || v == 192 || v == 224) ? v : 208;
+  const int want = (v == 256 || v == 192 || v == 224 || v == 512) ? v : 208;
+  if (want == 512) return 512;
   if (want == 224 && a.dim / 4 - 32 + 2 * 224 <= 512) return 224;
   if (want >= 208 && want != 256 && a.dim / 4 + 2 * 208 <= 512) return 208;
   if (want == 256) return 256;
   return 192;
 }
-static size_t ts_smem_extra(int bn) { return bn == 224 ? (size_t)ts::BM * ts::BK : 0; }
-static int ts_stages(int k, int bn) {
+static int ts_rows(int code) { return code == 512 ? 256 : code; }
+static size_t ts_smem_extra(int code, int dim) {
+  return code == 224 ? (size_t)ts::BM * ts::BK : code == 512 ? (size_t)ts::BM * dim : 0;
+}
+static int ts_stages(int k, int code, int dim) {
   for (int s = 8; s >= 3; --s)
-    if (ts_fixed_smem(k) + ts_smem_extra(bn) + (size_t)s * bn * ts::BK <= 227 * 1024) return s;
+    if (ts_fixed_smem(k) + ts_smem_extra(code, dim) + (size_t)s * ts_rows(code) * ts::BK <=
+        227 * 1024)
+      return s;
   return 0;
 }
 
 bool topk_ts_supported(const TopkArgs& a) {
   const int bn = ts_bn(a);
-  const int acols = bn == 256 ? 256 : 2 * bn;
-  const int a_tmem = bn == 224 ? a.dim / 4 - 32 : a.dim / 4;
+  const int acols = bn == 256 ? 256 : bn == 512 ? 512 : 2 * bn;
+  const int a_tmem = bn == 224 ? a.dim / 4 - 32 : bn == 512 ? 0 : a.dim / 4;
   if (a.dim % ts::BK || a.dim % 128 || a_tmem + acols > 512 || a.k < 1 || a.k > ts::KMAX)
     return false;
   if (a.n_rows >= (1LL << 31) || a.nq >= (1LL << 31)) return false;
   if (!a.inv_padded) return false;  // tiles of inverse norms are bulk-copied whole
-  return ts_stages(a.k, ts_bn(a)) >= 3;
+  return ts_stages(a.k, bn, a.dim) >= 3;
+}
+
+// Cluster pairs along the query-tile axis sharing each bank tile by TMA
+// multicast (SS_TC_MC=1): needs an even number of query tiles.
+static bool ts_mc(const TopkArgs& a) {
+  static const int v = getenv("SS_TC_MC") ? atoi(getenv("SS_TC_MC")) : 0;
+  const int64_t qtiles = (a.nq + ts::BM - 1) / ts::BM;
+  return v == 1 && qtiles >= 2 && qtiles % 2 == 0;
+}
+
+template <int BN, int NACC, int ASPLIT>
+static constexpr int ts_code() { return ASPLIT == 2 ? 512 : BN; }
+
+template <int BN, int NACC, int ASPLIT>
+static size_t ts_smem_bytes(const TopkArgs& a, bool share) {
+  constexpr int code = ts_code<BN, NACC, ASPLIT>();
+  return ts_fixed_smem(a.k) + ts_smem_extra(code, a.dim) +
+         (size_t)ts_stages(a.k, code, a.dim) * BN * ts::BK + (share ? ts::BM * 16 : 0);
+}
+
+// SMs usable by 2-CTA clusters of this kernel (GPCs may leave SMs unpaired)
+template <int BN, int NACC, int ASPLIT>
+static int ts_mc_sms(const TopkArgs& a, int sms) {
+  static int cached = -1;
+  if (cached < 0) {
+    auto kern = ts::k_topk_ts<BN, NACC, ASPLIT, false>;
+    const size_t smem = ts_smem_bytes<BN, NACC, ASPLIT>(a, false);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2, (unsigned)sms);
+    cfg.blockDim = dim3(ts::THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n < 1) {
+      cudaGetLastError();
+      n = sms / 2;
+    }
+    cached = std::min(sms, 2 * n);
+  }
+  return cached;
 }
 
 // one partial list per CTA slice
 int topk_ts_lists(const TopkArgs& a, int device) {
   const int64_t qtiles = (a.nq + ts::BM - 1) / ts::BM;
-  const int64_t tiles = (a.n_rows + ts_bn(a) - 1) / ts_bn(a);
-  return pick_slices(qtiles, tiles, sm_count(device));
+  const int64_t tiles = (a.n_rows + ts_rows(ts_bn(a)) - 1) / ts_rows(ts_bn(a));
+  int sms = sm_count(device);
+  if (ts_mc(a)) {
+    switch (ts_bn(a)) {
+      case 512: sms = ts_mc_sms<256, 2, 2>(a, sms); break;
+      case 256: sms = ts_mc_sms<256, 1, false>(a, sms); break;
+      case 192: sms = ts_mc_sms<192, 2, false>(a, sms); break;
+      case 208: sms = ts_mc_sms<208, 2, false>(a, sms); break;
+      default: sms = ts_mc_sms<224, 2, true>(a, sms); break;
+    }
+  }
+  return pick_slices(qtiles, tiles, sms);
 }
 
-template <int BN, int NACC, bool ASPLIT>
+template <int BN, int NACC, int ASPLIT>
 static int launch_ts_t(const TopkArgs& a, uint64_t* partials, int n_slices, cudaStream_t st) {
   // pure top-k: share per-slice bounds (see k_topk_ts SHARE)
   int rshare = 0;
@@ -707,7 +823,8 @@ static int launch_ts_t(const TopkArgs& a, uint64_t* partials, int n_slices, cuda
   CUtensorMap mb;
   cuuint64_t gdim[2] = {(cuuint64_t)a.dim, (cuuint64_t)a.n_rows};
   cuuint64_t gstride[1] = {(cuuint64_t)a.dim};
-  cuuint32_t box[2] = {(cuuint32_t)ts::BK, (cuuint32_t)BN};
+  const bool mc = ts_mc(a);
+  cuuint32_t box[2] = {(cuuint32_t)ts::BK, (cuuint32_t)(mc ? BN / 2 : BN)};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(&mb, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(a.emb), gdim, gstride,
                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -722,8 +839,9 @@ static int launch_ts_t(const TopkArgs& a, uint64_t* partials, int n_slices, cuda
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return set_error(SS_ERR_CUDA, "cuTensorMapEncodeTiled (q) failed (%d)", (int)r);
   }
-  const int stages = ts_stages(a.k, BN);
-  const size_t smem = ts_fixed_smem(a.k) + ts_smem_extra(BN) + (size_t)stages * BN * ts::BK +
+  const int stages = ts_stages(a.k, ts_code<BN, NACC, ASPLIT>(), a.dim);
+  const size_t smem = ts_fixed_smem(a.k) + ts_smem_extra(ts_code<BN, NACC, ASPLIT>(), a.dim) +
+                      (size_t)stages * BN * ts::BK +
                       (rshare ? ts::BM * 16 : 0);
   auto kern = rshare ? ts::k_topk_ts<BN, NACC, ASPLIT, true> : ts::k_topk_ts<BN, NACC, ASPLIT, false>;
   SS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -734,9 +852,27 @@ static int launch_ts_t(const TopkArgs& a, uint64_t* partials, int n_slices, cuda
   dim3 grid((unsigned)((a.nq + ts::BM - 1) / ts::BM), (unsigned)n_slices);
   const char* dv = getenv("SS_TC_DEBUG");
   count_launch();
-  kern<<<grid, ts::THREADS, smem, st>>>(
-      mb, mq, a.q, a.q_inv, a.nq, a.inv, a.n_rows, a.dim, stages, a.k, a.theta, a.head % a.gcap, a.gcap,
-      a.slot_offset, tps, partials, dv ? atoi(dv) : 0, a.gslots, rshare);
+  if (mc) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(ts::THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    SS_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, mb, mq, a.q, a.q_inv, a.nq, a.inv, a.n_rows, a.dim,
+                                   stages, a.k, a.theta, a.head % a.gcap, a.gcap, a.slot_offset,
+                                   tps, partials, dv ? atoi(dv) : 0, a.gslots, rshare, 1));
+  } else {
+    kern<<<grid, ts::THREADS, smem, st>>>(
+        mb, mq, a.q, a.q_inv, a.nq, a.inv, a.n_rows, a.dim, stages, a.k, a.theta, a.head % a.gcap,
+        a.gcap, a.slot_offset, tps, partials, dv ? atoi(dv) : 0, a.gslots, rshare, 0);
+  }
   SS_LAUNCH_CHECK();
   return SS_OK;
 }
@@ -744,6 +880,7 @@ static int launch_ts_t(const TopkArgs& a, uint64_t* partials, int n_slices, cuda
 int launch_topk_ts(const TopkArgs& a, uint64_t* partials, int n_lists, cudaStream_t st) {
   if (n_lists < 1) return set_error(SS_ERR_ARG, "ts: no slices");
   switch (ts_bn(a)) {
+    case 512: return launch_ts_t<256, 2, 2>(a, partials, n_lists, st);
     case 256: return launch_ts_t<256, 1, false>(a, partials, n_lists, st);
     case 192: return launch_ts_t<192, 2, false>(a, partials, n_lists, st);
     case 208: return launch_ts_t<208, 2, false>(a, partials, n_lists, st);
