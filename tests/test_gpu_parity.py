@@ -276,6 +276,37 @@ def test_round_c1_bit_exact(cuda, algo, nbins, theta):
     assert np.array_equal(Gh, Gr) and np.array_equal(ph, O.rank(Gr, ids))
 
 
+@pytest.mark.parametrize("theta", [0.8, -1.0])
+def test_round_c2_full_size_sampled(cuda, theta):
+    """BASELINE configs[1] at full size (1M-row bank, 1024 requests, k = 64,
+    128 bins, the bench's synthetic data; theta = -1 is the pure top-k kernel
+    with cross-slice bound sharing): Gittins indices of 32 sampled
+    requests equal the oracle's bit for bit (the oracle scores those requests
+    against the whole bank), and the permutation orders every request by
+    (G, id)."""
+    from paper_2603_07917_b200.history import HistoryWindow
+    from paper_2603_07917_b200.scheduler import RoundConfig, SageScheduler
+    from paper_2603_07917_b200.synthetic import make_bank_device, make_queries
+    n, dim, nq, k, nbins = 1 << 20, 384, 1024, 64, 128
+    emb, lens, _ = make_bank_device(n, dim, 4096, 0)
+    w = HistoryWindow(n, dim)
+    w.push(emb, lens)
+    q, qi, I, ids = make_queries(nq, dim, 4096, 0, qseed=1000)
+    cfg = RoundConfig(k=k, theta=theta, min_matches=20, max_len=2048, nbins=nbins)
+    perm, G, _ = SageScheduler(w, cfg).schedule_round(_t(q), _t(qi), _t(I), _t(ids))
+    G, perm = G.cpu().numpy(), perm.cpu().numpy()
+    assert np.array_equal(perm, O.rank(G, ids))
+    be, bl = emb.cpu().numpy(), lens.cpu().numpy()
+    del emb, lens
+    binv = O.inv_norm(be)
+    smp = np.random.default_rng(3).choice(nq, 32, replace=False)
+    keys = np.concatenate([O.scores(q[smp], qi[smp], be[s:s + (1 << 18)], binv[s:s + (1 << 18)])
+                           for s in range(0, n, 1 << 18)], axis=1)
+    ref = O.predict_round(keys, np.arange(n), bl, I[smp], k, theta, 20, 2048, nbins, window_lens=bl)
+    assert np.array_equal(G[smp], np.array([r["G"] for r in ref]))
+    assert sum(not r["used_fallback"] for r in ref) >= 16  # the top-k path, not only the fallback
+
+
 def test_round_host_graph_replay(cuda):
     """The plugin call with pinned host buffers: calls 1-2 run eagerly, the
     repeat is captured and later calls replay one graph (H2D + round + D2H).
