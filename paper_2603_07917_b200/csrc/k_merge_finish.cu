@@ -682,19 +682,20 @@ k_merge_finish_w(const uint64_t* __restrict__ partials, int nlists, int64_t nq, 
   // of the global k-th best; candidates below it are dropped afterwards.
   int m1 = 0;
   uint64_t tau = 1ull;
-  if ((k & 31) == 0) {  // k multiple of 32: 8 lists' loads in flight per batch
+  if ((k & 31) == 0) {  // k multiple of 32: LB lists' loads in flight per batch
+    constexpr int LB = 24;
     const int per = k >> 5;
     const uint64_t* src0 = partials + q * k + lane;
     const int64_t lstride = nq * (int64_t)k;
-    for (int l0 = 0; l0 < nlists; l0 += 8) {
-      const int nl = min(8, nlists - l0);
-      uint64_t root[8];  // entry 0 of each list of the batch
+    for (int l0 = 0; l0 < nlists; l0 += LB) {
+      const int nl = min(LB, nlists - l0);
+      uint64_t root[LB];  // entry 0 of each list of the batch
       for (int jj = 0; jj < per; ++jj) {
-        uint64_t v[8];
+        uint64_t v[LB];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = (u < nl) ? __ldcs(src0 + (l0 + u) * lstride + jj * 32) : 0ull;
+        for (int u = 0; u < LB; ++u) v[u] = (u < nl) ? __ldcs(src0 + (l0 + u) * lstride + jj * 32) : 0ull;
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < LB; ++u) {
           const unsigned b = __ballot_sync(0xffffffffu, v[u] != 0ull);
           if (v[u] != 0ull) cand[m1 + __popc(b & lt)] = v[u];
           m1 += __popc(b);
