@@ -176,6 +176,7 @@ k_os_init(const double* __restrict__ G, const int64_t* __restrict__ ids, int64_t
 __global__ void __launch_bounds__(256)
 k_os_scan(uint32_t* __restrict__ ghist, int64_t n, const uint32_t* __restrict__ unsorted,
           OsMeta* __restrict__ meta) {
+  pdl_wait();  // k_os_init's histograms
   __shared__ uint32_t s_warp[OS_PASSES][8];
   __shared__ int s_triv[OS_PASSES];
   const int d = threadIdx.x, lane = d & 31, warp = d >> 5;
@@ -224,6 +225,11 @@ k_os_pass(uint64_t* __restrict__ key0, uint64_t* __restrict__ key1, uint64_t* __
           uint64_t* __restrict__ id1, uint32_t* __restrict__ ix0, uint32_t* __restrict__ ix1,
           int64_t n, int pass, const uint32_t* __restrict__ gofs, uint32_t* __restrict__ status,
           uint32_t* __restrict__ tile_ctr, const OsMeta* __restrict__ meta) {
+  // PDL: the previous pass (or k_os_scan) has completed and flushed; let the
+  // next pass's CTAs launch now, so a trivial pass costs little more than
+  // its predecessor's tail (they wait for this grid in their pdl_wait)
+  pdl_wait();
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   if (meta->trivial[pass]) return;
   __shared__ uint32_t cnt[RT_THREADS / 32][256];
   __shared__ uint32_t s_excl[256];   // global offset of the tile's run of each digit
@@ -352,6 +358,7 @@ k_os_pass(uint64_t* __restrict__ key0, uint64_t* __restrict__ key1, uint64_t* __
 
 __global__ void k_os_out(const uint32_t* __restrict__ ix0, const uint32_t* __restrict__ ix1,
                          int64_t n, const OsMeta* __restrict__ meta, int64_t* __restrict__ perm) {
+  pdl_wait();  // the last pass
   const uint32_t* ix = meta->src[OS_PASSES] ? ix1 : ix0;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) perm[i] = ix[i];
@@ -418,19 +425,19 @@ int launch_rank(const double* G, const int64_t* ids, int64_t n, int64_t* perm, v
   count_launch();
   k_os_init<<<ntiles, RT_THREADS, 0, st>>>(G, ids, n, key0, id0, ix0, ghist, unsorted);
   SS_LAUNCH_CHECK();
+  // scan, passes and output with programmatic dependent launch: each kernel
+  // waits for its predecessor in pdl_wait(), and trivial passes overlap
   count_launch();
-  k_os_scan<<<1, 256, 0, st>>>(ghist, n, unsorted, meta);
-  SS_LAUNCH_CHECK();
+  SS_CUDA_TRY(pdl_launch(k_os_scan, dim3(1), dim3(256), 0, st, ghist, n, unsorted, meta));
   for (int pass = 0; pass < OS_PASSES; ++pass) {
     count_launch();
-    k_os_pass<<<ntiles, RT_THREADS, OS_SMEM, st>>>(key0, key1, id0, id1, ix0, ix1, n, pass, ghist,
-                                             status + (size_t)pass * ntiles * 256, tctr + pass,
-                                             meta);
-    SS_LAUNCH_CHECK();
+    SS_CUDA_TRY(pdl_launch(k_os_pass, dim3(ntiles), dim3(RT_THREADS), OS_SMEM, st, key0, key1, id0,
+                           id1, ix0, ix1, n, pass, ghist, status + (size_t)pass * ntiles * 256,
+                           tctr + pass, meta));
   }
   count_launch();
-  k_os_out<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(ix0, ix1, n, meta, perm);
-  SS_LAUNCH_CHECK();
+  SS_CUDA_TRY(pdl_launch(k_os_out, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, st, ix0, ix1, n,
+                         meta, perm));
   return SS_OK;
 }
 
