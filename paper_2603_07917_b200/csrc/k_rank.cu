@@ -115,7 +115,14 @@ k_rank_count(const double* __restrict__ G, const int64_t* __restrict__ ids, int 
 //                  stable scatter -- no separate histogram/scan launches
 //   4. k_os_out    perm = final index array
 constexpr int RT_THREADS = 256;
-constexpr int RT_ITEMS = 8;
+#ifndef SS_RT_ITEMS
+#define SS_RT_ITEMS 8
+#endif
+constexpr int RT_ITEMS = SS_RT_ITEMS;
+#ifndef SS_OS_LB
+#define SS_OS_LB 8
+#endif
+constexpr int OS_LB = SS_OS_LB;  // look-back window (predecessor tiles per round trip)
 constexpr int RT_TILE = RT_THREADS * RT_ITEMS;
 constexpr int OS_PASSES = 16;
 constexpr int OS_SMEM = RT_TILE * (8 + 8 + 4);
@@ -300,16 +307,16 @@ k_os_pass(uint64_t* __restrict__ key0, uint64_t* __restrict__ key1, uint64_t* __
       s_excl[d] = 0;
     } else {
       st_relaxed(st, OS_AGG | run);
-      // look back 8 predecessors per round trip (independent loads in flight)
+      // look back OS_LB predecessors per round trip (independent loads in flight)
       uint32_t excl = 0;
       bool found = false;
-      for (int t0 = tile - 1; t0 >= 0 && !found; t0 -= 8) {
-        uint32_t v[8];
+      for (int t0 = tile - 1; t0 >= 0 && !found; t0 -= OS_LB) {
+        uint32_t v[OS_LB];
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
+        for (int u = 0; u < OS_LB; ++u)
           v[u] = (t0 - u >= 0) ? ld_relaxed(status + (size_t)(t0 - u) * 256 + d) : OS_PRE;
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < OS_LB; ++u) {
           if (found) break;
           while ((v[u] & ~OS_VAL) == 0u) v[u] = ld_relaxed(status + (size_t)(t0 - u) * 256 + d);
           if (t0 - u >= 0) excl += v[u] & OS_VAL;
