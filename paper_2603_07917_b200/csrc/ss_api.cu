@@ -686,6 +686,17 @@ static bool is_pinned(const void* p) {
   return a.type == cudaMemoryTypeHost;
 }
 
+// device address of pinned (page-locked, mapped) host memory; nullptr otherwise
+static void* mapped_ptr(void* p) {
+  if (!p) return nullptr;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return a.type == cudaMemoryTypeHost ? a.devicePointer : nullptr;
+}
+
 // H2D of the inputs, the fused round, D2H of G and perm -- all enqueued on st
 static int host_round_enqueue(ss_bank* h, const int8_t* q_host, const float* q_inv_host,
                               const int32_t* input_len_host, const int64_t* ids_host, int64_t nq,
@@ -714,15 +725,18 @@ static int host_round_enqueue(ss_bank* h, const int8_t* q_host, const float* q_i
   SS_CUDA_TRY(cudaMemcpyAsync(w + oI, input_len_host, (size_t)nq * 4, cudaMemcpyHostToDevice, st));
   if (ids_host)
     SS_CUDA_TRY(cudaMemcpyAsync(w + oid, ids_host, (size_t)nq * 8, cudaMemcpyHostToDevice, st));
+  // pinned perm buffer: the rank kernel stores the order straight into host
+  // memory (one D2H copy node fewer per round)
+  int64_t* perm_dev = static_cast<int64_t*>(mapped_ptr(perm_host));
   int rc = round_impl(h, (const int8_t*)(w + oq), (const float*)(w + oqi), (const int32_t*)(w + oI),
                       ids_host ? (const int64_t*)(w + oid) : nullptr, nq, k, theta, min_matches,
                       max_len, nbins, algo, P, (int32_t*)(w + onp), (int32_t*)(w + opb),
                       (int32_t*)(w + opc), (int64_t*)(w + opD), (uint8_t*)(w + ofb),
-                      (double*)(w + oG), (int64_t*)(w + operm), o, st);
+                      (double*)(w + oG), perm_dev ? perm_dev : (int64_t*)(w + operm), o, st);
   if (rc) return rc;
   w = (char*)h->ws;
   if (G_host) SS_CUDA_TRY(cudaMemcpyAsync(G_host, w + oG, (size_t)nq * 8, cudaMemcpyDeviceToHost, st));
-  if (perm_host)
+  if (perm_host && !perm_dev)
     SS_CUDA_TRY(cudaMemcpyAsync(perm_host, w + operm, (size_t)nq * 8, cudaMemcpyDeviceToHost, st));
   return SS_OK;
 }
