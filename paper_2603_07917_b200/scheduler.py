@@ -156,6 +156,7 @@ class SageScheduler:
         self.window = window
         self.cfg = cfg
         self.fallback_events = 0  # SPEC.md:194 fallback counter
+        self._host_call = None  # cached ss_schedule_round_host arguments
 
     # ---------------------------------------------------------- stages 1-3 --
     def predict(self, q, q_inv, input_len, stream=None) -> PredictState:
@@ -255,12 +256,25 @@ class SageScheduler:
         if perm_out is None:
             perm_out = np.empty(n, dtype=np.int64)
 
-        def hp(a):
-            return None if a is None else a.ctypes.data
+        # the engine calls this once per iteration with the same buffers: the
+        # argument tuple is rebuilt only when a buffer object, the stream or
+        # the config changes (numpy arrays never move their data)
+        bufs = (q, q_inv, input_len, ids, G_out, perm_out)
+        sp = _lib.stream_ptr(stream)
+        key = (n, c.k, c.theta, c.min_matches, c.max_len, c.nbins, c.algo)
+        hc = self._host_call
+        if (hc is None or hc[2] != sp or hc[3] != key or hc[4] != self.window.handle
+                or any(x is not y for x, y in zip(bufs, hc[0]))):
+            def hp(a):
+                return None if a is None else a.ctypes.data
 
-        _lib.call("ss_schedule_round_host", self.window.handle, hp(q), hp(q_inv), hp(input_len),
-                  hp(ids), n, c.k, float(np.float32(c.theta)), c.min_matches, c.max_len, c.nbins,
-                  _lib.ALGO[c.algo], hp(G_out), hp(perm_out), _lib.stream_ptr(stream))
+            args = (self.window.handle, hp(q), hp(q_inv), hp(input_len), hp(ids), n, c.k,
+                    float(np.float32(c.theta)), c.min_matches, c.max_len, c.nbins,
+                    _lib.ALGO[c.algo], hp(G_out), hp(perm_out), sp)
+            hc = self._host_call = (bufs, args, sp, key, self.window.handle)
+        rc = _lib.lib().ss_schedule_round_host(*hc[1])
+        if rc:
+            _lib.check(rc, "ss_schedule_round_host")
         return perm_out, G_out
 
     def capture_round(self, q, q_inv, input_len, ids=None, warmup: int = 2):
