@@ -571,7 +571,7 @@ __device__ __forceinline__ void warp_finish_tail(
     const int64_t* __restrict__ fb_sv2, int P, int32_t* __restrict__ npts,
     int32_t* __restrict__ pbin, int32_t* __restrict__ pcnt, int64_t* __restrict__ pD,
     int64_t* __restrict__ psv, uint8_t* __restrict__ used_fb, double* __restrict__ G,
-    FinishSmem f, int lane) {
+    FinishSmem f, int lane, double* __restrict__ G2 = nullptr) {
   const unsigned lt = (1u << lane) - 1u;
   // 3b. histogram of the winners (or the fallback law)
   const long long Iq = Iq_in;
@@ -637,6 +637,7 @@ __device__ __forceinline__ void warp_finish_tail(
   const double g = (np > 0) ? warp_gittins_exact(f.l_c, f.l_D, np, 0, (int)Iq, 0, 0, lane) : INFINITY;
   if (lane == 0) {
     G[q] = g;
+    if (G2) G2[q] = g;  // mirror (e.g. pinned host memory of the plugin call)
     npts[q] = np;
     if (used_fb) used_fb[q] = fb ? 1 : 0;
   }
@@ -659,7 +660,7 @@ k_merge_finish_w(const uint64_t* __restrict__ partials, int nlists, int64_t nq, 
                  const int64_t* __restrict__ fb_sv2, int P, int32_t* __restrict__ npts,
                  int32_t* __restrict__ pbin, int32_t* __restrict__ pcnt, int64_t* __restrict__ pD,
                  int64_t* __restrict__ psv, uint8_t* __restrict__ used_fb, double* __restrict__ G,
-                 size_t warp_bytes) {
+                 size_t warp_bytes, double* __restrict__ G2) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t q = (int64_t)blockIdx.x * MFW_WARPS + warp;
@@ -827,7 +828,7 @@ k_merge_finish_w(const uint64_t* __restrict__ partials, int nlists, int64_t nq, 
     if (out_len) out_len[q * k + i] = (i < m) ? slen[i] : 0;
   }
   warp_finish_tail(slen, m, q, k, min_matches, max_len, nbins, I[q], fb_cnt, fb_sv, fb_sv2, P, npts,
-                   pbin, pcnt, pD, psv, used_fb, G, f, lane);
+                   pbin, pcnt, pD, psv, used_fb, G, f, lane, G2);
 }
 
 // finish for neighbour lists already merged (ss_finish: the predictor API and
@@ -902,7 +903,8 @@ int launch_merge_finish(const uint64_t* partials, int nlists, int64_t nq, int k,
                         uint64_t* out_comp, int32_t* out_len, int min_matches, int max_len,
                         int nbins, const int32_t* I, const int64_t* fb_cnt, const int64_t* fb_sv,
                         const int64_t* fb_sv2, int P, int32_t* npts, int32_t* pbin, int32_t* pcnt,
-                        int64_t* pD, int64_t* psv, uint8_t* used_fb, double* G, cudaStream_t st) {
+                        int64_t* pD, int64_t* psv, uint8_t* used_fb, double* G, cudaStream_t st,
+                        double* G_mirror) {
   if (nq <= 0) return SS_OK;
   {
     const size_t wb = (((size_t)nlists * k * 8 + (size_t)k * 8 + (size_t)((k + 3) & ~3) * 4 + 15) &
@@ -916,7 +918,8 @@ int launch_merge_finish(const uint64_t* partials, int nlists, int64_t nq, int k,
       SS_CUDA_TRY(pdl_launch(k_merge_finish_w, dim3((unsigned)((nq + MFW_WARPS - 1) / MFW_WARPS)),
                              dim3(MFW_WARPS * 32), smem, st, partials, nlists, nq, k, bank_lens, head,
                              gcap, slot_offset, out_comp, out_len, min_matches, max_len, nbins, I,
-                             fb_cnt, fb_sv, fb_sv2, P, npts, pbin, pcnt, pD, psv, used_fb, G, wb));
+                             fb_cnt, fb_sv, fb_sv2, P, npts, pbin, pcnt, pD, psv, used_fb, G, wb,
+                             G_mirror));
       SS_LAUNCH_CHECK();
       return SS_OK;
     }
@@ -934,6 +937,7 @@ int launch_merge_finish(const uint64_t* partials, int nlists, int64_t nq, int k,
       partials, nlists, nq, k, kpad, bank_lens, head, gcap, slot_offset, out_comp, out_len,
       min_matches, max_len, nbins, I, fb_cnt, fb_sv, fb_sv2, P, npts, pbin, pcnt, pD, psv, used_fb, G);
   SS_LAUNCH_CHECK();
+  if (G_mirror) SS_CUDA_TRY(cudaMemcpyAsync(G_mirror, G, (size_t)nq * 8, cudaMemcpyDefault, st));
   return SS_OK;
 }
 

@@ -621,7 +621,8 @@ static int round_impl(ss_bank* h, const int8_t* q, const float* q_inv, const int
                       const int64_t* ids, int64_t nq, int32_t k, float theta, int32_t min_matches,
                       int32_t max_len, int32_t nbins, int32_t algo, int32_t P, int32_t* npts,
                       int32_t* pbin, int32_t* pcnt, int64_t* pD, uint8_t* used_fb, double* G,
-                      int64_t* perm, size_t extra_front, cudaStream_t st, bool do_rank = true) {
+                      int64_t* perm, size_t extra_front, cudaStream_t st, bool do_rank = true,
+                      double* G_mirror = nullptr) {
   if (int rc = check_bins(max_len, nbins)) return rc;
   if (P < nbins) return set_error(SS_ERR_ARG, "P (%d) must be >= nbins (%d)", P, nbins);
   if (h->head <= 0) return set_error(SS_ERR_EMPTY, "cold start: the history window is empty");
@@ -658,7 +659,8 @@ static int round_impl(ss_bank* h, const int8_t* q, const float* q_inv, const int
   if (rc) return rc;
   rc = launch_merge_finish(partials, slices, nq, k, h->lens, h->head, h->gcap, h->slot_offset, comp,
                            len, min_matches, max_len, nbins, input_len, fb, fb + nbins,
-                           fb + 2 * nbins, P, npts, pbin, pcnt, pD, nullptr, used_fb, G, st);
+                           fb + 2 * nbins, P, npts, pbin, pcnt, pD, nullptr, used_fb, G, st,
+                           G_mirror);
   if (rc) return rc;
   if (!do_rank) return SS_OK;
   return launch_rank(G, ids, nq, perm, ws + L.rank, (int64_t)rank_workspace_bytes(nq), st);
@@ -728,14 +730,16 @@ static int host_round_enqueue(ss_bank* h, const int8_t* q_host, const float* q_i
   // pinned perm buffer: the rank kernel stores the order straight into host
   // memory (one D2H copy node fewer per round)
   int64_t* perm_dev = static_cast<int64_t*>(mapped_ptr(perm_host));
+  double* G_dev = static_cast<double*>(mapped_ptr(G_host));  // finish mirrors G into it
   int rc = round_impl(h, (const int8_t*)(w + oq), (const float*)(w + oqi), (const int32_t*)(w + oI),
                       ids_host ? (const int64_t*)(w + oid) : nullptr, nq, k, theta, min_matches,
                       max_len, nbins, algo, P, (int32_t*)(w + onp), (int32_t*)(w + opb),
                       (int32_t*)(w + opc), (int64_t*)(w + opD), (uint8_t*)(w + ofb),
-                      (double*)(w + oG), perm_dev ? perm_dev : (int64_t*)(w + operm), o, st);
+                      (double*)(w + oG), perm_dev ? perm_dev : (int64_t*)(w + operm), o, st, true,
+                      G_dev);
   if (rc) return rc;
   w = (char*)h->ws;
-  if (G_host) SS_CUDA_TRY(cudaMemcpyAsync(G_host, w + oG, (size_t)nq * 8, cudaMemcpyDeviceToHost, st));
+  if (G_host && !G_dev) SS_CUDA_TRY(cudaMemcpyAsync(G_host, w + oG, (size_t)nq * 8, cudaMemcpyDeviceToHost, st));
   if (perm_host && !perm_dev)
     SS_CUDA_TRY(cudaMemcpyAsync(perm_host, w + operm, (size_t)nq * 8, cudaMemcpyDeviceToHost, st));
   return SS_OK;

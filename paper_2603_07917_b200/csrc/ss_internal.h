@@ -126,7 +126,8 @@ int launch_merge_finish(const uint64_t* partials, int nlists, int64_t nq, int k,
                         uint64_t* out_comp, int32_t* out_len, int min_matches, int max_len,
                         int nbins, const int32_t* I, const int64_t* fb_cnt, const int64_t* fb_sv,
                         const int64_t* fb_sv2, int P, int32_t* npts, int32_t* pbin, int32_t* pcnt,
-                        int64_t* pD, int64_t* psv, uint8_t* used_fb, double* G, cudaStream_t st);
+                        int64_t* pD, int64_t* psv, uint8_t* used_fb, double* G, cudaStream_t st,
+                        double* G_mirror = nullptr);
 int launch_refresh(int64_t n, const int32_t* I, const int32_t* g_new, int32_t* bucket_io,
                    int bucket_size, const int32_t* npts, const int32_t* pcnt,
                    const int64_t* pD, int P, double* G_io, uint8_t* refreshed, int force,
