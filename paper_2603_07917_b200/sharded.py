@@ -282,6 +282,42 @@ class ShardedScheduler:
                      out["perm"])
         return perm, out["G"], out
 
+    def schedule_round_host(self, q, q_inv, input_len, ids, G_out, perm_out):
+        """The round from (pinned) host buffers, as an engine calls it once per
+        iteration: H2D of this rank's queue into static device buffers, the
+        captured round (collectives included), D2H of the index and order
+        into ``G_out`` / ``perm_out``, synchronise.  Collective: every rank
+        calls it with the same queue size.  The first call per queue size
+        captures the round (eager rounds if capture is unavailable)."""
+        t = [x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x))
+             for x in (q, q_inv, input_len, ids)]
+        nq = t[0].shape[0]
+        if not hasattr(self, "_host"):
+            self._host = {}
+        st = self._host.get(nq)
+        if st is None:
+            dev = [torch.empty(x.shape, dtype=x.dtype, device="cuda") for x in t]
+            for d, x in zip(dev, t):
+                d.copy_(x)
+            try:
+                g, res = self.capture_round(*dev)
+            except Exception:  # noqa: BLE001 -- NCCL without graph support: eager rounds
+                torch.cuda.synchronize()
+                g, res = None, None
+            st = self._host[nq] = (dev, g, res)
+        dev, g, res = st
+        for d, x in zip(dev, t):
+            d.copy_(x, non_blocking=True)
+        if g is not None:
+            g.replay()
+            perm, G, _ = res
+        else:
+            perm, G, _ = self.schedule_round(*dev)
+        G_out.copy_(G, non_blocking=True)
+        perm_out.copy_(perm, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return perm_out, G_out
+
     def capture_round(self, q, q_inv, input_len, ids=None, warmup: int = 2):
         """CUDA-graph the sharded round (collectives included) for fixed input
         buffers; returns (graph, (perm, G, out)).  Every rank must capture."""

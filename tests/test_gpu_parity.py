@@ -616,6 +616,15 @@ def test_sharded_round_world1_equals_single_gpu(cuda, exchange):
         ids = np.arange(nq)
         ss = ShardedScheduler(sh, cfg, exchange=exchange)
         p1, G1, _ = ss.schedule_round(_t(q), _t(qi), _t(I), _t(ids))
+        p1, G1 = p1.clone(), G1.clone()
+        # the host-buffer call (captured round + copies), twice: same answer
+        hG = torch.empty(nq, dtype=torch.float64).pin_memory()
+        hp = torch.empty(nq, dtype=torch.int64).pin_memory()
+        for _ in range(2):
+            hG.zero_()
+            hp.zero_()
+            ss.schedule_round_host(q, qi, I, ids.astype(np.int64), hG, hp)
+            assert torch.equal(hG, G1.cpu()) and torch.equal(hp, p1.cpu())
         if ss.peer is not None:
             p1, G1 = p1.clone(), G1.clone()
             p1b, G1b, _ = ss.schedule_round(_t(q), _t(qi), _t(I), _t(ids))  # buffers reused
