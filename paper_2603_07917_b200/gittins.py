@@ -82,8 +82,8 @@ def gittins_index_batch(support: torch.Tensor, masses: torch.Tensor, npts: torch
 
 
 def _to_dev(d: DiscreteDistribution):
-    s = torch.as_tensor(np.ascontiguousarray(d.support), dtype=torch.float64, device="cuda")
-    m = torch.as_tensor(np.ascontiguousarray(d.masses), dtype=torch.float64, device="cuda")
+    s = torch.as_tensor(np.array(d.support, dtype=np.float64), dtype=torch.float64, device="cuda")
+    m = torch.as_tensor(np.array(d.masses, dtype=np.float64), dtype=torch.float64, device="cuda")
     return s.reshape(1, -1), m.reshape(1, -1)
 
 
