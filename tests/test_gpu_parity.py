@@ -576,11 +576,12 @@ def test_rank_bit_exact(cuda, n):
     assert np.array_equal(perm, O.rank(G, sids))
 
 
-def test_rank_special_values(cuda):
-    """inf (no law yet), zero, wide exponent range, negative and > 2^32 ids."""
+@pytest.mark.parametrize("n", [3001, 50_000])
+def test_rank_special_values(cuda, n):
+    """inf (no law yet), zero, wide exponent range, negative and > 2^32 ids
+    (counting rank and onesweep)."""
     from paper_2603_07917_b200.scheduler import rank
     rng = np.random.default_rng(9)
-    n = 50_000
     G = rng.choice(np.array([np.inf, 0.0, 1e-300, 1e300, 2.0, 2.0, 5e3, 7.25]), n)
     ids = rng.integers(-(1 << 40), 1 << 40, n).astype(np.int64)
     ids[:10] = ids[10]  # duplicate ids: index order breaks the tie (stable)
