@@ -493,9 +493,13 @@ int ss_topk_scatter(ss_bank_t* h, const int8_t* q, const float* q_inv, int64_t n
 
 int ss_ipc_malloc(int32_t device, int64_t bytes, void** out) {
   if (!out || bytes <= 0) return set_error(SS_ERR_ARG, "ipc_malloc: bad args");
+  int prev = 0;
+  SS_CUDA_TRY(cudaGetDevice(&prev));
   SS_CUDA_TRY(cudaSetDevice(device));
-  SS_CUDA_TRY(cudaMalloc(out, (size_t)bytes));  // plain cudaMalloc: IPC-exportable
-  SS_CUDA_TRY(cudaMemset(*out, 0, (size_t)bytes));
+  cudaError_t e = cudaMalloc(out, (size_t)bytes);  // plain cudaMalloc: IPC-exportable
+  if (e == cudaSuccess) e = cudaMemset(*out, 0, (size_t)bytes);
+  cudaSetDevice(prev);  // the caller's current device is left as it was
+  if (e != cudaSuccess) return set_error(SS_ERR_CUDA, "ipc_malloc: %s", cudaGetErrorString(e));
   return SS_OK;
 }
 

@@ -318,6 +318,11 @@ class ShardedScheduler:
         torch.cuda.current_stream().synchronize()
         return perm_out, G_out
 
+    def close(self):
+        """Release the P2P receive buffers and peer mappings (if any)."""
+        if self.peer is not None:
+            self.peer.close()
+
     def capture_round(self, q, q_inv, input_len, ids=None, warmup: int = 2):
         """CUDA-graph the sharded round (collectives included) for fixed input
         buffers; returns (graph, (perm, G, out)).  Every rank must capture."""
