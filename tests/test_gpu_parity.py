@@ -638,8 +638,8 @@ def test_sharded_round_world1_equals_single_gpu(cuda, exchange):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_topk_scatter_shards_equal_single_bank(cuda, world):
+@pytest.mark.parametrize("world,algo", [(2, "auto"), (3, "auto"), (2, "scan")])
+def test_topk_scatter_shards_equal_single_bank(cuda, world, algo):
     """ss_topk_scatter addressing, all ranks simulated in one process: shard r
     stores the merged rows of every rank's queries into that rank's receive
     buffer at [r][q]; merging a receive buffer gives the single-bank top-k of
@@ -667,7 +667,7 @@ def test_topk_scatter_shards_equal_single_bank(cuda, world):
     tl = (C.c_void_p * world)(*[t.data_ptr() for t in recv_l])
     for r, w in enumerate(wins):
         _lib.call("ss_topk_scatter", w.handle, _lib.ptr(q), _lib.ptr(qi), world * nq, k, 0.5,
-                  _lib.ALGO["auto"], world, r, tc, tl, _lib.stream_ptr())
+                  _lib.ALGO[algo], world, r, tc, tl, _lib.stream_ptr())
     full, *_ = _bank(n, dim, 40, 5, world * nq)
     c0, l0 = full.topk(q, qi, k, 0.5)
     for r in range(world):
