@@ -728,7 +728,9 @@ static size_t ts_smem_extra(int code, int dim) {
   return code == 224 ? (size_t)ts::BM * ts::BK : code == 512 ? (size_t)ts::BM * dim : 0;
 }
 static int ts_stages(int k, int code, int dim) {
-  for (int s = 8; s >= 3; --s)
+  // SS_TS_STAGES caps the bank-stage ring (ablation; default: as many as fit)
+  static const int cap = getenv("SS_TS_STAGES") ? atoi(getenv("SS_TS_STAGES")) : 8;
+  for (int s = std::min(8, std::max(3, cap)); s >= 3; --s)
     if (ts_fixed_smem(k) + ts_smem_extra(code, dim) + (size_t)s * ts_rows(code) * ts::BK <=
         227 * 1024)
       return s;
