@@ -213,6 +213,16 @@ def test_topk_large_batch_tcgen05(cuda, theta):
     _check_topk(w, comp, keys, seq, ref, 64)
 
 
+@pytest.mark.parametrize("theta", [-1.0, 0.0])
+def test_topk_pure_large_bank_bit_exact(cuda, theta):
+    """theta <= 0 (the TS kernel's shared slice bounds) on a 300k-row bank
+    with 256 queries: every query's top-k equals the oracle's."""
+    w, be, bl, q, qi = _bank(300_000, 384, 64, 21, 256)
+    keys, seq, ref = _oracle_topk(w, be, q, qi, 64, theta)
+    comp, ln = w.topk(q, qi, 64, theta, "tcgen05")
+    _check_topk(w, comp, keys, seq, ref, 64)
+
+
 @pytest.mark.parametrize("algo", ["scan", "tcgen05"])
 def test_topk_edges(cuda, algo):
     """ragged nq, partially filled ring, ties, degenerate query, k > rows."""
