@@ -284,6 +284,11 @@ __device__ __noinline__ float insert_locked(uint32_t mask, const float* sl, floa
 // slice has published, the union of their top-R holds >= k rows at or above
 // that minimum, so it bounds the global k-th key from below.  Slots that are
 // still 0 make the minimum 0 (no bound).
+#ifndef SS_SHARE_EVERY
+#define SS_SHARE_EVERY 2
+#endif
+constexpr int SHARE_EVERY = SS_SHARE_EVERY;
+
 template <int BN, int NACC, int ASPLIT, bool SHARE = false>
 __global__ void __launch_bounds__(THREADS, 1)
 k_topk_ts(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmQ,
@@ -482,8 +487,10 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUten
       const float* ciw = s_inv + sl * 256 + grp * HALF;
       if constexpr (SHARE) {
         // minimum over the slices' published R-th best keys (independent
-        // loads; their latency overlaps the wait for this tile's MMA)
-        if (q < nq) {
+        // loads; their latency overlaps the wait for this tile's MMA), every
+        // SHARE_EVERY tiles: a staler bound only prunes less, and the
+        // gridDim.y L2 loads per query were a visible share of the tile loop
+        if (q < nq && (t % SHARE_EVERY) == 0) {
           uint32_t m = ~0u;
           for (int s2 = 0; s2 < (int)gridDim.y; ++s2) m = min(m, __ldcg(gslots + (int64_t)s2 * nq + q));
           if (m != 0u && m != ~0u) thr = fmaxf(thr, s_threshold(f32_unorder(m), iq));
