@@ -1,40 +1,70 @@
 """Benchmark of the SageSched per-round scheduling hot path on B200.
 
 One step = one scheduling round over one batch of synthetic pending requests:
-predict (1M x 384 int8 history bank -> top-64 -> 128-bin length histogram)
--> cost (O^2/2 + I*O) -> Gittins index -> rank.  Workload = BASELINE.json
-configs[1] ("1M-entry bank, 1024 pending prompts per round, k=64, 128 bins").
+predict (history bank -> top-64 -> 128-bin length histogram) -> cost
+(O^2/2 + I*O) -> Gittins index -> rank.
+
+  N = 1   workload = BASELINE.json configs[1] (1M x 384 bank, 1024 pending
+          prompts per round, k=64, 128 bins, theta = 0.8) on one GPU.
+  N > 1   workload = configs[3] (16M x 384 bank row-sharded over the N GPUs,
+          one 8192-request queue owned by rank 0; single-owner round:
+          query broadcast, local fused top-k, all-gather of k candidates per
+          query, merge + cost + Gittins + rank on the owner) -- strong
+          scaling.  ``--config c4 --sharded`` runs the same code path at N=1.
 
   value  requests scheduled / s with inputs resident in HBM (CUDA-graph replay
-         of the fused round, CUDA events, max over ranks)
+         of the round, CUDA events, max over ranks)
   e2e    same metric through the plugin call from pinned HOST buffers
-         (ss_schedule_round_host: H2D + round + D2H inside the timed region)
+         (H2D + round + D2H inside the timed region)
+  roofline       the dominant kernel (the tcgen05 similarity + fused top-k)
+                 against the int8 tensor peak measured live by tools/mma_peak.cu
+  roofline_scan  the bank-scan form of the same kernel (8 queries, HBM-bound)
+                 against the measured HBM copy bandwidth -- BASELINE's "bank-scan
+                 HBM GB/s % of peak"
 
 ``--impl reference`` times the reference's CPU implementation of the path
-(servesim from baseline/_ref where the code exists, the oracle restatement of
-the SPEC-only pieces) on a bounded sample, on the host cores.
+(servesim from baseline/_ref where the code exists -- match/gittins_min --
+and the oracle restatement of the SPEC-only pieces) on the host cores: every
+step is a sample of the round's queries scored against the WHOLE bank.
 """
 
 from __future__ import annotations
 
-import argparse
-import json
-import math
 import os
-import subprocess
-import sys
-import threading
-import time
 
-import numpy as np
+# CPU thread pools (OpenBLAS GEMM, numba) sized before numpy / numba load
+_NCPU = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+for _v in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS", "NUMBA_NUM_THREADS"):
+    os.environ[_v] = str(_NCPU)
+os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/nbcache")
+
+import argparse  # noqa: E402
+import ctypes  # noqa: E402
+import json  # noqa: E402
+import socket  # noqa: E402
+import subprocess  # noqa: E402
+import sys  # noqa: E402
+import threading  # noqa: E402
+import time  # noqa: E402
+
+import numpy as np  # noqa: E402
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-N_BANK, DIM, NQ, K, NBINS, MAX_LEN = 1 << 20, 384, 1024, 64, 128, 2048
+DIM, K, NBINS, MAX_LEN = 384, 64, 128, 2048
 THETA, MIN_MATCHES, N_CLUSTERS = 0.8, 20, 4096
 SEED = 0
-WORKLOAD = "c2: 1M-entry x 384-d int8 history bank, 1024 pending prompts/round, k=64, 128 bins"
+CONFIGS = {
+    "c2": dict(n_bank=1 << 20, nq=1024,
+               workload="c2: 1M-entry x 384-d int8 history bank, 1024 pending prompts/round, "
+                        "k=64, 128 bins"),
+    "c4": dict(n_bank=1 << 24, nq=8192,
+               workload="c4: 16M-entry x 384-d int8 history bank, 8192 pending prompts/round, "
+                        "k=64, 128 bins"),
+}
+METRIC = "requests scheduled/sec per round (predict+cost+Gittins+rank)"
+SCAN_NQ = 8  # the bank-scan (HBM-bound) form of the similarity kernel
 
 
 def peaks():
@@ -72,9 +102,6 @@ class ClockSampler:
         for line in self.proc.stdout:
             self.lines.append((time.time(), line.strip()))
 
-    def mark(self):
-        return time.time()
-
     def __exit__(self, *a):
         if self.proc:
             time.sleep(0.1)
@@ -102,41 +129,143 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+# ------------------------------------------------------ device measurement --
+def time_ms(fn, reps, stream=None):
+    """Average CUDA-event time of fn() on `stream` (default: torch's current)."""
+    import torch
+    st = stream or torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(st)
+    for _ in range(reps):
+        fn()
+    e1.record(st)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+def int8_peak():
+    """Dense int8 tensor-core ceiling measured now on this GPU by the probe
+    tools/mma_peak.cu (operands resident, back-to-back tcgen05.mma kind::i8,
+    M=128 K=32, one CTA per SM).  -> (TOPS, detail)."""
+    import torch
+    from paper_2603_07917_b200 import _build
+    _build.build_probes()
+    so = _build.PROBES[os.path.join(_build.TOOLS_DIR, "mma_peak.cu")]
+    lib = ctypes.CDLL(so)
+    lib.mma_peak_run.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p]
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    st = torch.cuda.current_stream()
+    out = {}
+    for n, a_tmem in ((256, 0), (256, 1), (208, 1)):
+        tiles = 12000
+        if lib.mma_peak_run(sms, 50, n, a_tmem, ctypes.c_void_p(st.cuda_stream)):
+            continue
+        ms = min(time_ms(lambda: lib.mma_peak_run(sms, tiles, n, a_tmem,
+                                                  ctypes.c_void_p(st.cuda_stream)), 1)
+                 for _ in range(3))
+        ops = 2.0 * 128 * n * DIM * tiles * sms
+        out[f"N{n}_{'ts' if a_tmem else 'ss'}"] = round(ops / (ms / 1e3) / 1e12, 1)
+    best = max(out.values()) if out else None
+    return best, out
+
+
+def cublas_int8_tops():
+    """cuBLASLt int8 GEMM rate (torch._int_mm, 8192 x 8192 x 384 -> int32), for context."""
+    import torch
+    try:
+        a = torch.randint(-127, 128, (8192, DIM), dtype=torch.int8, device="cuda")
+        b = torch.randint(-127, 128, (DIM, 8192), dtype=torch.int8, device="cuda")
+        torch._int_mm(a, b)
+        ms = min(time_ms(lambda: torch._int_mm(a, b), 20) for _ in range(3))
+        return round(2.0 * 8192 * 8192 * DIM / (ms / 1e3) / 1e12, 1)
+    except Exception:
+        return None
+
+
+def ncu_traffic(workload_key: str, kernel: str):
+    """dram read+write bytes per launch of `kernel` on this workload, from the
+    committed ncu --set full summary (profiles/ncu_traffic.json), else None."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        return d.get(workload_key, {}).get(kernel)
+    except Exception:
+        return None
+
+
+def topk_kernel_name(nq: int) -> str:
+    """The stage-1 kernel the library launches for nq queries (csrc/k_topk_sm100.cu
+    use_ts): the A-in-TMEM kernel above one 128-query tile, the streaming
+    form of k_topk_tc at or below it."""
+    return "k_topk_ts" if nq > 128 else "k_topk_tc"
+
+
+def time_topk(window, q, qi, nq, theta, reps):
+    """The dominant kernel alone (similarity + fused top-k, ss_topk_partials)
+    on torch's current stream, CUDA events.  -> (ms per launch, slices)."""
+    import torch
+    from paper_2603_07917_b200 import _lib
+    max_slices = 1024
+    part = torch.empty(max_slices * nq * K, dtype=torch.int64, device="cuda")
+    ns = ctypes.c_int32()
+    lib = _lib.lib()
+
+    def go():
+        rc = lib.ss_topk_partials(window.handle, q.data_ptr(), qi.data_ptr(), nq, K,
+                                  float(np.float32(theta)), _lib.ALGO["tcgen05"], part.data_ptr(),
+                                  max_slices, ctypes.byref(ns), _lib.stream_ptr())
+        if rc:
+            _lib.check(rc, "ss_topk_partials")
+    go()
+    return time_ms(go, reps), int(ns.value)
+
+
 # ------------------------------------------------------------ our arm -----
 def run_ours(args):
     import torch
     import torch.distributed as dist
 
     from paper_2603_07917_b200 import _build, _lib
-    from paper_2603_07917_b200.history import HistoryWindow
-    from paper_2603_07917_b200.scheduler import RoundConfig, SageScheduler
-    from paper_2603_07917_b200.synthetic import make_bank_device, make_queries
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    # SS_BENCH_SHARDED=1 runs the sharded (multi-GPU) round even at N = 1,
-    # under torchrun, so its code path can be exercised on one GPU
-    sharded = world > 1 or os.environ.get("SS_BENCH_SHARDED") == "1"
+    sharded = world > 1 or args.sharded
     if sharded:
+        if "MASTER_ADDR" not in os.environ:  # --sharded at N = 1 without torchrun
+            with socket.socket() as s:
+                s.bind(("127.0.0.1", 0))
+                os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(s.getsockname()[1]),
+                                  RANK="0", WORLD_SIZE="1")
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
-    if _build.is_stale() and rank == 0:
+    if rank == 0 and (_build.is_stale() or not os.path.exists(_build.LIB_PATH)):
         _build.build()
     if sharded:
         dist.barrier()
     _lib.load()
-
     if sharded:
         return run_sharded(args, world, rank, local)
-    emb, lens, _ = make_bank_device(N_BANK, DIM, N_CLUSTERS, SEED)
-    win = HistoryWindow(N_BANK, DIM)
+    return run_single(args)
+
+
+def run_single(args):
+    import torch
+
+    from paper_2603_07917_b200 import _lib
+    from paper_2603_07917_b200.history import HistoryWindow
+    from paper_2603_07917_b200.scheduler import RoundConfig, SageScheduler
+    from paper_2603_07917_b200.synthetic import make_bank_device, make_queries
+
+    C = CONFIGS[args.config]
+    n_bank, nq = C["n_bank"], C["nq"]
+    emb, lens, _ = make_bank_device(n_bank, DIM, N_CLUSTERS, SEED)
+    win = HistoryWindow(n_bank, DIM)
     win.push(emb, lens)
     del emb, lens
-    q, qi, I, ids = make_queries(NQ, DIM, N_CLUSTERS, SEED, qseed=1000 + rank)
+    q, qi, I, ids = make_queries(nq, DIM, N_CLUSTERS, SEED, qseed=1000)
     dq, dqi, dI, dids = (torch.as_tensor(x, device="cuda") for x in (q, qi, I, ids))
-    cfg = RoundConfig(k=K, theta=THETA, min_matches=MIN_MATCHES, max_len=MAX_LEN, nbins=NBINS,
-                      algo=args.algo)
+    cfg = RoundConfig(k=K, theta=THETA, min_matches=MIN_MATCHES, max_len=MAX_LEN, nbins=NBINS)
     sched = SageScheduler(win, cfg)
 
     # launches per round (counted on an eager round)
@@ -145,96 +274,111 @@ def run_ours(args):
     torch.cuda.synchronize()
     per_round = _lib.launch_count() - c0
 
-    graph, out = sched.capture_round(dq, dqi, dI, dids)
+    graph, _ = sched.capture_round(dq, dqi, dI, dids)
     for _ in range(args.warmup):
         graph.replay()
     torch.cuda.synchronize()
 
-    sampler = ClockSampler(local)
+    sampler = ClockSampler(0)
     with sampler:
-        if world > 1:
-            dist.barrier()
         torch.cuda.synchronize()
         t0 = time.time()
-        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ev0.record()
-        for _ in range(args.steps):
-            graph.replay()
-        ev1.record()
-        torch.cuda.synchronize()
+        ms = time_ms(graph.replay, args.steps) * args.steps
         t1 = time.time()
-        if world > 1:
-            dist.barrier()
-        ms = ev0.elapsed_time(ev1)
         clocks = sampler.summary(t0, t1)
-
-        # dominant kernel alone (similarity + fused top-k), same stream, CUDA events
-        algo_used, kern_ms, n_slices = time_topk_kernel(sched, dq, dqi, args)
-
+        # dominant kernel alone (similarity + fused top-k), same stream
+        kern_ms, n_slices = time_topk(win, dq, dqi, nq, THETA, max(3, args.steps))
+        # the bank scan: 8 queries against the whole bank (HBM-bound form)
+        scan_ms, scan_slices = time_topk(win, dq[:SCAN_NQ].contiguous(), dqi[:SCAN_NQ].contiguous(),
+                                         SCAN_NQ, THETA, max(10, args.steps))
         # e2e: plugin call from pinned host buffers
         e2e_ms, h2d, d2h = time_e2e(sched, q, qi, I, ids, args)
+    # north star's literal "select top-k" (theta <= 0): same round, pure top-k
+    pure = None
+    if not args.no_pure:
+        pcfg = RoundConfig(k=K, theta=-1.0, min_matches=MIN_MATCHES, max_len=MAX_LEN, nbins=NBINS)
+        psched = SageScheduler(win, pcfg)
+        pg, _ = psched.capture_round(dq, dqi, dI, dids)
+        for _ in range(3):
+            pg.replay()
+        pms = time_ms(pg.replay, max(3, args.steps // 2))
+        pk_ms, _ = time_topk(win, dq, dqi, nq, -1.0, max(3, args.steps // 2))
+        pure = {"theta": -1.0, "value": round(nq / (pms / 1e3), 1), "unit": "requests/s",
+                "ms_per_step": round(pms, 4), "kernel_ms": round(pk_ms, 4)}
 
-    # max over ranks
-    vals = torch.tensor([ms, e2e_ms, kern_ms], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(vals, op=dist.ReduceOp.MAX)
-    ms, e2e_ms, kern_ms = vals.tolist()
+    pk = peaks()
+    i8_peak, i8_detail = int8_peak()
+    ops = 2.0 * nq * n_bank * DIM
+    achieved = ops / (kern_ms / 1e3) / 1e12
+    kname = topk_kernel_name(nq)
+    roof = {"bound": "tensor", "achieved": round(achieved, 1), "peak": i8_peak, "unit": "TFLOP/s",
+            "frac": round(achieved / i8_peak, 4) if i8_peak else None,
+            "peak_source": "int8 dense tcgen05.mma kind::i8 ceiling measured live on this GPU by "
+                           f"tools/mma_peak.cu (best of {i8_detail}); nominal 4500",
+            "cublas_int8_tops": cublas_int8_tops(),
+            "work_per_launch": f"2 * nq * N * d = 2 * {nq} * {n_bank} * {DIM} int8 ops",
+            "kernel": kname, "kernel_ms": round(kern_ms, 4), "n_slices": n_slices,
+            "kernel_share_of_step": round(kern_ms / (ms / args.steps), 3),
+            "traffic": ncu_traffic(args.config, kname),
+            "traffic_algorithmic": int(n_bank * (DIM + 4))}
+    scan_bytes = n_bank * (DIM + 4) + SCAN_NQ * (DIM + 4)
+    scan_gbs = scan_bytes / (scan_ms / 1e3) / 1e9
+    roof_scan = {"bound": "hbm", "achieved": round(scan_gbs, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
+                 "frac": round(scan_gbs / pk["hbm_gbs"], 4),
+                 "frac_of_8tbs_datasheet": round(scan_gbs / 8000.0, 4),
+                 "peak_source": "measured copy bandwidth (MEASURED_PEAKS.json)",
+                 "work_per_launch": f"bank bytes N * (d + 4) = {n_bank} * {DIM + 4}",
+                 "kernel": topk_kernel_name(SCAN_NQ), "nq": SCAN_NQ, "n_slices": scan_slices,
+                 "kernel_ms": round(scan_ms, 4),
+                 "traffic": ncu_traffic(args.config + "_scan8", topk_kernel_name(SCAN_NQ))}
+    line = {
+        "metric": METRIC, "value": round(nq * args.steps / (ms / 1e3), 1), "unit": "requests/s",
+        "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int8",
+        "data": "synthetic (seeded clustered int8 embeddings, lognormal lengths)",
+        "config": {"workload": C["workload"], "bank_rows": n_bank, "dim": DIM, "nq": nq, "k": K,
+                   "nbins": NBINS, "theta": THETA, "min_matches": MIN_MATCHES,
+                   "parallelism": "single GPU",
+                   "l2": f"bank ({n_bank * (DIM + 4) / 1e6:.0f} MB) > L2 (126 MB): every round "
+                         "streams it from HBM"},
+        "e2e": {"value": round(nq * args.steps / (e2e_ms / 1e3), 1), "unit": "requests/s",
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "ms_per_step": round(e2e_ms / args.steps, 4)},
+        "roofline": roof,
+        "roofline_scan": roof_scan,
+        "pure_topk": pure,
+        "gpu_launches": int(per_round * args.steps),
+        "clocks": clocks,
+    }
+    if not args.no_cpu_baseline and args.config == "c2":
+        line["cpu_baseline"] = cpu_baseline(args.config, budget_s=args.cpu_budget)
+    print(json.dumps(line), flush=True)
 
-    if rank == 0:
-        pk = peaks()
-        req = NQ * world
-        value = req * args.steps / (ms / 1e3)
-        kern_s = kern_ms / 1e3
-        if algo_used == "tcgen05":
-            ops = 2.0 * NQ * N_BANK * DIM
-            achieved = ops / kern_s / 1e12
-            peak = 2.0 * pk["bf16_tflops"]
-            roof = {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak,
-                    "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
-                    "peak_source": "int8 dense = 2 x measured bf16 burst (MEASURED_PEAKS.json)"}
-        else:
-            byts = N_BANK * DIM + N_BANK * 4.0 + NQ * DIM
-            achieved = byts / kern_s / 1e9
-            peak = pk["hbm_gbs"]
-            roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                    "frac": round(achieved / peak, 4),
-                    "peak_source": "measured copy bandwidth (MEASURED_PEAKS.json)"}
-        roof["kernel"] = topk_kernel_name(algo_used, NQ)
-        roof["kernel_ms"] = round(kern_ms, 4)
-        roof["kernel_share_of_step"] = round(kern_ms / (ms / args.steps), 3)
-        roof["traffic"] = ncu_traffic(roof["kernel"])
-        line = {
-            "metric": "requests scheduled/sec per round (predict+cost+Gittins+rank) vs a 1M-entry bank",
-            "value": round(value, 1), "unit": "requests/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int8",
-            "data": "synthetic (seeded clustered int8 embeddings, lognormal lengths)",
-            "config": {"workload": WORKLOAD, "bank_rows": N_BANK, "dim": DIM, "nq": NQ, "k": K,
-                       "nbins": NBINS, "theta": THETA, "min_matches": MIN_MATCHES,
-                       "similarity": algo_used, "n_slices": n_slices,
-                       "parallelism": f"replica x{world}" if world > 1 else "single GPU",
-                       "l2": f"bank ({N_BANK * (DIM + 4) / 1e6:.0f} MB) > L2 (126 MB): every "
-                             "round streams it from HBM"},
-            "e2e": {"value": round(req * args.steps / (e2e_ms / 1e3), 1), "unit": "requests/s",
-                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "ms_per_step": round(e2e_ms / args.steps, 4)},
-            "roofline": roof,
-            "gpu_launches": int(per_round * args.steps),
-            "clocks": clocks,
-        }
-        if world == 1 and not args.no_cpu_baseline:
-            line["cpu_baseline"] = cpu_baseline(budget_s=args.cpu_budget)
-        print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
+
+def time_e2e(sched, q, qi, I, ids, args):
+    import torch
+
+    def pin(a):
+        return torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+
+    nq = q.shape[0]
+    hq, hqi, hI, hids = pin(q), pin(qi), pin(I), pin(ids)
+    G = torch.empty(nq, dtype=torch.float64).pin_memory().numpy()
+    perm = torch.empty(nq, dtype=torch.int64).pin_memory().numpy()
+    s = torch.cuda.Stream()
+    for _ in range(max(3, args.warmup)):
+        sched.schedule_round_host(hq, hqi, hI, hids, G, perm, stream=s)
+    ms = time_ms(lambda: sched.schedule_round_host(hq, hqi, hI, hids, G, perm, stream=s),
+                 args.steps, stream=s) * args.steps
+    return ms, int(hq.nbytes + hqi.nbytes + hI.nbytes + hids.nbytes), int(G.nbytes + perm.nbytes)
 
 
 def run_sharded(args, world, rank, local):
-    """N GPUs: the 1M-row bank is row-sharded (1M/N rows per GPU) and every
-    rank owns a queue of 1024 pending prompts (weak scaling in requests:
-    per-GPU similarity work stays 1024 x 1M).  Per round: query all-gather,
-    local fused top-k of all N*1024 queries, candidate all-to-all, merge,
-    histogram all-reduce, then cost/Gittins/rank of each rank's own queue."""
+    """Single-owner round over a row-sharded bank (c4 by default at N > 1):
+    rank 0 owns the whole queue; every GPU scores it against its 1/N of the
+    bank; the k candidates per query are all-gathered; the owner merges,
+    finishes and ranks.  Strong scaling: the total work is fixed."""
     import torch
     import torch.distributed as dist
 
@@ -243,39 +387,37 @@ def run_sharded(args, world, rank, local):
     from paper_2603_07917_b200.sharded import ShardedHistory, ShardedScheduler
     from paper_2603_07917_b200.synthetic import make_bank_device, make_queries
 
-    emb, lens, _ = make_bank_device(N_BANK, DIM, N_CLUSTERS, SEED)
-    hist = ShardedHistory(N_BANK, DIM)
+    C = CONFIGS[args.config]
+    n_bank, nq = C["n_bank"], C["nq"]
+    owner = 0
+    emb, lens, _ = make_bank_device(n_bank, DIM, N_CLUSTERS, SEED)
+    hist = ShardedHistory(n_bank, DIM)
     hist.push(emb, lens)
     del emb, lens
-    q, qi, I, ids = make_queries(NQ, DIM, N_CLUSTERS, SEED, qseed=1000 + rank)
-    ids = ids + rank * NQ
+    torch.cuda.empty_cache()
+    q, qi, I, ids = make_queries(nq, DIM, N_CLUSTERS, SEED, qseed=1000)
     dq, dqi, dI, dids = (torch.as_tensor(x, device="cuda") for x in (q, qi, I, ids))
-    cfg = RoundConfig(k=K, theta=THETA, min_matches=MIN_MATCHES, max_len=MAX_LEN, nbins=NBINS,
-                      algo=args.algo)
-    # SS_SHARD_EXCHANGE=p2p: fused merge + exchange over IPC-mapped peer
-    # buffers (ss_topk_scatter) instead of the candidate all_to_all
-    exchange = os.environ.get("SS_SHARD_EXCHANGE", "nccl")
-    sched = ShardedScheduler(hist, cfg, exchange=exchange)
+    cfg = RoundConfig(k=K, theta=THETA, min_matches=MIN_MATCHES, max_len=MAX_LEN, nbins=NBINS)
+    sched = ShardedScheduler(hist, cfg, exchange=args.exchange, owner=owner)
+    mine = rank == owner
+    args_round = (dq, dqi, dI, dids) if mine else (None, None, None, None)
     c0 = _lib.launch_count()
-    sched.schedule_round(dq, dqi, dI, dids)
+    sched.schedule_round(*args_round, nq=nq)
     torch.cuda.synchronize()
     per_round = _lib.launch_count() - c0
-    # the whole sharded round (NCCL collectives included) as one CUDA graph;
-    # eager rounds if this NCCL/driver combination cannot capture
     graph = None
     try:
-        graph, _ = sched.capture_round(dq, dqi, dI, dids)
+        graph, _ = sched.capture_round(*args_round, nq=nq)
     except Exception as e:  # noqa: BLE001
         print(f"sharded round not captured ({type(e).__name__}: {e}); timing eager rounds",
               file=sys.stderr)
-        graph = None
         torch.cuda.synchronize()
 
     def one_round():
         if graph is not None:
             graph.replay()
         else:
-            sched.schedule_round(dq, dqi, dI, dids)
+            sched.schedule_round(*args_round, nq=nq)
 
     for _ in range(args.warmup):
         one_round()
@@ -285,77 +427,66 @@ def run_sharded(args, world, rank, local):
         dist.barrier()
         torch.cuda.synchronize()
         t0 = time.time()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(args.steps):
-            one_round()
-        e1.record()
-        torch.cuda.synchronize()
+        ms = time_ms(one_round, args.steps) * args.steps
         t1 = time.time()
         dist.barrier()
-        ms = e0.elapsed_time(e1)
         clocks = sampler.summary(t0, t1)
-        # e2e: pinned host queue in, order + indices out, every step
-        hq, hqi, hI, hids = (torch.from_numpy(np.ascontiguousarray(x)).pin_memory()
-                             for x in (q, qi, I, ids))
-        hG = torch.empty(NQ, dtype=torch.float64).pin_memory()
-        hp = torch.empty(NQ, dtype=torch.int64).pin_memory()
-        for _ in range(max(1, args.warmup)):  # first call captures the host round
-            sched.schedule_round_host(hq, hqi, hI, hids, hG, hp)
+        # e2e: the owner's pinned host queue in, order + indices out, every step
+        if mine:
+            hq, hqi, hI, hids = (torch.from_numpy(np.ascontiguousarray(x)).pin_memory()
+                                 for x in (q, qi, I, ids))
+            hG = torch.empty(nq, dtype=torch.float64).pin_memory()
+            hp = torch.empty(nq, dtype=torch.int64).pin_memory()
+            host_args = (hq, hqi, hI, hids, hG, hp)
+        else:
+            host_args = (None, None, None, None, None, None)
+        for _ in range(max(3, args.warmup)):
+            sched.schedule_round_host(*host_args, nq=nq)
         dist.barrier()
-        torch.cuda.synchronize()
-        e0.record()
-        for _ in range(args.steps):
-            sched.schedule_round_host(hq, hqi, hI, hids, hG, hp)
-        e1.record()
-        torch.cuda.synchronize()
-        e2e_ms = e0.elapsed_time(e1)
-        # dominant kernel: the local similarity over all world*NQ queries
-        q_all = torch.cat([dq] * world)
-        qi_all = torch.cat([dqi] * world)
-        algo_used, kern_ms, n_slices = time_topk_kernel(
-            type("S", (), {"cfg": cfg, "window": hist.window})(), q_all, qi_all, args,
-            nq=world * NQ)
+        e2e_ms = time_ms(lambda: sched.schedule_round_host(*host_args, nq=nq), args.steps) * args.steps
+        # dominant kernel: the local similarity of the whole queue against this shard
+        kern_ms, n_slices = time_topk(hist.window, dq, dqi, nq, THETA, max(3, args.steps))
     vals = torch.tensor([ms, e2e_ms, kern_ms], dtype=torch.float64, device="cuda")
     dist.all_reduce(vals, op=dist.ReduceOp.MAX)
     ms, e2e_ms, kern_ms = vals.tolist()
     if rank == 0:
-        pk = peaks()
-        req = NQ * world
-        ops = 2.0 * (world * NQ) * (N_BANK // world) * DIM
+        i8_peak, i8_detail = int8_peak()
+        ops = 2.0 * nq * (n_bank // world) * DIM
         achieved = ops / (kern_ms / 1e3) / 1e12
-        peak = 2.0 * pk["bf16_tflops"]
         line = {
-            "metric": "requests scheduled/sec per round (predict+cost+Gittins+rank) vs a 1M-entry bank",
-            "value": round(req * args.steps / (ms / 1e3), 1), "unit": "requests/s",
+            "metric": METRIC, "value": round(nq * args.steps / (ms / 1e3), 1), "unit": "requests/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "int8",
+            "scaling": "strong", "vs_baseline": None, "dtype": "int8",
             "data": "synthetic (seeded clustered int8 embeddings, lognormal lengths)",
-            "config": {"workload": WORKLOAD + f"; bank row-sharded over {world} GPUs, one "
-                       f"1024-request queue per GPU", "bank_rows": N_BANK, "dim": DIM,
-                       "nq_per_gpu": NQ, "k": K, "nbins": NBINS, "theta": THETA,
-                       "similarity": algo_used, "n_slices": n_slices,
-                       "parallelism": f"bank shard x{world} + NCCL all-gather/all-reduce + "
-                                      + ("P2P fused merge-exchange" if exchange == "p2p"
-                                         else "NCCL all-to-all"),
+            "config": {"workload": C["workload"] + f"; bank row-sharded over {world} GPU(s), "
+                       "one queue owned by rank 0", "bank_rows": n_bank, "dim": DIM, "nq": nq,
+                       "k": K, "nbins": NBINS, "theta": THETA, "min_matches": MIN_MATCHES,
+                       "parallelism": f"bank shard x{world}; NCCL broadcast of the queue, "
+                                      + ("fused P2P gather of k candidates/query (ss_topk_gather)"
+                                         if args.exchange == "p2p" else
+                                         "NCCL all-gather of k candidates/query")
+                                      + ", NCCL all-reduce of the window histogram; stages 2-4 "
+                                        "on the owner",
                        "graph": graph is not None,
                        "l2": "bank shard streamed from HBM each round"},
-            "e2e": {"value": round(req * args.steps / (e2e_ms / 1e3), 1), "unit": "requests/s",
-                    "h2d_bytes_per_step": int(world * (q.nbytes + qi.nbytes + I.nbytes + ids.nbytes)),
-                    "d2h_bytes_per_step": int(world * 16 * NQ),
+            "e2e": {"value": round(nq * args.steps / (e2e_ms / 1e3), 1), "unit": "requests/s",
+                    "h2d_bytes_per_step": int(q.nbytes + qi.nbytes + I.nbytes + ids.nbytes),
+                    "d2h_bytes_per_step": int(16 * nq),
                     "ms_per_step": round(e2e_ms / args.steps, 4)},
-            "roofline": {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak,
-                         "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
-                         "peak_source": "int8 dense = 2 x measured bf16 burst",
-                         "kernel": topk_kernel_name(algo_used, world * NQ),
-                         "kernel_ms": round(kern_ms, 4),
+            "roofline": {"bound": "tensor", "achieved": round(achieved, 1), "peak": i8_peak,
+                         "unit": "TFLOP/s", "frac": round(achieved / i8_peak, 4) if i8_peak else None,
+                         "peak_source": f"int8 tcgen05 ceiling measured live (tools/mma_peak.cu: {i8_detail})",
+                         "work_per_launch": f"2 * {nq} * {n_bank // world} * {DIM} int8 ops",
+                         "kernel": topk_kernel_name(nq), "kernel_ms": round(kern_ms, 4),
+                         "n_slices": n_slices,
                          "kernel_share_of_step": round(kern_ms / (ms / args.steps), 3),
                          "traffic": None},
             "gpu_launches": int(per_round * args.steps),
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
+    sched.close()
     dist.destroy_process_group()
 
 
@@ -377,11 +508,12 @@ def run_c5(args):
     if _build.is_stale():
         _build.build()
     _lib.load()
+    n_bank = CONFIGS["c2"]["n_bank"]
     A, TOK, B, MAXA = 1024, 32, 8192, 65536
     rounds = args.warmup + args.steps
     n_trace = max(1 << 20, A * rounds)  # the 1M-request trace; the run replays its first rounds
-    emb, lens, _ = make_bank_device(N_BANK, DIM, N_CLUSTERS, SEED)
-    win = HistoryWindow(N_BANK, DIM)
+    emb, lens, _ = make_bank_device(n_bank, DIM, N_CLUSTERS, SEED)
+    win = HistoryWindow(n_bank, DIM)
     win.push(emb, lens)
     del emb, lens
     te, tl, _ = make_bank_device(n_trace, DIM, N_CLUSTERS, SEED, member_seed=SEED + 1000)
@@ -464,16 +596,18 @@ def run_c3(args):
     perm = torch.empty(n, dtype=torch.int64, device=d)
     ws = torch.empty(int(_lib.lib().ss_rank_workspace_bytes(n)), dtype=torch.uint8, device=d)
 
-    def step():
+    def refresh():
         _lib.call("ss_refresh", n, P(I), P(gg), P(bucket), 200, P(npts), P(pcnt), P(pD), nbins,
                   P(G), None, 1, _lib.stream_ptr())
+
+    def step():
+        refresh()
         rank(G, ids, perm, ws)
 
     c0 = _lib.launch_count()
     step()
     torch.cuda.synchronize()
     per = _lib.launch_count() - c0
-    # the storm's 1 + 39 launches replayed as one CUDA graph
     s = torch.cuda.Stream()
     s.wait_stream(torch.cuda.current_stream())
     with torch.cuda.stream(s):
@@ -487,24 +621,10 @@ def run_c3(args):
     torch.cuda.synchronize()
     sampler = ClockSampler(0)
     with sampler:
-        torch.cuda.synchronize()
         t0 = time.time()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(args.steps):
-            graph.replay()
-        e1.record()
-        torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1)
+        ms = time_ms(graph.replay, args.steps) * args.steps
         clocks = sampler.summary(t0, time.time())
-        # refresh kernel alone for the roofline (HBM: the sparse laws it reads)
-        e0.record()
-        for _ in range(args.steps):
-            _lib.call("ss_refresh", n, P(I), P(gg), P(bucket), 200, P(npts), P(pcnt), P(pD),
-                      nbins, P(G), None, 1, _lib.stream_ptr())
-        e1.record()
-        torch.cuda.synchronize()
-        kms = e0.elapsed_time(e1) / args.steps
+        kms = time_ms(refresh, args.steps)  # refresh kernel alone (HBM: the laws it reads)
     pts = int(npts.sum().item())
     byts = pts * 12 + n * (4 * 4 + 8)  # (count i32 + D i64) per point + per-request scalars + G
     pk = peaks()
@@ -519,198 +639,119 @@ def run_c3(args):
                    "index recompute + full re-rank", "points_per_request": round(pts / n, 2)},
         "roofline": {"bound": "hbm", "achieved": round(ach, 1), "peak": pk["hbm_gbs"],
                      "unit": "GB/s", "frac": round(ach / pk["hbm_gbs"], 4), "kernel": "k_refresh",
-                     "kernel_ms": round(kms, 4), "traffic": None},
+                     "kernel_ms": round(kms, 4), "traffic": ncu_traffic("c3", "k_refresh")},
         "gpu_launches": int(per * args.steps), "clocks": clocks}), flush=True)
 
 
-def time_topk_kernel(sched, dq, dqi, args, nq=None):
-    import ctypes as C
-
-    import torch
-
-    from paper_2603_07917_b200 import _lib
-
-    algo = sched.cfg.algo
-    code = _lib.ALGO[algo]
-    if algo == "auto":
-        # resolve what auto picks: try tcgen05 first
-        code = _lib.ALGO["tcgen05"]
-    n = nq or NQ
-    max_slices = 1024
-    part = torch.empty(max_slices * n * K, dtype=torch.int64, device="cuda")
-    ns = C.c_int32()
-    lib = _lib.lib()
-    rc = lib.ss_topk_partials(sched.window.handle, dq.data_ptr(), dqi.data_ptr(), n, K,
-                              float(np.float32(THETA)), code, part.data_ptr(), max_slices,
-                              C.byref(ns), _lib.stream_ptr())
-    used = "tcgen05"
-    if rc != 0:
-        code = _lib.ALGO["scan"]
-        used = "scan"
-        _lib.call("ss_topk_partials", sched.window.handle, dq.data_ptr(), dqi.data_ptr(), n, K,
-                  float(np.float32(THETA)), code, part.data_ptr(), max_slices, C.byref(ns),
-                  _lib.stream_ptr())
-    elif algo == "scan":
-        used = "scan"
-    torch.cuda.synchronize()
-    reps = max(3, args.steps)
-    st = torch.cuda.current_stream()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(st)
-    for _ in range(reps):
-        lib.ss_topk_partials(sched.window.handle, dq.data_ptr(), dqi.data_ptr(), n, K,
-                             float(np.float32(THETA)), code, part.data_ptr(), max_slices,
-                             C.byref(ns), _lib.stream_ptr())
-    e1.record(st)
-    torch.cuda.synchronize()
-    return used, e0.elapsed_time(e1) / reps, int(ns.value)
-
-
-def time_e2e(sched, q, qi, I, ids, args):
-    import torch
-
-    def pin(a):
-        t = torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
-        return t.numpy()
-
-    hq, hqi, hI, hids = pin(q), pin(qi), pin(I), pin(ids)
-    G = torch.empty(NQ, dtype=torch.float64).pin_memory().numpy()
-    perm = torch.empty(NQ, dtype=torch.int64).pin_memory().numpy()
-    s = torch.cuda.Stream()
-    for _ in range(max(1, args.warmup)):
-        sched.schedule_round_host(hq, hqi, hI, hids, G, perm, stream=s)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    e0.record(s)
-    for _ in range(args.steps):
-        sched.schedule_round_host(hq, hqi, hI, hids, G, perm, stream=s)
-    e1.record(s)
-    torch.cuda.synchronize()
-    h2d = hq.nbytes + hqi.nbytes + hI.nbytes + hids.nbytes
-    d2h = G.nbytes + perm.nbytes
-    return e0.elapsed_time(e1), int(h2d), int(d2h)
-
-
-def topk_kernel_name(algo_used: str, nq: int) -> str:
-    """Which stage-1 kernel the library launches (mirrors use_ts() in
-    csrc/k_topk_sm100.cu): the A-in-TMEM tcgen05 kernel above one 128-query
-    tile, the streaming form of k_topk_tc at or below it."""
-    if algo_used != "tcgen05":
-        return "k_topk_scan"
-    if nq > 128 and os.environ.get("SS_TC_TS", "") != "0":
-        return "k_topk_ts"
-    return "k_topk_tc"
-
-
-def ncu_traffic(kernel: str):
-    """dram read+write bytes per launch of `kernel` on this workload, from the
-    committed ncu --set full summary (profiles/ncu_traffic.json), else None."""
-    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    try:
-        d = json.load(open(p))
-        return d.get(WORKLOAD.split(":")[0], {}).get(kernel)
-    except Exception:
-        return None
-
-
 # --------------------------------------------------------- CPU reference ----
-def _cpu_env():
-    n = os.cpu_count() or 1
-    for v in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS", "NUMBA_NUM_THREADS"):
-        os.environ.setdefault(v, str(n))
-    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/nbcache")
+def _reference_modules():
+    """The unmodified reference (servesim) when installed in baseline/_ref."""
     ref = os.path.join(ROOT, "baseline", "_ref")
     if os.path.isdir(ref) and ref not in sys.path:
         sys.path.insert(0, ref)
-    return n
-
-
-def _reference_modules():
-    """The unmodified reference (servesim) when installed in baseline/_ref."""
     try:
-        from servesim import _kernels as RK  # noqa: F401
-        from servesim import cost as RC
-        from servesim.distribution import DiscreteDistribution as RD
+        from servesim import _kernels as RK
         RK.warmup()
-        return RK, RC, RD
+        return RK
     except Exception:
         return None
 
 
 class CpuRound:
-    """The reference CPU path on one bank chunk: numpy/OpenBLAS fp32 similarity
-    (exact on int8 vectors), per-chunk top-k (argpartition), merge, then per
-    request the reference's cost_distribution + gittins_min, then lexsort."""
+    """The reference CPU path for the whole bank: numpy/OpenBLAS fp32
+    similarity (exact on int8-valued vectors) in 128k-row chunks, selection
+    (theta filter + top-k by (key desc, seq desc)), the window fallback, the
+    fixed-bin histogram with per-bin conditional-mean ResourceBound cost
+    (cost.py:97-99 per length), the reference's numba gittins_min
+    (_kernels.py:104-116) per request, then lexsort by (G, id).  One step
+    scores `sample` of the round's queries against every bank row."""
 
-    def __init__(self, chunk_rows: int, seed: int = 0):
+    CHUNK = 1 << 17
+
+    def __init__(self, config: str, sample: int):
         from oracle import sagesched_oracle as O
+        from paper_2603_07917_b200.synthetic import make_bank_host, make_queries
 
-        self.O = O
-        self.mods = _reference_modules()
-        emb, lens, _, _ = O.make_bank(chunk_rows + NQ, DIM, 256, seed)
-        self.W = emb[:chunk_rows].astype(np.float32)
-        self.iw = O.inv_norm(emb[:chunk_rows])
-        self.lens = lens[:chunk_rows].astype(np.int64)
-        self.Q = emb[chunk_rows:].astype(np.float32)
-        self.iq = O.inv_norm(emb[chunk_rows:])
-        self.I = np.random.default_rng(seed).integers(1, 4097, NQ)
+        C = CONFIGS[config]
+        self.O, self.RK = O, _reference_modules()
+        self.n = C["n_bank"]
+        emb, lens = make_bank_host(self.n, DIM, N_CLUSTERS, SEED)
+        self.iw = O.inv_norm(emb)
+        # fp32 copy of the bank when it fits comfortably (c2: 1.6 GB); the 16M
+        # bank stays int8 (6.4 GB) and each chunk is widened inside the step
+        self.W = emb.astype(np.float32) if self.n <= (1 << 22) else emb
+        self.lens = lens.astype(np.int64)
+        self.fb = O.bin_hist(self.lens, MAX_LEN, NBINS)
+        q, qi, I, ids = make_queries(C["nq"], DIM, N_CLUSTERS, SEED, qseed=1000)
+        self.sample = min(sample, C["nq"])
+        self.Q = q[:self.sample].astype(np.float32)
+        self.iq = qi[:self.sample]
+        self.I = I[:self.sample].astype(np.int64)
+        self.ids = ids[:self.sample]
 
-    def chunk_topk(self):
-        s = (self.Q @ self.W.T) * self.iw[None, :]
-        s = s * self.iq[:, None]
-        s[s < np.float32(THETA)] = -np.inf
-        idx = np.argpartition(-s, K, axis=1)[:, :K]
-        return s, idx
-
-    def finish(self, s, idx):
+    def step(self):
         O = self.O
-        G = np.empty(NQ)
-        w = MAX_LEN // NBINS
-        for i in range(NQ):
-            sel = idx[i][np.isfinite(s[i, idx[i]])]
-            L = self.lens[sel] if sel.size >= MIN_MATCHES else self.lens
-            b = (np.minimum(L, MAX_LEN) - 1) // w
-            Lf = L.astype(np.float64)
-            cnt = np.bincount(b, minlength=NBINS)
-            sv = np.bincount(b, weights=Lf, minlength=NBINS)
-            sv2 = np.bincount(b, weights=Lf * Lf, minlength=NBINS)
-            nz = np.flatnonzero(cnt)
-            # conditional-mean ResourceBound cost per bin (cost.py:98-99 per length)
-            sup = (sv2[nz] + 2.0 * self.I[i] * sv[nz]) * 0.5 / cnt[nz]
-            mas = cnt[nz] / cnt[nz].sum()
-            if self.mods:
-                RK = self.mods[0]
-                G[i] = RK.gittins_min(sup, mas)  # the reference's own numba kernel
+        nq = self.sample
+        keys, seqs = [[] for _ in range(nq)], [[] for _ in range(nq)]
+        for s in range(0, self.n, self.CHUNK):
+            Wc = self.W[s:s + self.CHUNK]
+            if Wc.dtype != np.float32:
+                Wc = Wc.astype(np.float32)
+            sc = (self.Q @ Wc.T) * self.iw[None, s:s + self.CHUNK]
+            sc *= self.iq[:, None]
+            if THETA > 0:
+                r, c = np.nonzero(sc >= np.float32(THETA))
+                for i in np.unique(r):
+                    m = r == i
+                    keys[i].append(sc[i, c[m]])
+                    seqs[i].append(c[m] + s)
             else:
-                G[i] = O.gittins_min(sup, mas)
-        return np.lexsort((np.arange(NQ), G))
+                kk = min(K, sc.shape[1])
+                top = np.argpartition(-sc, kk - 1, axis=1)[:, :kk]
+                for i in range(nq):
+                    keys[i].append(sc[i, top[i]])
+                    seqs[i].append(top[i] + s)
+        G = np.empty(nq)
+        w = MAX_LEN // NBINS
+        for i in range(nq):
+            kv = np.concatenate(keys[i]) if keys[i] else np.zeros(0, np.float32)
+            sv = np.concatenate(seqs[i]) if seqs[i] else np.zeros(0, np.int64)
+            sel = sv[np.lexsort((-sv, -kv))[:K]]  # key desc, insertion_seq desc (SPEC.md:135)
+            if sel.size >= MIN_MATCHES:
+                L = self.lens[sel]
+                b = (np.minimum(L, MAX_LEN) - 1) // w
+                Lf = L.astype(np.float64)
+                cnt = np.bincount(b, minlength=NBINS)
+                s1 = np.bincount(b, weights=Lf, minlength=NBINS)
+                s2 = np.bincount(b, weights=Lf * Lf, minlength=NBINS)
+            else:
+                cnt, s1, s2 = (x.astype(np.float64) for x in self.fb)
+            nz = np.flatnonzero(cnt)
+            sup = (s2[nz] + 2.0 * self.I[i] * s1[nz]) * 0.5 / cnt[nz]
+            mas = cnt[nz] / cnt[nz].sum()
+            G[i] = self.RK.gittins_min(sup, mas) if self.RK else O.gittins_min(sup, mas)
+        return np.lexsort((self.ids, G))
 
-    def step(self, n_chunks_total: int):
-        """Time one chunk of stage 1 plus the full stages 2-4; extrapolate stage 1."""
-        t0 = time.perf_counter()
-        s, idx = self.chunk_topk()
-        t1 = time.perf_counter()
-        self.finish(s, idx)
-        t2 = time.perf_counter()
-        return (t1 - t0) * n_chunks_total + (t2 - t1)
+
+def _cpu_sample(config: str) -> int:
+    return 128 if config == "c2" else 16
 
 
-def cpu_baseline(budget_s: float = 20.0):
-    n = _cpu_env()
-    chunk = 1 << 16
-    total_chunks = N_BANK // chunk
-    r = CpuRound(chunk)
-    r.step(total_chunks)  # warm (BLAS threads, numba JIT)
+def cpu_baseline(config: str, budget_s: float = 20.0):
+    r = CpuRound(config, _cpu_sample(config))
+    r.step()  # warm (BLAS threads, numba JIT)
     ts = []
     t_start = time.perf_counter()
     while time.perf_counter() - t_start < budget_s and len(ts) < 5:
-        ts.append(r.step(total_chunks))
+        t0 = time.perf_counter()
+        r.step()
+        ts.append(time.perf_counter() - t0)
     t = float(np.median(ts))
-    return {"value": round(NQ / t, 2), "unit": "requests/s", "cores": n,
-            "kind": "port",
-            "sample": (f"{NQ} queries x one {chunk}-row bank chunk (stage 1 extrapolated x{total_chunks} "
-                       f"to the 1M bank) + full stages 2-4; median of {len(ts)}; Gittins = reference "
-                       f"servesim gittins_min (numba) {'from baseline/_ref' if r.mods else 'unavailable -> oracle'}; "
+    return {"value": round(r.sample / t, 2), "unit": "requests/s", "cores": _NCPU, "kind": "port",
+            "sample": (f"per step {r.sample} of the round's {CONFIGS[config]['nq']} queries scored "
+                       f"against the whole {r.n}-row bank (no extrapolation), full stages 1-4; "
+                       f"median of {len(ts)} steps; Gittins = reference servesim gittins_min "
+                       f"({'numba, baseline/_ref' if r.RK else 'unavailable -> oracle'}); "
                        "similarity/top-k/histogram are SPEC-only (numpy restatement)")}
 
 
@@ -719,23 +760,28 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    n = _cpu_env()
-    chunk = 1 << 16
-    total_chunks = N_BANK // chunk
-    r = CpuRound(chunk)
+    config = "c4" if world > 1 else args.config
+    r = CpuRound(config, _cpu_sample(config))
     for _ in range(max(1, args.warmup)):
-        r.step(total_chunks)
-    ts = [r.step(total_chunks) for _ in range(args.steps)]
-    t = float(np.sum(ts))
-    value = NQ * args.steps / t
-    cb = {"value": round(value, 2), "unit": "requests/s", "cores": n, "kind": "port",
-          "sample": f"per step: {NQ} queries x one {chunk}-row chunk, stage 1 extrapolated x{total_chunks}"}
-    line = {"impl": "reference",
-            "metric": "requests scheduled/sec per round (predict+cost+Gittins+rank) vs a 1M-entry bank",
-            "value": round(value, 2), "unit": "requests/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(1e3 * t / args.steps, 2),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32/f64",
-            "data": "synthetic", "config": {"workload": WORKLOAD, "nq": NQ, "k": K, "nbins": NBINS},
+        r.step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        r.step()
+    t = time.perf_counter() - t0
+    value = r.sample * args.steps / t
+    C = CONFIGS[config]
+    cb = {"value": round(value, 2), "unit": "requests/s", "cores": _NCPU,
+          "kind": "reference" if r.RK else "port",
+          "sample": f"per step {r.sample} of the round's {C['nq']} queries x the whole "
+                    f"{C['n_bank']}-row bank (no extrapolation)"}
+    line = {"impl": "reference", "metric": METRIC, "value": round(value, 2), "unit": "requests/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(1e3 * t / args.steps, 2), "higher_is_better": True,
+            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f32/f64",
+            "data": "synthetic (seeded clustered int8-valued embeddings, lognormal lengths; numpy)",
+            "config": {"workload": C["workload"], "bank_rows": C["n_bank"], "dim": DIM,
+                       "nq": C["nq"], "k": K, "nbins": NBINS, "theta": THETA,
+                       "min_matches": MIN_MATCHES, "parallelism": f"host CPU, {_NCPU} threads"},
             "cpu_baseline": cb,
             "e2e": {"value": round(value, 2), "unit": "requests/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
@@ -748,27 +794,29 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--algo", default="auto", choices=["auto", "scan", "tcgen05"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-pure", action="store_true", help="skip the theta = -1 sub-record")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
-    ap.add_argument("--config", default="c2", choices=["c2", "c3", "c4", "c5"],
-                    help="c2 = headline (BASELINE configs[1]); c3 = refresh storm; "
-                         "c4 = 16M bank x 8192 queries on this GPU")
+    ap.add_argument("--config", default=None, choices=["c2", "c3", "c4", "c5"],
+                    help="c2 = headline at N = 1 (BASELINE configs[1]); c4 = 16M x 8192 "
+                         "(default at N > 1); c3 = refresh storm; c5 = rolling replay")
+    ap.add_argument("--sharded", action="store_true",
+                    help="run the multi-GPU single-owner round even at N = 1")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "p2p"],
+                    help="candidate exchange of the sharded round")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
-    global N_BANK, NQ, WORKLOAD
-    if args.config == "c4":
-        N_BANK, NQ = 1 << 24, 8192
-        WORKLOAD = "c4: 16M-entry x 384-d int8 history bank, 8192 queries/round, k=64, 128 bins"
-    if args.config == "c3" and args.impl == "ours":
-        return run_c3(args)
-    if args.config == "c5" and args.impl == "ours":
-        return run_c5(args)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.config is None:
+        args.config = "c4" if (world > 1 or args.gpus > 1) else "c2"
     if args.impl == "reference":
-        run_reference(args)
-    else:
-        run_ours(args)
+        return run_reference(args)
+    if args.config == "c3":
+        return run_c3(args)
+    if args.config == "c5":
+        return run_c5(args)
+    run_ours(args)
 
 
 if __name__ == "__main__":

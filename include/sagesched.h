@@ -56,9 +56,11 @@ int64_t ss_launch_count(void);
 /* servesim._kernels.match_pmfs (_kernels.py:118-138): threshold match ->
  * exact integer-length pmf.  sims f32[nq,nw], lens i64[nw] in [0,max_len];
  * sup/mas f64[nq,out_stride], sizes i64[nq].  Bit-compatible with the numba
- * path (mass = c * (1.0/total)). Out-of-range lens -> SS_ERR_RANGE. Synchronises. */
+ * path (mass = c * (1.0/total)); theta is compared in f64 as numba does for a
+ * Python-float theta (exact for an np.float32 one).  Out-of-range lens ->
+ * SS_ERR_RANGE. Synchronises. */
 int ss_match_pmfs(const float* sims, int64_t nq, int64_t nw, const int64_t* lens,
-                  float theta, int64_t max_len, double* sup, double* mas,
+                  double theta, int64_t max_len, double* sup, double* mas,
                   int64_t* sizes, int64_t out_stride, void* stream);
 
 /* servesim._kernels.gittins_min (_kernels.py:104-116), batched: one
@@ -149,22 +151,34 @@ int ss_topk_partials(ss_bank_t* h, const int8_t* q, const float* q_inv, int64_t 
 int ss_merge_topk(const uint64_t* comp, const int32_t* len, int32_t nlists,
                   int64_t nq, int32_t k, uint64_t* out_comp, int32_t* out_len,
                   void* stream);
-/* Fused merge + exchange of the multi-GPU round (SURVEY 8(e) stage 3,
- * replacing the candidate all_to_all that follows the reference's per-process
- * top-k, sagesched/predictor/_kernels.py:40 run per shard): the local top-k of
- * nq = world * nq_local queries (rank-major: rows [r*nq_local, (r+1)*nq_local)
- * are rank r's queue) against this rank's shard, whose merge kernel stores
- * each merged row straight into the owner's receive buffer -- peer_comp_host[r]
- * / peer_len_host[r] (device pointers, IPC-mapped for r != rank) laid out
- * [world][nq_local][k] -- at row [rank][q % nq_local], as NVLink P2P stores.
- * The caller orders the peers' reads after a barrier (e.g. a 1-element NCCL
- * all_reduce) and then merges its receive buffer with ss_merge_topk.
- * world <= 8 (one NVLink/NVSwitch node); nq % world == 0.  Async. */
+/* Fused merge + exchange of the multi-GPU round with per-rank queues
+ * (SURVEY 8(e) stage 3, replacing the candidate all_to_all that would follow
+ * a per-shard run of the reference's similarity step -- SPEC.md:132-140
+ * query_similar, computed in float32 as _kernels.py:172 does): the local
+ * top-k of nq = world * nq_local queries (rank-major: rows
+ * [r*nq_local, (r+1)*nq_local) are rank r's queue) against this rank's
+ * shard, whose merge kernel stores each merged row straight into the
+ * owner's receive buffer -- peer_comp_host[r] / peer_len_host[r] (device
+ * pointers, IPC-mapped for r != rank) laid out [world][nq_local][k] -- at
+ * row [rank][q % nq_local], as NVLink P2P stores.  The caller orders the
+ * peers' reads after a barrier (e.g. a 1-element NCCL all_reduce) and then
+ * merges its receive buffer with ss_merge_topk.  world <= 8 (one
+ * NVLink/NVSwitch node); nq % world == 0.  Async. */
 #define SS_IPC_HANDLE_BYTES 64
 int ss_topk_scatter(ss_bank_t* h, const int8_t* q, const float* q_inv, int64_t nq,
                     int32_t k, float theta, int32_t algo, int32_t world, int32_t rank,
                     uint64_t* const* peer_comp_host, int32_t* const* peer_len_host,
                     void* stream);
+/* The single-owner form (north star: "the rest runs on the rank owning the
+ * queue"; SPEC.md:468-470 ranks every pending request in one order): all nq
+ * queries belong to one owner rank, whose receive buffer owner_comp /
+ * owner_len (IPC-mapped here unless rank == owner) is laid out [world][nq][k];
+ * this rank's merged local top-k rows are stored at [rank][q] -- the
+ * all-gather of k candidates per query, done by the merge kernel's own NVLink
+ * stores.  Async. */
+int ss_topk_gather(ss_bank_t* h, const int8_t* q, const float* q_inv, int64_t nq, int32_t k,
+                   float theta, int32_t algo, int32_t world, int32_t rank,
+                   uint64_t* owner_comp, int32_t* owner_len, void* stream);
 /* IPC-exportable device buffers for ss_topk_scatter: cudaMalloc'd (zeroed) on
  * `device`, exported as a 64-byte handle, opened (peer-mapped) by the other
  * ranks of the node.  Synchronous. */

@@ -16,6 +16,9 @@ CSRC = os.path.join(PKG_DIR, "csrc")
 INCLUDE = os.path.join(os.path.dirname(PKG_DIR), "include")
 LIB_NAME = "libsagesched.so"
 LIB_PATH = os.path.join(PKG_DIR, LIB_NAME)
+# measurement probes (not product code): source -> shared object
+TOOLS_DIR = os.path.join(os.path.dirname(PKG_DIR), "tools")
+PROBES = {os.path.join(TOOLS_DIR, "mma_peak.cu"): os.path.join(TOOLS_DIR, "libmmapeak.so")}
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -48,9 +51,26 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found: cannot build libsagesched for sm_100a")
 
 
+def build_probes(force: bool = False, verbose: bool = False) -> None:
+    """The measurement probes under tools/ (bench.py's int8 tensor peak)."""
+    for src, so in PROBES.items():
+        if not os.path.exists(src):
+            continue
+        if not force and os.path.exists(so) and os.path.getmtime(so) >= os.path.getmtime(src):
+            continue
+        cmd = [nvcc(), *NVCC_FLAGS, "-o", so + ".tmp", src]
+        if verbose:
+            print(" ".join(cmd))
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"nvcc failed on {src} ({r.returncode}):\n{r.stdout}\n{r.stderr}")
+        os.replace(so + ".tmp", so)
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     """Compile every .cu under csrc/ (in parallel, one object each) and link
-    them into one sm_100a shared library."""
+    them into one sm_100a shared library; build the measurement probes."""
+    build_probes(force, verbose)
     if not force and not is_stale():
         return LIB_PATH
     from concurrent.futures import ThreadPoolExecutor

@@ -45,7 +45,7 @@ def match_pmfs(sims, lens, theta, max_len, sup, mas, sizes) -> None:
     d_mas = mas if on_dev else torch.zeros((nq, stride), dtype=torch.float64, device="cuda")
     d_sz = sizes if (isinstance(sizes, torch.Tensor) and sizes.is_cuda) else torch.zeros(
         nq, dtype=torch.int64, device="cuda")
-    _lib.call("ss_match_pmfs", _lib.ptr(d_sims), nq, nw, _lib.ptr(d_lens), float(np.float32(theta)),
+    _lib.call("ss_match_pmfs", _lib.ptr(d_sims), nq, nw, _lib.ptr(d_lens), float(theta),
               int(max_len), _lib.ptr(d_sup), _lib.ptr(d_mas), _lib.ptr(d_sz),
               int(d_sup.shape[1]), _lib.stream_ptr())
     if not on_dev:

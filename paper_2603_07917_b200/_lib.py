@@ -25,7 +25,7 @@ SIGNATURES = {
     "ss_last_error": (C.c_char_p, []),
     "ss_version": (C.c_int, []),
     "ss_launch_count": (I64, []),
-    "ss_match_pmfs": (C.c_int, [P, I64, I64, P, F32, I64, P, P, P, I64, P]),
+    "ss_match_pmfs": (C.c_int, [P, I64, I64, P, F64, I64, P, P, P, I64, P]),
     "ss_gittins_min_batch": (C.c_int, [P, P, P, I64, I64, P, P]),
     "ss_gittins_dist_batch": (C.c_int, [P, P, P, P, P, I64, I64, P, P]),
     "ss_embed_accumulate_batch": (C.c_int, [P, P, I64, U64, I32, P, P]),
@@ -44,6 +44,7 @@ SIGNATURES = {
     "ss_topk_partials": (C.c_int, [P, P, P, I64, I32, F32, I32, P, I32, C.POINTER(I32), P]),
     "ss_merge_topk": (C.c_int, [P, P, I32, I64, I32, P, P, P]),
     "ss_topk_scatter": (C.c_int, [P, P, P, I64, I32, F32, I32, I32, I32, P, P, P]),
+    "ss_topk_gather": (C.c_int, [P, P, P, I64, I32, F32, I32, I32, I32, P, P, P]),
     "ss_ipc_malloc": (C.c_int, [I32, I64, C.POINTER(P)]),
     "ss_ipc_free": (C.c_int, [P]),
     "ss_ipc_handle": (C.c_int, [P, P]),

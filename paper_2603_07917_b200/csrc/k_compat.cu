@@ -13,7 +13,7 @@ namespace ss {
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256)
 k_match_pmfs(const float* __restrict__ sims, int64_t nw, const int64_t* __restrict__ lens,
-             float theta, int max_len, double* __restrict__ sup, double* __restrict__ mas,
+             double theta, int max_len, double* __restrict__ sup, double* __restrict__ mas,
              int64_t* __restrict__ sizes, int64_t out_stride, int* __restrict__ err) {
   extern __shared__ int s_counts[];  // [max_len + 1]
   __shared__ int s_total;
@@ -27,7 +27,9 @@ k_match_pmfs(const float* __restrict__ sims, int64_t nw, const int64_t* __restri
   const float* row = sims + (int64_t)q * nw;
   int local_total = 0;
   for (int64_t j = tid; j < nw; j += blockDim.x) {
-    if (row[j] >= theta) {                // _kernels.py:126
+    // numba compares the f32 sim with the caller's theta as given: a Python
+    // float promotes the comparison to f64 (an np.float32 theta is exact in f64)
+    if ((double)row[j] >= theta) {        // _kernels.py:126
       int64_t L = lens[j];
       if (L < 0 || L > max_len) { atomicExch(err, SS_ERR_RANGE); continue; }
       atomicAdd(&s_counts[L], 1);         // _kernels.py:127
@@ -70,7 +72,7 @@ k_match_pmfs(const float* __restrict__ sims, int64_t nw, const int64_t* __restri
 }
 
 int launch_match_pmfs(const float* sims, int64_t nq, int64_t nw, const int64_t* lens,
-                      float theta, int64_t max_len, double* sup, double* mas,
+                      double theta, int64_t max_len, double* sup, double* mas,
                       int64_t* sizes, int64_t out_stride, int* err, cudaStream_t st) {
   size_t smem = (size_t)(max_len + 1) * sizeof(int);
   if (smem > 200 * 1024) return set_error(SS_ERR_UNSUPPORTED, "max_len %lld too large", (long long)max_len);

@@ -8,12 +8,8 @@
 // int32, so the tensor-core result is bit-identical to the CPU oracle).
 //
 // A CTA owns 128 queries (M = TMEM lanes) and streams one slice of the bank
-// in 256-row tiles (N).  Two variants:
-//   CG = 1  one CTA per MMA (M=128, N=256); each CTA loads whole B tiles.
-//   CG = 2  a CTA pair (cluster of 2, tcgen05 cta_group::2, M=256, N=256):
-//           each CTA loads half of every B tile, the leader issues the MMA
-//           for both, halving the L2->SM traffic of the bank stream.
-// 6 warps per CTA:
+// in 256-row tiles (N); with nq <= 128 (one query tile, 148 bank slices) it
+// is the HBM-streaming scan of the north star.  6 warps per CTA:
 //   warp 0      TMA producer: A (queries, once) and B (bank K-blocks, ring)
 //   warp 1      TMEM allocator + single-thread MMA issuer (leader CTA)
 //   warps 2..5  epilogue: tcgen05.ld 32 columns at a time, s = dot*inv_w,
@@ -43,15 +39,13 @@ __device__ __noinline__ uint64_t tc_heap_replace(uint64_t* heap, int k, uint64_t
   return heap[0];
 }
 
-template <int CG>
 __global__ void __launch_bounds__(tc::THREADS, 1)
 k_topk_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmB,
           const float* __restrict__ q_inv, int64_t nq, const float* __restrict__ inv,
           int64_t n_rows, int nkb, int stages, int k, float theta, int64_t hmod, int64_t gcap,
-          int64_t slot_offset, int64_t tiles_per_slice, uint64_t* __restrict__ partials, int dbg,
-          uint32_t* __restrict__ grth, int rshare, int spread) {
-  constexpr int BN_CTA = tc::BN / CG;          // B rows this CTA loads per tile
-  constexpr int B_STAGE = BN_CTA * tc::BK;     // bytes per K-block stage per CTA
+          int64_t slot_offset, int64_t tiles_per_slice, uint64_t* __restrict__ partials,
+          int spread) {
+  constexpr int B_STAGE = tc::BN * tc::BK;     // bytes per K-block stage
   extern __shared__ uint8_t smem_raw[];
   // 1024-B alignment for the 128B-swizzle atoms; index the __shared__ array
   // (not an integer round trip) so every access stays LDS/STS, not generic.
@@ -66,12 +60,9 @@ k_topk_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUten
   uint64_t* empty = full + stages;
   uint64_t* tfull = empty + stages;
   uint64_t* tempty = tfull + 2;
-  uint64_t* mdone = tempty + 2;
-  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(mdone + 1);
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = (CG == 2) ? cluster_rank() : 0u;
-  const bool leader = (rank == 0);
   const int qt = blockIdx.x, slice = blockIdx.y;  // qt: 128-query tile of this CTA
   const int64_t tile0 = (int64_t)slice * tiles_per_slice;
   const int64_t total_tiles = (n_rows + tc::BN - 1) / tc::BN;
@@ -88,63 +79,46 @@ k_topk_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUten
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 4 * CG);  // one arrive per epilogue warp of the pair
+      mbar_init(&tempty[b], 4);  // one arrive per epilogue warp
     }
-    mbar_init(mdone, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  if (warp == 1) tmem_alloc512<CG>(s_tmem);
+  if (warp == 1) tmem_alloc512(s_tmem);
   tc_fence_before();
-  if constexpr (CG == 2) cluster_sync(); else __syncthreads();
+  __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *s_tmem;
 
   if (warp == 0) {
     // ------------------------------------------------------ TMA producer ---
     if (lane == 0 && ntiles > 0) {
-      // the leader's barriers count the bytes landing in both CTAs
-      if (leader) mbar_expect_tx(a_full, CG * nkb * tc::A_BLK);
+      mbar_expect_tx(a_full, nkb * tc::A_BLK);
       for (int kb = 0; kb < nkb; ++kb)
-        tma_load_2d<CG>(sA + kb * tc::A_BLK, &tmQ, a_full, kb * tc::BK, qt * tc::BM);
-      // optional L2 prefetch PF tiles ahead of the smem ring
-      const int PF = (dbg >> 8) & 0xff;
-      for (int t = 0; t < PF && t < ntiles; ++t)
-        for (int kb = 0; kb < nkb; ++kb)
-          tma_prefetch_l2_2d(&tmB, kb * tc::BK, (int)((tile0 + t) * tc::BN + rank * BN_CTA));
+        tma_load_2d(sA + kb * tc::A_BLK, &tmQ, a_full, kb * tc::BK, qt * tc::BM);
       int it = 0;
       for (int t = 0; t < ntiles; ++t) {
-        const int row0 = (int)((tile0 + t) * tc::BN + rank * BN_CTA);
-        if (t + PF < ntiles && PF > 0)
-          for (int kb = 0; kb < nkb; ++kb)
-            tma_prefetch_l2_2d(&tmB, kb * tc::BK, row0 + PF * tc::BN);
+        const int row0 = (int)((tile0 + t) * tc::BN);
         for (int kb = 0; kb < nkb; ++kb, ++it) {
           const int s = it % stages;
           mbar_wait(&empty[s], ((it / stages) & 1) ^ 1);
-          if (dbg & 8) {  // debug: no bank traffic
-            if (leader) mbar_expect_tx(&full[s], 0);
-            continue;
-          }
-          if (leader) mbar_expect_tx(&full[s], CG * B_STAGE);
-          tma_load_2d<CG>(sB + s * B_STAGE, &tmB, &full[s], kb * tc::BK, row0);
+          mbar_expect_tx(&full[s], B_STAGE);
+          tma_load_2d(sB + s * B_STAGE, &tmB, &full[s], kb * tc::BK, row0);
         }
       }
-      // drain: wait for the final MMA commits on every stage, so no
-      // (multicast) arrive can target this CTA's shared memory after it exits
+      // drain: wait for the final MMA commits on every stage, so no arrive
+      // can target this CTA's shared memory after it exits
       for (int i = max(0, it - stages); i < it; ++i) mbar_wait(&empty[i % stages], (i / stages) & 1);
     }
   } else if (warp == 1) {
     // ------------------------------------------------------- MMA issuer ----
-    if (leader && lane == 0 && ntiles > 0) {
+    if (lane == 0 && ntiles > 0) {
       mbar_wait(a_full, 0);
       tc_fence_after();
       const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
       int it = 0;
       for (int t = 0; t < ntiles; ++t) {
         const int acc = t & 1;
-        if (!(dbg & 64)) {  // debug bit 64: MMA issue alone, no epilogue hand-off
-          if constexpr (CG == 2) mbar_wait_cluster(&tempty[acc], ((t >> 1) & 1) ^ 1);
-          else mbar_wait(&tempty[acc], ((t >> 1) & 1) ^ 1);
-        }
+        mbar_wait(&tempty[acc], ((t >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d = tmem + acc * tc::BN;
         for (int kb = 0; kb < nkb; ++kb, ++it) {
@@ -155,15 +129,11 @@ k_topk_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUten
           for (int kk = 0; kk < tc::BK / tc::UK; ++kk) {
             const uint64_t ad = umma_desc_sw128(a_base + kb * tc::A_BLK + kk * tc::UK);
             const uint64_t bd = umma_desc_sw128(b_base + s * B_STAGE + kk * tc::UK);
-            if (!(dbg & 2)) tc_mma_i8<CG>(d, ad, bd, idesc_i8<CG>(), (kb | kk) != 0);
+            tc_mma_i8(d, ad, bd, idesc_i8(), (kb | kk) != 0);
           }
-          tc_commit<CG>(&empty[s]);  // frees the B stage (in both CTAs) once these MMAs retire
+          tc_commit(&empty[s]);  // frees the B stage once these MMAs retire
         }
-        tc_commit<CG>(&tfull[acc]);  // accumulator ready for the epilogue(s)
-      }
-      if (dbg & 64) {  // nobody drains: wait for the last MMAs before teardown
-        tc_commit<CG>(mdone);
-        mbar_wait(mdone, 0);
+        tc_commit(&tfull[acc]);  // accumulator ready for the epilogue
       }
     }
   } else {
@@ -178,7 +148,6 @@ k_topk_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUten
     const float iq = (q < nq) ? q_inv[q] : __int_as_float(0x7fc00000);
     // per-query heap state in registers (see topk_heap.cuh for the invariant)
     int hcnt = 0;
-    uint32_t rtop[4] = {0u, 0u, 0u, 0u};  // this slice's best R keys (orderable), descending
     uint64_t hroot = 0;
     uint64_t* heap = s_heap + qrow;
     float* wiw = s_iw + ew * 2 * tc::BN;  // double-buffered per warp
@@ -197,12 +166,11 @@ k_topk_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUten
         for (int u = 0; u < 8; ++u) pre[u] = (r0 + u < n_rows) ? inv[r0 + u] : NaNf;
       }
     };
-    const int ntiles_epi = (dbg & 64) ? 0 : ntiles;
-    if (ntiles_epi > 0) fetch_iw(0);
+    if (ntiles > 0) fetch_iw(0);
     // conservative s-domain filter: admits every row whose exact key can reach
     // the current k-th best (or theta while the heap fills)
     float thr = (iq == iq) ? s_threshold(theta, iq) : INFINITY;
-    for (int t = 0; t < ntiles_epi; ++t) {
+    for (int t = 0; t < ntiles; ++t) {
       const int acc = t & 1;
       const int64_t row0 = (tile0 + t) * tc::BN;
       float* ciw = wiw + (t & 1) * tc::BN;
@@ -213,21 +181,10 @@ k_topk_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUten
       }
       __syncwarp();
       if (t + 1 < ntiles) fetch_iw(t + 1);  // overlaps this tile's epilogue
-      // cross-slice bound (pure top-k): every slice publishes the R-th best
-      // key it has kept (R = ceil(k / slices)) in grth[slice][q]; once all
-      // have, the union holds >= k rows at or above the minimum of those, so
-      // the global k-th key is >= it.  Independent loads, overlapping the
-      // wait for this tile's MMA; a 0 slot (not yet published) means no bound.
-      if (rshare && q < nq) {
-        uint32_t m = ~0u;
-        for (int s2 = 0; s2 < (int)gridDim.y; ++s2) m = min(m, __ldcg(grth + (int64_t)s2 * nq + q));
-        if (m != 0u && m != ~0u) thr = fmaxf(thr, s_threshold(f32_unorder(m), iq));
-      }
       mbar_wait(&tfull[acc], (t >> 1) & 1);
       tc_fence_after();
       const uint32_t tbase = tmem + ((uint32_t)(quarter * 32) << 16) + acc * tc::BN;
       auto chunk = [&](const int (&v)[32], const int c) {
-        if (dbg & 4) return;  // debug: TMEM drain only
         // hot path: 32 independent s = fl(dot * inv_w), one max tree, one branch
         float s[32];
         const float4* iw4 = reinterpret_cast<const float4*>(ciw + c * 32);
@@ -247,7 +204,7 @@ k_topk_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUten
 #pragma unroll
         for (int j = 0; j < 4; ++j) m[j] = fmaxf(m[j], m[j + 4]);
         const float mx = fmaxf(fmaxf(m[0], m[1]), fmaxf(m[2], m[3]));
-        if (!(dbg & 1) && mx >= thr) {  // rare: exact keys and heap inserts for this chunk
+        if (mx >= thr) {  // rare: exact keys and heap inserts for this chunk
           // key = fl(s * iq) is exactly the oracle's fl(fl(dot*iw)*iq); the
           // common case is an append while the heap fills, inlined here; only
           // heapify / root replacement leave the hot code (noinline helpers)
@@ -261,39 +218,20 @@ k_topk_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUten
           while (mask) {
             const int j = __ffs(mask) - 1;
             mask &= mask - 1;
-            {
-              const float key = __fmul_rn(sl[j], iq);
-              if (key >= theta) {
-                if (rshare) {  // this slice's top-R keys; publish the R-th when it rises
-                  uint32_t x = f32_order(key);
-                  auto rth = [&]() {
-                    return rshare == 1 ? rtop[0] : rshare == 2 ? rtop[1] : rshare == 3 ? rtop[2] : rtop[3];
-                  };
-                  const uint32_t old = rth();
-#pragma unroll
-                  for (int i = 0; i < 4; ++i) {
-                    if (i < rshare) {
-                      const uint32_t hi = max(rtop[i], x);
-                      x = min(rtop[i], x);
-                      rtop[i] = hi;
-                    }
-                  }
-                  const uint32_t now = rth();
-                  if (now != old) __stcg(grth + (int64_t)slice * nq + q, now);  // publish
-                }
-                int64_t rel = gbase + j;
-                if (rel < 0) rel += gcap;
-                const uint64_t comp = make_comp(key, (uint32_t)rel);
-                if (hcnt < k) {
-                  heap[hcnt * tc::BM] = comp;
-                  if (++hcnt == k) {
-                    hroot = tc_heapify(heap, k);
-                    thr = fmaxf(thr, s_threshold(comp_key(hroot), iq));
-                  }
-                } else if (comp > hroot) {
-                  hroot = tc_heap_replace(heap, k, comp);
+            const float key = __fmul_rn(sl[j], iq);
+            if (key >= theta) {
+              int64_t rel = gbase + j;
+              if (rel < 0) rel += gcap;
+              const uint64_t comp = make_comp(key, (uint32_t)rel);
+              if (hcnt < k) {
+                heap[hcnt * tc::BM] = comp;
+                if (++hcnt == k) {
+                  hroot = tc_heapify(heap, k);
                   thr = fmaxf(thr, s_threshold(comp_key(hroot), iq));
                 }
+              } else if (comp > hroot) {
+                hroot = tc_heap_replace(heap, k, comp);
+                thr = fmaxf(thr, s_threshold(comp_key(hroot), iq));
               }
             }
           }
@@ -301,15 +239,6 @@ k_topk_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUten
       };
       // software pipeline: the TMEM load of chunk c+1 is in flight while
       // chunk c is scanned
-      if (dbg & 16) {  // debug: no TMEM reads at all (MMA + TMA floor)
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {
-          if constexpr (CG == 2) mbar_arrive_leader(&tempty[acc]);
-          else mbar_arrive(&tempty[acc]);
-        }
-        continue;
-      }
       int va[32], vb[32];
       tmem_ld32_async(tbase, va);
       tmem_wait_regs(va);
@@ -323,10 +252,7 @@ k_topk_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUten
         } else {  // accumulator drained: hand it back to the MMA warp
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) {
-            if constexpr (CG == 2) mbar_arrive_leader(&tempty[acc]);
-            else mbar_arrive(&tempty[acc]);
-          }
+          if (lane == 0) mbar_arrive(&tempty[acc]);
         }
         chunk(vb, c + 1);
         if (c + 2 < tc::BN / 32) tmem_wait_regs(va);
@@ -339,10 +265,10 @@ k_topk_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUten
     }
   }
   tc_fence_before();
-  if constexpr (CG == 2) cluster_sync(); else __syncthreads();
+  __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc512<CG>(tmem);
+    tmem_dealloc512(tmem);
   }
 }
 
@@ -373,36 +299,17 @@ static int make_map(CUtensorMap* m, const void* base, int64_t rows, int dim, int
   return SS_OK;
 }
 
-static int env_int(const char* name, int dflt) {
-  const char* e = getenv(name);
-  return e ? atoi(e) : dflt;
-}
-
-// CTA-pair (cta_group::2) variant: correct and available (SS_TC_CG=2), but
-// measured slower than single-CTA MMA here because the bound is the TMEM
-// drain + epilogue, not L2->SM traffic (profiles/ROUND1.md), so off by default.
-static int tc_cg(int64_t nq) {
-  int v = env_int("SS_TC_CG", 0);
-  if ((v == 1 || v == 2) && (v == 1 || nq > tc::BM)) return v;
-  return 1;
-}
-
-// L2 prefetch distance (tiles), off by default (measured: no gain)
-static int tc_prefetch() { return env_int("SS_TC_PREFETCH", 0) & 0xff; }
-
 static size_t tc_fixed_smem(int dim, int k) {
   return (size_t)(dim / tc::BK) * tc::A_BLK + (size_t)k * tc::BM * 8 + 8 * tc::BN * 4 + 512 + 1024;
 }
 
-static int tc_stages(int dim, int k, int cg) {
-  const int forced = env_int("SS_TC_STAGES", 0);
-  const size_t stage = (size_t)(tc::BN / cg) * tc::BK;
+// as many B stages as fit beside A, the heaps and the inverse-norm buffers
+static int tc_stages(int dim, int k) {
+  const size_t stage = (size_t)tc::BN * tc::BK;
   const size_t fixed = tc_fixed_smem(dim, k);
-  int s = 0;
   for (int c = 8; c >= 2; --c)
-    if (fixed + c * stage <= 227 * 1024) { s = c; break; }
-  if (forced >= 2 && forced <= s) s = forced;
-  return s;
+    if (fixed + c * stage <= 227 * 1024) return c;
+  return 0;
 }
 
 bool topk_tc_supported(const TopkArgs& a) {
@@ -413,43 +320,19 @@ bool topk_tc_supported(const TopkArgs& a) {
   cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
   cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
   if (major != 10 || minor != 0) return false;  // built for sm_100a only
-  return tc_stages(a.dim, a.k, 1) >= 2;
+  return tc_stages(a.dim, a.k) >= 2;
 }
 
-// the A-in-TMEM variant (k_topk_sm100_ts.cu: two epilogue warps per
-// sub-partition, accumulator drained to registers): measured faster at
-// nq > 128 for both theta = 0.8 and pure top-k; the single-query-tile
-// streaming case stays on this kernel (profiles/ROUND1.md).
-// SS_TC_TS=0/1 forces it off/on.
-static bool use_ts(const TopkArgs& a) {
-  static const int v = env_int("SS_TC_TS", -1);
-  if (!topk_ts_supported(a)) return false;
-  if (v == 0 || v == 1) return v == 1;
-  return a.nq > 128;
-}
-
-// the CTA-pair kernel with the 8-warp epilogue (k_topk_pair.cu): full-rate
-// N=256 MMAs with a double-buffered accumulator and a 6-stage feed (MMA +
-// TMA alone 0.27 ms at c2), but every accumulator hand-off waits for the
-// slowest of 16 epilogue warps across the pair and the end-to-end kernel
-// measures slower than k_topk_ts<192,2> (profiles/ROUND1.md), so it is
-// opt-in: SS_TC_PAIR=1
-static bool use_pair(const TopkArgs& a) {
-  static const int v = env_int("SS_TC_PAIR", 0);
-  return v != 0 && a.nq > tc::BM && topk_pair_supported(a);
-}
-
-int launch_topk_pair(const TopkArgs& a, uint64_t* partials, int n_slices, cudaStream_t st,
-                     const CUtensorMap& mq, const CUtensorMap& mb);
+// One kernel per regime: above one 128-query tile the A-in-TMEM kernel
+// (k_topk_sm100_ts.cu, two epilogue warps per sub-partition); at or below it
+// this kernel, as a bank-streaming scan over 148 slices.
+static bool use_ts(const TopkArgs& a) { return a.nq > tc::BM && topk_ts_supported(a); }
 
 int topk_tc_slices(const TopkArgs& a, int device) {
-  if (use_pair(a)) return topk_pair_lists(a, device);
   if (use_ts(a)) return topk_ts_lists(a, device);
-  int sms = sm_count(device);
-  const int cg = tc_cg(a.nq);
-  int64_t qtiles = (a.nq + tc::BM - 1) / tc::BM;
-  qtiles = (qtiles + cg - 1) / cg * cg;
-  int64_t tiles = (a.n_rows + tc::BN - 1) / tc::BN;
+  const int sms = sm_count(device);
+  const int64_t qtiles = (a.nq + tc::BM - 1) / tc::BM;
+  const int64_t tiles = (a.n_rows + tc::BN - 1) / tc::BN;
   int64_t want = sms / qtiles;
   if (want < 1) want = 1;
   if (want > tiles) want = tiles;
@@ -467,18 +350,17 @@ __global__ void k_spread_queries(const int8_t* __restrict__ q, int64_t nq, int d
   for (int j = threadIdx.x; j < dim / 16; j += blockDim.x) dst[j] = src[j];
 }
 
-template <int CG>
-static int launch_cg(const TopkArgs& a, uint64_t* partials, int n_slices, cudaStream_t st) {
-  const int stages = tc_stages(a.dim, a.k, CG);
+static int launch_tc(const TopkArgs& a, uint64_t* partials, int n_slices, cudaStream_t st) {
+  const int stages = tc_stages(a.dim, a.k);
   if (stages < 2) return set_error(SS_ERR_UNSUPPORTED, "tcgen05: not enough shared memory");
-  const size_t smem = tc_fixed_smem(a.dim, a.k) + (size_t)stages * (tc::BN / CG) * tc::BK;
+  const size_t smem = tc_fixed_smem(a.dim, a.k) + (size_t)stages * tc::BN * tc::BK;
   CUtensorMap mq, mb;
   // pure top-k on a single query tile: spread the queries over the four TMEM
   // lane quarters so every epilogue warp shares the (then frequent) exact
   // path (rows past nq in the scratch are never used: their query index maps
   // >= nq).  With a similarity floor the exact path is rare and the extra
   // copy launch would only cost time.
-  const int spread = (CG == 1 && a.nq <= tc::BM && a.qscratch && a.theta <= 0.f) ? 1 : 0;
+  const int spread = (a.nq <= tc::BM && a.qscratch && a.theta <= 0.f) ? 1 : 0;
   if (spread) {
     count_launch();
     k_spread_queries<<<(unsigned)a.nq, 32, 0, st>>>(a.q, a.nq, a.dim, a.qscratch);
@@ -487,58 +369,23 @@ static int launch_cg(const TopkArgs& a, uint64_t* partials, int n_slices, cudaSt
   } else if (int rc = make_map(&mq, a.q, a.nq, a.dim, tc::BM)) {
     return rc;
   }
-  if (int rc = make_map(&mb, a.emb, a.n_rows, a.dim, tc::BN / CG)) return rc;
-  SS_CUDA_TRY(cudaFuncSetAttribute(k_topk_tc<CG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)smem));
+  if (int rc = make_map(&mb, a.emb, a.n_rows, a.dim, tc::BN)) return rc;
+  SS_CUDA_TRY(cudaFuncSetAttribute(k_topk_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int64_t tiles = (a.n_rows + tc::BN - 1) / tc::BN;
   const int64_t tps = (tiles + n_slices - 1) / n_slices;
-  int64_t qtiles = (a.nq + tc::BM - 1) / tc::BM;
-  qtiles = (qtiles + CG - 1) / CG * CG;  // a pair always has two CTAs
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)qtiles, (unsigned)n_slices);
-  cfg.blockDim = dim3(tc::THREADS);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CG;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  const int dbg = env_int("SS_TC_DEBUG", 0) | (tc_prefetch() << 8);
-  // cross-slice bound sharing: R = ceil(k / slices) <= 4 so every slice
-  // tracks its best R keys in registers (needs >= 16 slices at k = 64)
-  // cross-slice bound sharing, opt-in (SS_TC_GTHR=1: a.gthr, slots after
-  // gmin[nq]).  Not used for pure top-k here: with ~148 slices the bound is
-  // each slice's best key (R = 1), too weak to pay for reading 148 slots per
-  // tile (theta=-1, nq=8: 0.65 vs 0.52 ms); the TS kernel shares instead.
-  uint32_t* slots = a.gthr ? a.gthr + a.nq : nullptr;
-  int rshare = 0;
-  if (slots && n_slices >= 2 && n_slices <= kMaxShareSlices) {
-    const int R = (a.k + n_slices - 1) / n_slices;
-    if (R <= 4) rshare = R;
-  }
-  if (rshare)
-    SS_CUDA_TRY(cudaMemsetAsync(slots, 0, (size_t)n_slices * a.nq * sizeof(uint32_t), st));
+  const int64_t qtiles = (a.nq + tc::BM - 1) / tc::BM;
   count_launch();
-  SS_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_topk_tc<CG>, mq, mb, a.q_inv, a.nq, a.inv, a.n_rows,
-                                 a.dim / tc::BK, stages, a.k, a.theta, a.head % a.gcap, a.gcap,
-                                 a.slot_offset, tps, partials, dbg, slots, rshare, spread));
+  k_topk_tc<<<dim3((unsigned)qtiles, (unsigned)n_slices), tc::THREADS, smem, st>>>(
+      mq, mb, a.q_inv, a.nq, a.inv, a.n_rows, a.dim / tc::BK, stages, a.k, a.theta,
+      a.head % a.gcap, a.gcap, a.slot_offset, tps, partials, spread);
+  SS_LAUNCH_CHECK();
   return SS_OK;
 }
 
 int launch_topk_tc(const TopkArgs& a, uint64_t* partials, int n_slices, cudaStream_t st) {
   if (!topk_tc_supported(a)) return set_error(SS_ERR_UNSUPPORTED, "tcgen05 path unsupported");
-  if (use_pair(a)) {
-    CUtensorMap mq, mb;
-    if (int rc = make_map(&mq, a.q, a.nq, a.dim, tc::BM)) return rc;
-    if (int rc = make_map(&mb, a.emb, a.n_rows, a.dim, tc::BN / 2)) return rc;
-    return launch_topk_pair(a, partials, n_slices, st, mq, mb);
-  }
   if (use_ts(a)) return launch_topk_ts(a, partials, n_slices, st);
-  return tc_cg(a.nq) == 2 ? launch_cg<2>(a, partials, n_slices, st)
-                          : launch_cg<1>(a, partials, n_slices, st);
+  return launch_tc(a, partials, n_slices, st);
 }
 
 }  // namespace ss

@@ -1,4 +1,4 @@
-// Stage 1, large-batch path, v3: the query block (A operand) lives in TMEM.
+// Stage 1, large-batch path (nq > 128): the query block (A operand) lives in TMEM.
 //
 // Same math and parity contract as k_topk_sm100.cu (tcgen05.mma kind::i8,
 // exact int32 dots, fused per-query top-k), restructured so the epilogue is
@@ -10,12 +10,13 @@
 //     columns in halves; the two warps serving a query share its heap under
 //     a per-query shared-memory lock (inserts are rare), so one heap set and
 //     four 32 KB bank stages fit;
-//   * one N=256 accumulator (N=256 and 128B-swizzled K-blocks are what keep
-//     the int8 MMA at full rate): each epilogue warp pulls its 4 column
-//     chunks into registers, releases the accumulator at once, and filters
-//     from registers while the MMA of the next tile runs.
+//   * two accumulators of BN columns (BN = 208 beside dim 384, 192 beside
+//     dim 512: the widest double buffer that fits next to A in 512 TMEM
+//     columns): each epilogue warp pulls its BN/2 columns into registers,
+//     releases the accumulator at once, and filters from registers while the
+//     MMA of the next tile runs.
 // Warps: 0 TMA producer (bank tiles), 1 TMEM allocator + MMA issuer,
-// 2..9 epilogue (group g = (warp-2)/4 owns columns [128g, 128g+128)).
+// 2..9 epilogue (group g = (warp-2)/4 owns columns [g*BN/2, (g+1)*BN/2)).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <stdlib.h>
@@ -63,25 +64,6 @@ __device__ __forceinline__ void tma2d(void* dst, const CUtensorMap* m, uint64_t*
       "l"(m), "r"(su32(b)), "r"(c0), "r"(c1)
       : "memory");
 }
-// the same box, multicast into the same smem offset of every CTA in `mask`
-// (each destination CTA's barrier at `b`'s offset receives the byte count)
-__device__ __forceinline__ void tma2d_mc(void* dst, const CUtensorMap* m, uint64_t* b, int c0, int c1,
-                                         uint16_t mask) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
-      " [%0], [%1, {%3, %4}], [%2], %5;\n" ::"r"(su32(dst)),
-      "l"(m), "r"(su32(b)), "r"(c0), "r"(c1), "h"(mask)
-      : "memory");
-}
-__device__ __forceinline__ uint32_t cluster_rank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ void cluster_sync() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::
-                   : "memory");
-}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
@@ -95,29 +77,12 @@ __device__ __forceinline__ void commit(uint64_t* b) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(su32(b))
                : "memory");
 }
-// arrive on the barrier at `b`'s offset in every CTA of `mask` when this
-// thread's MMAs complete
-__device__ __forceinline__ void commit_mc(uint64_t* b, uint16_t mask) {
-  asm volatile(
-      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
-      " [%0], %1;\n" ::"r"(su32(b)), "h"(mask)
-      : "memory");
-}
 // D[tmem] (+)= A[tmem] x B[smem]^T
 __device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
   asm volatile(
       "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
       "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d),
       "r"(a), "l"(bdesc), "r"(idesc), "r"(acc)
-      : "memory");
-}
-// D[tmem] (+)= A[smem] x B[smem]^T (the last K-block when A is split)
-__device__ __forceinline__ void mma_ss(uint32_t d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                       uint32_t acc) {
-  asm volatile(
-      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
       : "memory");
 }
 // K-major, 128B swizzle: rows of 128 B, 8-row atoms 1024 B apart (SBO)
@@ -171,23 +136,6 @@ __device__ __forceinline__ void wait_ld8(int (&v)[8]) {
                :
                : "memory");
 }
-__device__ __forceinline__ void ld16_async(uint32_t taddr, int (&v)[16]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
-      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];\n"
-      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
-        "=r"(v[14]), "=r"(v[15])
-      : "r"(taddr));
-}
-__device__ __forceinline__ void wait_ld16(int (&v)[16]) {
-  asm volatile("tcgen05.wait::ld.sync.aligned;\n"
-               : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]),
-                 "+r"(v[7]), "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]), "+r"(v[12]),
-                 "+r"(v[13]), "+r"(v[14]), "+r"(v[15])
-               :
-               : "memory");
-}
 __device__ __forceinline__ void st32(uint32_t taddr, const uint32_t (&v)[32]) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
@@ -210,13 +158,6 @@ __device__ __noinline__ uint64_t heap_replace(uint64_t* heap, int k, uint64_t x)
   return heap[0];
 }
 
-// BN bank rows per tile (UMMA N), NACC accumulators of BN columns in TMEM
-// (NACC = 2 lets the MMA of tile t+1 run while tile t is drained), A in
-// columns [NACC * BN, NACC * BN + dim / 4).
-// ASPLIT = 1: the last K-block of A lives in shared memory (TMA) instead of
-// TMEM, which frees 32 TMEM columns: two N=224 accumulators + 64 A columns
-// fill the 512 columns exactly.  ASPLIT = 2: all of A in shared memory
-// (SS-form MMA), so two N=256 accumulators fill TMEM.
 // The slow path of the pure-top-k (SHARE) filter, out of line: many chunks
 // pass there, and one copy of this code (instead of one per inlined chunk)
 // measured faster (1.29 vs 1.45 ms at c2, theta = -1); with a similarity
@@ -284,40 +225,31 @@ __device__ __noinline__ float insert_locked(uint32_t mask, const float* sl, floa
 // slice has published, the union of their top-R holds >= k rows at or above
 // that minimum, so it bounds the global k-th key from below.  Slots that are
 // still 0 make the minimum 0 (no bound).
-#ifndef SS_SHARE_EVERY
-#define SS_SHARE_EVERY 2
-#endif
-constexpr int SHARE_EVERY = SS_SHARE_EVERY;
+constexpr int SHARE_EVERY = 2;
+constexpr int NACC = 2;  // accumulators: the MMA of tile t+1 runs while tile t drains
 
-template <int BN, int NACC, int ASPLIT, bool SHARE = false>
+template <int BN, bool SHARE>
 __global__ void __launch_bounds__(THREADS, 1)
-k_topk_ts(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmQ,
-          const int8_t* __restrict__ Q,
+k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
           const float* __restrict__ q_inv, int64_t nq, const float* __restrict__ inv, int64_t n_rows,
           int dim, int stages, int k, float theta, int64_t hmod, int64_t gcap, int64_t slot_offset,
-          int64_t tiles_per_slice, uint64_t* __restrict__ partials, int dbg,
-          uint32_t* __restrict__ gslots = nullptr, int rshare = 0, int mc = 0) {
+          int64_t tiles_per_slice, uint64_t* __restrict__ partials,
+          uint32_t* __restrict__ gslots, int rshare) {
   constexpr int A_COL = NACC * BN;
   constexpr int B_STAGE = BN * BK;
   constexpr int HALF = BN / 2;     // columns per epilogue warp per tile
   constexpr int CPW = HALF / 32;   // full 32-column chunks per epilogue warp per tile
-  constexpr int TAIL = HALF % 32;  // + one 8- or 16-column chunk (BN = 208 / 224)
-  static_assert((CPW == 3 || CPW == 4) && (TAIL == 0 || ((TAIL == 8 || TAIL == 16) && CPW == 3)),
-                "tile shape");
-  constexpr bool A_ALL = ASPLIT == 2, A_LAST = ASPLIT == 1;
-  static_assert(A_ALL || A_COL + (A_LAST ? 64 : 96) <= 512,
-                "TMEM columns (dim 384 beside the accumulators)");
+  constexpr int TAIL = HALF % 32;  // + one 8-column chunk (BN = 208)
+  static_assert(CPW == 3 && (TAIL == 0 || TAIL == 8), "tile shape");
   constexpr uint32_t IDESC = idesc(BN);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
-  uint8_t* sB = smem;                                                    // stages x 32 KB
-  uint8_t* sA = sB + stages * B_STAGE;  // ASPLIT: the last K-block of A (16 KB, 1024-aligned)
-  uint64_t* s_heap =
-      reinterpret_cast<uint64_t*>(sA + (A_ALL ? BM * dim : A_LAST ? BM * BK : 0));  // [k][128]
+  uint8_t* sB = smem;                                                    // stages x BN x 128 B
+  uint64_t* s_heap = reinterpret_cast<uint64_t*>(sB + stages * B_STAGE);  // [k][128]
   uint64_t* s_hroot = s_heap + (size_t)k * BM;                           // [128]
   int* s_hcnt = reinterpret_cast<int*>(s_hroot + BM);                    // [128]
   int* s_hlock = s_hcnt + BM;                                            // [128]
-  float* s_inv = reinterpret_cast<float*>(s_hlock + BM);                 // [ISLOTS][BN]
+  float* s_inv = reinterpret_cast<float*>(s_hlock + BM);                 // [ISLOTS][256]
   float* s_ib = s_inv + ISLOTS * 256;                                    // [8 warps][16]
   uint64_t* bars = reinterpret_cast<uint64_t*>(s_ib + EPI_WARPS * 16);
   uint64_t* a_full = bars;
@@ -327,8 +259,7 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUten
   uint64_t* tempty = tfull + NACC;
   uint64_t* ifull = tempty + NACC;   // [ISLOTS] tile's inverse norms landed
   uint64_t* iempty = ifull + ISLOTS; // [ISLOTS] consumed by every epilogue warp
-  uint64_t* mdone = iempty + ISLOTS;
-  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(mdone + 1);
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(iempty + ISLOTS);
   // SHARE: this slice's top-R keys per query, after everything else
   uint32_t* s_rtop = s_tmem + 4;  // [128][4]
 
@@ -337,17 +268,14 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUten
   const int nkb = dim / BK;
   const int64_t tile0 = (int64_t)slice * tiles_per_slice;
   const int64_t total_tiles = (n_rows + BN - 1) / BN;
-  int ntiles = (int)max((int64_t)0, min(total_tiles, tile0 + tiles_per_slice) - tile0);
+  const int ntiles = (int)max((int64_t)0, min(total_tiles, tile0 + tiles_per_slice) - tile0);
 
   if (threadIdx.x == 0) {
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmB) : "memory");
-    // 4 TMEM-writer warps (+ the TMA of the smem K-block); A_ALL: the TMA alone
-    bar_init(a_full, A_ALL ? 1 : A_LAST ? 5 : 4);
-    // mc: a slot is refilled (for both CTAs of the pair) once both MMAs freed it
-    for (int s = 0; s < stages; ++s) { bar_init(&full[s], 1); bar_init(&empty[s], mc ? 2 : 1); }
+    bar_init(a_full, 4);  // the 4 warps writing A into TMEM
+    for (int s = 0; s < stages; ++s) { bar_init(&full[s], 1); bar_init(&empty[s], 1); }
     for (int b = 0; b < NACC; ++b) { bar_init(&tfull[b], 1); bar_init(&tempty[b], EPI_WARPS); }
     for (int b = 0; b < ISLOTS; ++b) { bar_init(&ifull[b], 1); bar_init(&iempty[b], EPI_WARPS); }
-    bar_init(mdone, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   for (int i = threadIdx.x; i < BM; i += blockDim.x) { s_hcnt[i] = 0; s_hroot[i] = 0; s_hlock[i] = 0; }
@@ -359,51 +287,27 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUten
   }
   fence_before();
   __syncthreads();
-  if (mc) cluster_sync();  // the peer's barriers are initialised before any multicast
   fence_after();
   const uint32_t tmem = *s_tmem;
 
   if (warp == 0) {
     // ------------------------------------------------------ TMA producer ---
     if (lane == 0 && ntiles > 0) {
-      if constexpr (A_LAST) {
-        bar_expect(a_full, BM * BK);
-        tma2d(sA, &tmQ, a_full, (nkb - 1) * BK, qt * BM);
-      }
-      if constexpr (A_ALL) {
-        bar_expect(a_full, BM * dim);
-        for (int kb = 0; kb < nkb; ++kb) tma2d(sA + kb * BM * BK, &tmQ, a_full, kb * BK, qt * BM);
-      }
       int it = 0;
       for (int t = 0; t < ntiles; ++t) {
         const int row0 = (int)((tile0 + t) * BN);
         // the tile's BN inverse norms into the ring (the bank pads inv with
         // one NaN tile, so the copy never leaves the allocation); the
         // epilogue then issues no global loads in its tile loop
-        if (!(dbg & 64)) {
-          const int sl = t % ISLOTS;
-          bar_wait(&iempty[sl], ((t / ISLOTS) & 1) ^ 1);
-          bar_expect(&ifull[sl], BN * 4);
-          bulk_g2s(s_inv + sl * 256, inv + row0, BN * 4, &ifull[sl]);
-        }
+        const int sl = t % ISLOTS;
+        bar_wait(&iempty[sl], ((t / ISLOTS) & 1) ^ 1);
+        bar_expect(&ifull[sl], BN * 4);
+        bulk_g2s(s_inv + sl * 256, inv + row0, BN * 4, &ifull[sl]);
         for (int kb = 0; kb < nkb; ++kb, ++it) {
           const int s = it % stages;
           bar_wait(&empty[s], ((it / stages) & 1) ^ 1);
-          if (dbg & 8) {  // debug: MMA on stale tiles, no bank traffic
-            bar_arrive(&full[s]);
-            continue;
-          }
           bar_expect(&full[s], B_STAGE);
-          if (mc) {
-            // cluster pair = two query tiles of one slice: each CTA fetches half
-            // of the bank tile's rows and multicasts it into both CTAs' slot,
-            // halving the L2 -> SM traffic of the tile
-            const uint32_t cr = cluster_rank();
-            tma2d_mc(sB + s * B_STAGE + cr * (B_STAGE / 2), &tmB, &full[s], kb * BK,
-                     row0 + (int)cr * (BN / 2), (uint16_t)3);
-          } else {
-            tma2d(sB + s * B_STAGE, &tmB, &full[s], kb * BK, row0);
-          }
+          tma2d(sB + s * B_STAGE, &tmB, &full[s], kb * BK, row0);
         }
       }
       for (int i = max(0, it - stages); i < it; ++i) bar_wait(&empty[i % stages], (i / stages) & 1);
@@ -418,36 +322,20 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUten
       for (int t = 0; t < ntiles; ++t) {
         const int acc = t % NACC;
         // every epilogue warp has pulled tile t - NACC out of this accumulator
-        if (!(dbg & 64)) bar_wait(&tempty[acc], ((t / NACC) & 1) ^ 1);
+        bar_wait(&tempty[acc], ((t / NACC) & 1) ^ 1);
         fence_after();
         const uint32_t dacc = tmem + acc * BN;
         for (int kb = 0; kb < nkb; ++kb, ++it) {
           const int s = it % stages;
           bar_wait(&full[s], (it / stages) & 1);
           fence_after();
-          if (A_ALL || (A_LAST && kb == nkb - 1)) {
 #pragma unroll
-            for (int kk = 0; kk < BK / UK; ++kk)
-              if (!(dbg & 2))
-                mma_ss(dacc, desc_sw128(su32(sA) + (A_ALL ? kb * BM * BK : 0) + kk * UK),
-                       desc_sw128(b_base + s * B_STAGE + kk * UK), IDESC, (kb | kk) != 0);
-          } else {
-#pragma unroll
-            for (int kk = 0; kk < BK / UK; ++kk)
-              if (!(dbg & 2))
-                mma_ts(dacc, tmem + A_COL + (kb * (BK / UK) + kk) * (UK / 4),
-                       desc_sw128(b_base + s * B_STAGE + kk * UK), IDESC, (kb | kk) != 0);
-          }
-          if (mc)
-            commit_mc(&empty[s], (uint16_t)3);
-          else
-            commit(&empty[s]);
+          for (int kk = 0; kk < BK / UK; ++kk)
+            mma_ts(dacc, tmem + A_COL + (kb * (BK / UK) + kk) * (UK / 4),
+                   desc_sw128(b_base + s * B_STAGE + kk * UK), IDESC, (kb | kk) != 0);
+          commit(&empty[s]);
         }
         commit(&tfull[acc]);
-      }
-      if (dbg & 64) {  // nobody drains: wait for the last MMA before teardown
-        commit(mdone);
-        bar_wait(mdone, 0);
       }
     }
   } else {
@@ -459,8 +347,8 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUten
     const int64_t q = (int64_t)qt * BM + qrow;
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
     // group 0 writes this query's int8 vector into TMEM (A operand)
-    if (grp == 0 && !A_ALL) {
-      const int ncol = (A_LAST ? dim - BK : dim) / 4;
+    if (grp == 0) {
+      const int ncol = dim / 4;
       for (int c0 = 0; c0 < ncol; c0 += 32) {
         uint32_t v[32];
         const uint4* src = reinterpret_cast<const uint4*>(Q + q * dim) + c0 / 4;
@@ -479,7 +367,6 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUten
     const float iq = (q < nq) ? q_inv[q] : __int_as_float(0x7fc00000);
     uint64_t* heap = s_heap + qrow;  // shared by the two column-half warps of this quarter
     float* cib = s_ib + ew * 16;  // [max inv_w of half 0..7][min inv_w of half 0..7]
-    if (dbg & 64) ntiles = 0;  // debug: MMA issue rate alone (no epilogue hand-off)
     float thr = (iq == iq) ? s_threshold(theta, iq) : INFINITY;
     for (int t = 0; t < ntiles; ++t) {
       const int64_t row0 = (tile0 + t) * BN + grp * HALF;  // first bank row of my columns
@@ -519,38 +406,19 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUten
       bar_wait(&tfull[acc], (t / NACC) & 1);
       fence_after();
       const uint32_t tbase = tmem + lane_base + acc * BN + grp * HALF;
-      if (dbg & 16) {
-        fence_before();
-        __syncwarp();
-        if (lane == 0) { bar_arrive(&tempty[acc]); bar_arrive(&iempty[sl]); }
-        continue;
-      }
-      // pull my 4 chunks into registers, then hand the accumulator back
-      int v0[32], v1[32], v2[32], v3[32], vt[TAIL ? TAIL : 1];
+      // pull my chunks into registers, then hand the accumulator back
+      int v0[32], v1[32], v2[32], vt[TAIL ? TAIL : 1];
       ld32_async(tbase, v0);
       ld32_async(tbase + 32, v1);
       ld32_async(tbase + 64, v2);
-      if constexpr (CPW == 4) ld32_async(tbase + 96, v3);
       if constexpr (TAIL == 8) ld8_async(tbase + 96, vt);
-      if constexpr (TAIL == 16) ld16_async(tbase + 96, vt);
       wait_ld(v0);
       wait_ld(v1);
       wait_ld(v2);
-      if constexpr (CPW == 4) wait_ld(v3);
       if constexpr (TAIL == 8) wait_ld8(vt);
-      if constexpr (TAIL == 16) wait_ld16(vt);
       fence_before();
       __syncwarp();
       if (lane == 0) bar_arrive(&tempty[acc]);
-      if (dbg & 4) {
-        if (lane == 0) bar_arrive(&iempty[sl]);
-        continue;
-      }
-      // Filter: a chunk of 32 columns can only hold a score >= thr if
-      // fl(fl(max dot) * (max inv_w)) >= thr (or the min inv_w when every dot
-      // is negative) -- monotone rounding makes this a superset test, so the
-      // exact per-column scores (one int->float conversion each, quarter rate)
-      // are only computed for the rare chunks that pass it.
       // Filter per 16-column half: a half can only hold a score >= thr if
       // fl(fl(max dot) * (max inv_w)) >= thr (or the min inv_w when every dot
       // is negative) -- monotone rounding makes this a superset test, so the
@@ -559,30 +427,29 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUten
       auto exact = [&](const auto& v, const int c, auto off_c, auto w_c) {
         constexpr int OFF = decltype(off_c)::value;
         constexpr int WW = decltype(w_c)::value;
-          float s[WW];
-          const float4* iw4 = reinterpret_cast<const float4*>(ciw + c * 32 + OFF);
+        float s[WW];
+        const float4* iw4 = reinterpret_cast<const float4*>(ciw + c * 32 + OFF);
 #pragma unroll
-          for (int j4 = 0; j4 < WW / 4; ++j4) {
-            const float4 w = iw4[j4];
-            s[4 * j4 + 0] = __fmul_rn(__int2float_rn(v[OFF + 4 * j4 + 0]), w.x);
-            s[4 * j4 + 1] = __fmul_rn(__int2float_rn(v[OFF + 4 * j4 + 1]), w.y);
-            s[4 * j4 + 2] = __fmul_rn(__int2float_rn(v[OFF + 4 * j4 + 2]), w.z);
-            s[4 * j4 + 3] = __fmul_rn(__int2float_rn(v[OFF + 4 * j4 + 3]), w.w);
-          }
-          const int64_t gbase = slot_offset + row0 + c * 32 + OFF - hmod;
-          uint32_t mask = 0;
+        for (int j4 = 0; j4 < WW / 4; ++j4) {
+          const float4 w = iw4[j4];
+          s[4 * j4 + 0] = __fmul_rn(__int2float_rn(v[OFF + 4 * j4 + 0]), w.x);
+          s[4 * j4 + 1] = __fmul_rn(__int2float_rn(v[OFF + 4 * j4 + 1]), w.y);
+          s[4 * j4 + 2] = __fmul_rn(__int2float_rn(v[OFF + 4 * j4 + 2]), w.z);
+          s[4 * j4 + 3] = __fmul_rn(__int2float_rn(v[OFF + 4 * j4 + 3]), w.w);
+        }
+        const int64_t gbase = slot_offset + row0 + c * 32 + OFF - hmod;
+        uint32_t mask = 0;
 #pragma unroll
-          for (int j = 0; j < WW; ++j) mask |= (s[j] >= thr ? 1u : 0u) << j;
-          if (!mask) return;
-          float sl[WW];
+        for (int j = 0; j < WW; ++j) mask |= (s[j] >= thr ? 1u : 0u) << j;
+        if (!mask) return;
+        float sl[WW];
 #pragma unroll
-          for (int j = 0; j < WW; ++j) sl[j] = s[j];
-          if constexpr (SHARE) {
-            thr = insert_locked<true>(mask, sl, iq, theta, gbase, gcap, heap, k, s_hlock, s_hcnt,
-                                      s_hroot, qrow, s_rtop, rshare, gslots,
-                                      (int64_t)slice * nq + q, thr);
-            return;
-          }
+        for (int j = 0; j < WW; ++j) sl[j] = s[j];
+        if constexpr (SHARE) {
+          thr = insert_locked<true>(mask, sl, iq, theta, gbase, gcap, heap, k, s_hlock, s_hcnt,
+                                    s_hroot, qrow, s_rtop, rshare, gslots,
+                                    (int64_t)slice * nq + q, thr);
+        } else {
           // this query's heap is shared with the other column-half warp: take
           // its lock (one lock per thread at a time, never nested)
           while (atomicCAS(&s_hlock[qrow], 0, 1) != 0) {
@@ -590,8 +457,6 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUten
           __threadfence_block();
           int hcnt = s_hcnt[qrow];
           uint64_t hroot = s_hroot[qrow];
-          uint32_t rth0 = 0u;
-          if constexpr (SHARE) rth0 = s_rtop[qrow * 4 + rshare - 1];
           while (mask) {
             const int j = __ffs(mask) - 1;
             mask &= mask - 1;
@@ -600,36 +465,20 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUten
               int64_t rel = gbase + j;
               if (rel < 0) rel += gcap;
               const uint64_t comp = make_comp(key, (uint32_t)rel);
-              bool kept = true;
               if (hcnt < k) {
                 heap[hcnt * BM] = comp;
                 if (++hcnt == k) hroot = heapify(heap, k);
               } else if (comp > hroot) {
                 hroot = heap_replace(heap, k, comp);
-              } else {
-                kept = false;
-              }
-              if constexpr (SHARE) {
-                if (kept) {  // this slice's top-R keys, descending
-                  uint32_t x = f32_order(key);
-                  for (int i = 0; i < rshare; ++i) {
-                    const uint32_t cur = s_rtop[qrow * 4 + i];
-                    if (x > cur) { s_rtop[qrow * 4 + i] = x; x = cur; }
-                  }
-                }
               }
             }
           }
-          uint32_t rth1 = 0u;
-          if constexpr (SHARE) rth1 = s_rtop[qrow * 4 + rshare - 1];
           s_hcnt[qrow] = hcnt;
           s_hroot[qrow] = hroot;
           __threadfence_block();
           atomicExch(&s_hlock[qrow], 0);
           if (hcnt >= k) thr = fmaxf(thr, s_threshold(comp_key(hroot), iq));
-          if constexpr (SHARE) {
-            if (rth1 != rth0) __stcg(gslots + (int64_t)slice * nq + q, rth1);  // publish
-          }
+        }
       };
       auto chunk = [&](const auto& v, const int c) {
         constexpr int W = sizeof(v) / sizeof(v[0]);  // 32, or 8 for the N=208 tail
@@ -648,34 +497,22 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUten
           if constexpr (SHARE) {
             // pure top-k: many chunks pass while the bounds rise -- one exact
             // pass (and one heap lock) per 32 columns is cheaper there
-            if (!(dbg & 1) && fmaxf(bl, bh) >= thr)
+            if (fmaxf(bl, bh) >= thr)
               exact(v, c, std::integral_constant<int, 0>(), std::integral_constant<int, 32>());
           } else {
-            if (!(dbg & 1) && bl >= thr)
-              exact(v, c, std::integral_constant<int, 0>(), std::integral_constant<int, 16>());
-            if (!(dbg & 1) && bh >= thr)
-              exact(v, c, std::integral_constant<int, 16>(), std::integral_constant<int, 16>());
+            if (bl >= thr) exact(v, c, std::integral_constant<int, 0>(), std::integral_constant<int, 16>());
+            if (bh >= thr) exact(v, c, std::integral_constant<int, 16>(), std::integral_constant<int, 16>());
           }
-        } else {  // the tail chunk: one half of 8 (BN = 208) or 16 (BN = 224) columns
-          int md;
-          if constexpr (W == 16) {
-            const int a0 = __vimax3_s32(v[0], v[1], v[2]), a1 = __vimax3_s32(v[3], v[4], v[5]);
-            const int a2 = __vimax3_s32(v[6], v[7], v[8]), a3 = __vimax3_s32(v[9], v[10], v[11]);
-            const int a4 = __vimax3_s32(v[12], v[13], v[14]);
-            md = __vimax3_s32(__vimax3_s32(a0, a1, a2), __vimax3_s32(a3, a4, v[15]), a0);
-          } else {
-            md = __vimax3_s32(__vimax3_s32(v[0], v[1], v[2]), __vimax3_s32(v[3], v[4], v[5]),
-                              max(v[6], v[7]));
-          }
+        } else {  // the tail chunk: 8 columns (BN = 208)
+          const int md = __vimax3_s32(__vimax3_s32(v[0], v[1], v[2]), __vimax3_s32(v[3], v[4], v[5]),
+                                      max(v[6], v[7]));
           const float bnd = __fmul_rn(__int2float_rn(md), md >= 0 ? cib[2 * c] : cib[8 + 2 * c]);
-          if (!(dbg & 1) && bnd >= thr)
-            exact(v, c, std::integral_constant<int, 0>(), std::integral_constant<int, W>());
+          if (bnd >= thr) exact(v, c, std::integral_constant<int, 0>(), std::integral_constant<int, W>());
         }
       };
       chunk(v0, 0);
       chunk(v1, 1);
       chunk(v2, 2);
-      if constexpr (CPW == 4) chunk(v3, 3);
       if constexpr (TAIL != 0) chunk(vt, 3);
       __syncwarp();
       if (lane == 0) bar_arrive(&iempty[sl]);  // this tile's inverse norms consumed
@@ -689,7 +526,6 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUten
   }
   fence_before();
   __syncthreads();
-  if (mc) cluster_sync();  // no multicast / remote arrive targets an exited CTA
   if (warp == 1) {
     fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
@@ -715,111 +551,33 @@ static size_t ts_fixed_smem(int k) {
          1024;
 }
 
-// Tile shape (bank rows per tile, accumulators): 208 x 2 with all of A in
-// TMEM (default: the widest double buffer that fits beside A), 224 x 2 with
-// the last K-block of A in shared memory (SS_TC_TSN=224; the SS-form MMA of
-// that K-block ran slower, 0.303 vs 0.297 ms MMA-only, 0.378 vs 0.373 ms end
-// to end), 192 x 2, 256 x 1, or (code 512) 256 x 2 with all of A in shared
-// memory (SS-form MMA, SS_TC_TSN=512).
-static int ts_bn(const TopkArgs& a) {
-  static const int v = getenv("SS_TC_TSN") ? atoi(getenv("SS_TC_TSN")) : 208;
-  const int want = (v == 256 || v == 192 || v == 224 || v == 512) ? v : 208;
-  if (want == 512) return 512;
-  if (want == 224 && a.dim / 4 - 32 + 2 * 224 <= 512) return 224;
-  if (want >= 208 && want != 256 && a.dim / 4 + 2 * 208 <= 512) return 208;
-  if (want == 256) return 256;
-  return 192;
-}
-static int ts_rows(int code) { return code == 512 ? 256 : code; }
-static size_t ts_smem_extra(int code, int dim) {
-  return code == 224 ? (size_t)ts::BM * ts::BK : code == 512 ? (size_t)ts::BM * dim : 0;
-}
-static int ts_stages(int k, int code, int dim) {
-  // SS_TS_STAGES caps the bank-stage ring (ablation; default: as many as fit)
-  static const int cap = getenv("SS_TS_STAGES") ? atoi(getenv("SS_TS_STAGES")) : 8;
-  for (int s = std::min(8, std::max(3, cap)); s >= 3; --s)
-    if (ts_fixed_smem(k) + ts_smem_extra(code, dim) + (size_t)s * ts_rows(code) * ts::BK <=
-        227 * 1024)
-      return s;
+// Tile rows: the widest double buffer of accumulators that fits beside A
+// (dim / 4 TMEM columns): 2 x 208 + 96 = 512 at dim 384 (and below), 2 x 192
+// + 128 = 512 at dim 512.
+static int ts_bn(int dim) { return dim / 4 + 2 * 208 <= 512 ? 208 : 192; }
+
+static int ts_stages(int k, int bn) {
+  for (int s = 8; s >= 3; --s)
+    if (ts_fixed_smem(k) + ts::BM * 16 + (size_t)s * bn * ts::BK <= 227 * 1024) return s;
   return 0;
 }
 
 bool topk_ts_supported(const TopkArgs& a) {
-  const int bn = ts_bn(a);
-  const int acols = bn == 256 ? 256 : bn == 512 ? 512 : 2 * bn;
-  const int a_tmem = bn == 224 ? a.dim / 4 - 32 : bn == 512 ? 0 : a.dim / 4;
-  if (a.dim % ts::BK || a.dim % 128 || a_tmem + acols > 512 || a.k < 1 || a.k > ts::KMAX)
-    return false;
+  const int bn = ts_bn(a.dim);
+  if (a.dim % ts::BK || a.dim / 4 + 2 * bn > 512 || a.k < 1 || a.k > ts::KMAX) return false;
   if (a.n_rows >= (1LL << 31) || a.nq >= (1LL << 31)) return false;
   if (!a.inv_padded) return false;  // tiles of inverse norms are bulk-copied whole
-  return ts_stages(a.k, bn, a.dim) >= 3;
-}
-
-// Cluster pairs along the query-tile axis sharing each bank tile by TMA
-// multicast (SS_TC_MC=1): needs an even number of query tiles.
-static bool ts_mc(const TopkArgs& a) {
-  static const int v = getenv("SS_TC_MC") ? atoi(getenv("SS_TC_MC")) : 0;
-  const int64_t qtiles = (a.nq + ts::BM - 1) / ts::BM;
-  return v == 1 && qtiles >= 2 && qtiles % 2 == 0;
-}
-
-template <int BN, int NACC, int ASPLIT>
-static constexpr int ts_code() { return ASPLIT == 2 ? 512 : BN; }
-
-template <int BN, int NACC, int ASPLIT>
-static size_t ts_smem_bytes(const TopkArgs& a, bool share) {
-  constexpr int code = ts_code<BN, NACC, ASPLIT>();
-  return ts_fixed_smem(a.k) + ts_smem_extra(code, a.dim) +
-         (size_t)ts_stages(a.k, code, a.dim) * BN * ts::BK + (share ? ts::BM * 16 : 0);
-}
-
-// SMs usable by 2-CTA clusters of this kernel (GPCs may leave SMs unpaired)
-template <int BN, int NACC, int ASPLIT>
-static int ts_mc_sms(const TopkArgs& a, int sms) {
-  static int cached = -1;
-  if (cached < 0) {
-    auto kern = ts::k_topk_ts<BN, NACC, ASPLIT, false>;
-    const size_t smem = ts_smem_bytes<BN, NACC, ASPLIT>(a, false);
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(2, (unsigned)sms);
-    cfg.blockDim = dim3(ts::THREADS);
-    cfg.dynamicSmemBytes = smem;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 2;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n < 1) {
-      cudaGetLastError();
-      n = sms / 2;
-    }
-    cached = std::min(sms, 2 * n);
-  }
-  return cached;
+  return ts_stages(a.k, bn) >= 3;
 }
 
 // one partial list per CTA slice
 int topk_ts_lists(const TopkArgs& a, int device) {
   const int64_t qtiles = (a.nq + ts::BM - 1) / ts::BM;
-  const int64_t tiles = (a.n_rows + ts_rows(ts_bn(a)) - 1) / ts_rows(ts_bn(a));
-  int sms = sm_count(device);
-  if (ts_mc(a)) {
-    switch (ts_bn(a)) {
-      case 512: sms = ts_mc_sms<256, 2, 2>(a, sms); break;
-      case 256: sms = ts_mc_sms<256, 1, false>(a, sms); break;
-      case 192: sms = ts_mc_sms<192, 2, false>(a, sms); break;
-      case 208: sms = ts_mc_sms<208, 2, false>(a, sms); break;
-      default: sms = ts_mc_sms<224, 2, true>(a, sms); break;
-    }
-  }
-  return pick_slices(qtiles, tiles, sms);
+  const int64_t tiles = (a.n_rows + ts_bn(a.dim) - 1) / ts_bn(a.dim);
+  return pick_slices(qtiles, tiles, sm_count(device));
 }
 
-template <int BN, int NACC, int ASPLIT>
+template <int BN>
 static int launch_ts_t(const TopkArgs& a, uint64_t* partials, int n_slices, cudaStream_t st) {
   // pure top-k: share per-slice bounds (see k_topk_ts SHARE)
   int rshare = 0;
@@ -832,69 +590,33 @@ static int launch_ts_t(const TopkArgs& a, uint64_t* partials, int n_slices, cuda
   CUtensorMap mb;
   cuuint64_t gdim[2] = {(cuuint64_t)a.dim, (cuuint64_t)a.n_rows};
   cuuint64_t gstride[1] = {(cuuint64_t)a.dim};
-  const bool mc = ts_mc(a);
-  cuuint32_t box[2] = {(cuuint32_t)ts::BK, (cuuint32_t)(mc ? BN / 2 : BN)};
+  cuuint32_t box[2] = {(cuuint32_t)ts::BK, (cuuint32_t)BN};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(&mb, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(a.emb), gdim, gstride,
                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_error(SS_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
-  CUtensorMap mq = mb;  // queries (A) for the smem K-block of the split form
-  if (ASPLIT) {
-    cuuint64_t qdim[2] = {(cuuint64_t)a.dim, (cuuint64_t)a.nq};
-    cuuint32_t qbox[2] = {(cuuint32_t)ts::BK, (cuuint32_t)ts::BM};
-    r = enc(&mq, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(a.q), qdim, gstride, qbox,
-            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) return set_error(SS_ERR_CUDA, "cuTensorMapEncodeTiled (q) failed (%d)", (int)r);
-  }
-  const int stages = ts_stages(a.k, ts_code<BN, NACC, ASPLIT>(), a.dim);
-  const size_t smem = ts_fixed_smem(a.k) + ts_smem_extra(ts_code<BN, NACC, ASPLIT>(), a.dim) +
-                      (size_t)stages * BN * ts::BK +
-                      (rshare ? ts::BM * 16 : 0);
-  auto kern = rshare ? ts::k_topk_ts<BN, NACC, ASPLIT, true> : ts::k_topk_ts<BN, NACC, ASPLIT, false>;
+  const int stages = ts_stages(a.k, BN);
+  const size_t smem = ts_fixed_smem(a.k) + (size_t)stages * BN * ts::BK + (rshare ? ts::BM * 16 : 0);
+  auto kern = rshare ? ts::k_topk_ts<BN, true> : ts::k_topk_ts<BN, false>;
   SS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   if (rshare)
     SS_CUDA_TRY(cudaMemsetAsync(a.gslots, 0, (size_t)n_slices * a.nq * sizeof(uint32_t), st));
   const int64_t tiles = (a.n_rows + BN - 1) / BN;
   const int64_t tps = (tiles + n_slices - 1) / n_slices;
   dim3 grid((unsigned)((a.nq + ts::BM - 1) / ts::BM), (unsigned)n_slices);
-  const char* dv = getenv("SS_TC_DEBUG");
   count_launch();
-  if (mc) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = grid;
-    cfg.blockDim = dim3(ts::THREADS);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 2;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    SS_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, mb, mq, a.q, a.q_inv, a.nq, a.inv, a.n_rows, a.dim,
-                                   stages, a.k, a.theta, a.head % a.gcap, a.gcap, a.slot_offset,
-                                   tps, partials, dv ? atoi(dv) : 0, a.gslots, rshare, 1));
-  } else {
-    kern<<<grid, ts::THREADS, smem, st>>>(
-        mb, mq, a.q, a.q_inv, a.nq, a.inv, a.n_rows, a.dim, stages, a.k, a.theta, a.head % a.gcap,
-        a.gcap, a.slot_offset, tps, partials, dv ? atoi(dv) : 0, a.gslots, rshare, 0);
-  }
+  kern<<<grid, ts::THREADS, smem, st>>>(mb, a.q, a.q_inv, a.nq, a.inv, a.n_rows, a.dim, stages, a.k,
+                                        a.theta, a.head % a.gcap, a.gcap, a.slot_offset, tps,
+                                        partials, a.gslots, rshare);
   SS_LAUNCH_CHECK();
   return SS_OK;
 }
 
 int launch_topk_ts(const TopkArgs& a, uint64_t* partials, int n_lists, cudaStream_t st) {
   if (n_lists < 1) return set_error(SS_ERR_ARG, "ts: no slices");
-  switch (ts_bn(a)) {
-    case 512: return launch_ts_t<256, 2, 2>(a, partials, n_lists, st);
-    case 256: return launch_ts_t<256, 1, false>(a, partials, n_lists, st);
-    case 192: return launch_ts_t<192, 2, false>(a, partials, n_lists, st);
-    case 208: return launch_ts_t<208, 2, false>(a, partials, n_lists, st);
-    default: return launch_ts_t<224, 2, true>(a, partials, n_lists, st);
-  }
+  return ts_bn(a.dim) == 208 ? launch_ts_t<208>(a, partials, n_lists, st)
+                             : launch_ts_t<192>(a, partials, n_lists, st);
 }
 
 }  // namespace ss

@@ -111,8 +111,6 @@ struct ss_bank {
   int* d_err = nullptr;
   void* ws = nullptr;
   size_t ws_bytes = 0;
-  uint32_t* gthr = nullptr;  // per-query shared k-th-key bound for the top-k slices
-  int64_t gthr_cap = 0;
   uint32_t* gslots = nullptr;  // TS kernel pure top-k: per-slice published bounds
   int64_t gslots_cap = 0;
   int8_t* qscratch = nullptr;  // 128 x dim: single-tile query spread (k_topk_tc)
@@ -139,40 +137,17 @@ struct ss_bank {
   cudaStream_t cap_stream = nullptr;
 };
 
-// grow-on-demand (call once outside CUDA-graph capture); nullptr on failure
-// simply disables the cross-slice threshold sharing
-static uint32_t* gthr_reserve(ss_bank* h, int64_t nq) {
-  // cross-slice R-th-best sharing in the tcgen05 top-k: correct, but measured
-  // slower than independent slices (profiles/ROUND1.md), so opt-in via
-  // SS_TC_GTHR=1
-  static const bool on = getenv("SS_TC_GTHR") && atoi(getenv("SS_TC_GTHR")) == 1;
-  if (!on) return nullptr;
-  nq *= kMaxShareSlices + 1;
-  if (nq <= h->gthr_cap) return h->gthr;
-  if (h->gthr) cudaFree(h->gthr);
-  h->gthr = nullptr;
-  h->gthr_cap = 0;
-  int64_t want = nq + nq / 4 + 64;
-  if (cudaMalloc(&h->gthr, (size_t)want * sizeof(uint32_t)) != cudaSuccess) {
-    cudaGetLastError();
-    h->gthr = nullptr;
-    return nullptr;
-  }
-  h->gthr_cap = want;
-  return h->gthr;
-}
-
 // per-slice published bounds for the TS kernel in pure top-k mode (theta <=
-// 0); SS_TC_SHARE=0 disables.  Grow-on-demand outside graph capture, like the
-// workspace; nullptr simply disables the sharing.
+// 0).  Grow-on-demand outside graph capture, like the workspace; nullptr
+// simply disables the sharing.
 static uint32_t* gslots_reserve(ss_bank* h, int64_t nq, float theta) {
-  static const bool off = getenv("SS_TC_SHARE") && atoi(getenv("SS_TC_SHARE")) == 0;
-  if (off || !(theta <= 0.f)) return nullptr;
+  if (!(theta <= 0.f)) return nullptr;
   const int64_t need = nq * kMaxShareSlices;
   if (need <= h->gslots_cap) return h->gslots;
   if (h->gslots) cudaFree(h->gslots);
   h->gslots = nullptr;
   h->gslots_cap = 0;
+  ++h->ws_gen;  // a captured host round baked the old pointer in: re-capture
   if (cudaMalloc(&h->gslots, (size_t)need * sizeof(uint32_t)) != cudaSuccess) {
     cudaGetLastError();
     return nullptr;
@@ -202,7 +177,7 @@ int ss_version(void) { return 10000; }
 int64_t ss_launch_count(void) { return g_launches.load(); }
 
 // ------------------------------------------------------------- compat -----
-int ss_match_pmfs(const float* sims, int64_t nq, int64_t nw, const int64_t* lens, float theta,
+int ss_match_pmfs(const float* sims, int64_t nq, int64_t nw, const int64_t* lens, double theta,
                   int64_t max_len, double* sup, double* mas, int64_t* sizes, int64_t out_stride,
                   void* stream) {
   if (nq < 0 || nw < 0 || max_len < 1 || out_stride < max_len)
@@ -336,7 +311,6 @@ int ss_bank_destroy(ss_bank_t* h) {
   cudaFree(h->len_cnt);
   cudaFree(h->d_err);
   cudaFree(h->ws);
-  cudaFree(h->gthr);
   cudaFree(h->gslots);
   cudaFree(h->qscratch);
   if (h->host_exec) cudaGraphExecDestroy(h->host_exec);
@@ -449,7 +423,6 @@ static int topk_impl(ss_bank* h, const int8_t* q, const float* q_inv, int64_t nq
   TopkArgs a{q, q_inv, nq, h->emb, h->inv, h->cap, h->dim, k, theta, h->head, h->gcap,
              h->slot_offset};
   a.inv_padded = true;  // the bank pads inv with one NaN tile
-  a.gthr = gthr_reserve(h, nq);
   a.gslots = gslots_reserve(h, nq, theta);
   a.qscratch = h->qscratch;
   int slices = 1;
@@ -488,6 +461,25 @@ int ss_topk_scatter(ss_bank_t* h, const int8_t* q, const float* q_inv, int64_t n
     po.comp[r] = peer_comp_host[r];
     po.len[r] = peer_len_host[r];
   }
+  return topk_impl(h, q, q_inv, nq, k, theta, algo, nullptr, nullptr, 0, (cudaStream_t)stream, &po);
+}
+
+int ss_topk_gather(ss_bank_t* h, const int8_t* q, const float* q_inv, int64_t nq, int32_t k,
+                   float theta, int32_t algo, int32_t world, int32_t rank, uint64_t* owner_comp,
+                   int32_t* owner_len, void* stream) {
+  if (!h || !owner_comp || !owner_len) return set_error(SS_ERR_ARG, "topk_gather: null args");
+  if (world < 1 || rank < 0 || rank >= world || nq < 0)
+    return set_error(SS_ERR_ARG, "topk_gather: bad world/rank/nq (%d, %d, %lld)", world, rank,
+                     (long long)nq);
+  if (nq == 0) return SS_OK;
+  // every query belongs to the one owner: owner index q / nq == 0 in the merge
+  // kernel's exchange epilogue, row [rank][q] of the owner's buffer
+  PeerOut po{};
+  po.world = world;
+  po.rank = rank;
+  po.nq_local = nq;
+  po.comp[0] = owner_comp;
+  po.len[0] = owner_len;
   return topk_impl(h, q, q_inv, nq, k, theta, algo, nullptr, nullptr, 0, (cudaStream_t)stream, &po);
 }
 
@@ -538,7 +530,6 @@ int ss_topk_partials(ss_bank_t* h, const int8_t* q, const float* q_inv, int64_t 
   TopkArgs a{q, q_inv, nq, h->emb, h->inv, h->cap, h->dim, k, theta, h->head, h->gcap,
              h->slot_offset};
   a.inv_padded = true;  // the bank pads inv with one NaN tile
-  a.gthr = gthr_reserve(h, nq);
   a.gslots = gslots_reserve(h, nq, theta);
   a.qscratch = h->qscratch;
   int slices = 1;
@@ -644,7 +635,6 @@ static int round_impl(ss_bank* h, const int8_t* q, const float* q_inv, const int
   TopkArgs a{q, q_inv, nq, h->emb, h->inv, h->cap, h->dim, k, theta, h->head, h->gcap,
              h->slot_offset};
   a.inv_padded = true;  // the bank pads inv with one NaN tile
-  a.gthr = gthr_reserve(h, nq);
   a.gslots = gslots_reserve(h, nq, theta);
   a.qscratch = h->qscratch;
   int slices = 1;

@@ -36,7 +36,7 @@ int sm_count(int device);
 int pick_slices(int64_t qtiles, int64_t tiles, int sms);
 
 int launch_match_pmfs(const float* sims, int64_t nq, int64_t nw, const int64_t* lens,
-                      float theta, int64_t max_len, double* sup, double* mas,
+                      double theta, int64_t max_len, double* sup, double* mas,
                       int64_t* sizes, int64_t out_stride, int* err, cudaStream_t st);
 int launch_gittins_dist(const double* support, const double* masses, const int64_t* npts,
                         const double* attained, const double* outlived, int64_t n,
@@ -69,10 +69,6 @@ struct TopkArgs {
   int k;
   float theta;
   int64_t head, gcap, slot_offset;  // rel = (slot_offset + j - head) mod gcap
-  // optional [nq] scratch: per-query best known lower bound of the global k-th
-  // key (orderable bits), shared by all slices so each slice filters with the
-  // tightest threshold any slice has proven
-  uint32_t* gthr = nullptr;  // [slices][nq], slices <= kMaxShareSlices
   // inv is followed by at least one tile (256 floats) of NaN padding, so a
   // whole tile's inverse norms may be bulk-copied (the bank allocates it so)
   bool inv_padded = false;
@@ -96,9 +92,6 @@ bool topk_tc_supported(const TopkArgs& a);
 bool topk_ts_supported(const TopkArgs& a);
 int topk_ts_lists(const TopkArgs& a, int device);
 int launch_topk_ts(const TopkArgs& a, uint64_t* partials, int n_lists, cudaStream_t st);
-// CTA-pair tcgen05 kernel with the 8-warp epilogue (k_topk_pair.cu)
-bool topk_pair_supported(const TopkArgs& a);
-int topk_pair_lists(const TopkArgs& a, int device);
 
 // Receive buffers of every rank for the fused merge + exchange (k_merge with
 // po.world > 0): rank r's [world][nq_local][k] rows, IPC-mapped into this process.

@@ -265,6 +265,25 @@ class SageScheduler:
         hc = self._host_call
         if (hc is None or hc[2] != sp or hc[3] != key or hc[4] != self.window.handle
                 or any(x is not y for x, y in zip(bufs, hc[0]))):
+            # the C ABI reads raw pointers: check each buffer's dtype, layout
+            # and length once per argument tuple (a silent mismatch, e.g. an
+            # int64 input_len, would otherwise be read as wrong values)
+            dim = self.window.dim
+            want = (("q", q, np.int8, (n, dim)), ("q_inv", q_inv, np.float32, (n,)),
+                    ("input_len", input_len, np.int32, (n,)), ("ids", ids, np.int64, (n,)),
+                    ("G_out", G_out, np.float64, (n,)), ("perm_out", perm_out, np.int64, (n,)))
+            for name, a, dt, shape in want:
+                if a is None and name == "ids":
+                    continue
+                if not isinstance(a, np.ndarray):
+                    raise TypeError(f"{name} must be a numpy array, got {type(a).__name__}")
+                if a.dtype != dt or tuple(a.shape) != shape or not a.flags["C_CONTIGUOUS"]:
+                    raise ValueError(f"{name}: need a C-contiguous {np.dtype(dt).name} array of shape "
+                                     f"{shape}, got {a.dtype} {tuple(a.shape)}"
+                                     f"{'' if a.flags['C_CONTIGUOUS'] else ' (not contiguous)'}")
+                if name in ("G_out", "perm_out") and not a.flags["WRITEABLE"]:
+                    raise ValueError(f"{name} must be writeable")
+
             def hp(a):
                 return None if a is None else a.ctypes.data
 

@@ -3,30 +3,29 @@
 One process per GPU (torch.distributed, NCCL over NVLink on the box; gloo in
 the CPU tests).  The global FIFO ring of ``global_capacity`` slots is split
 into contiguous shards: rank r owns global slots [r*L, (r+1)*L), L =
-global_capacity / world.  Every rank owns its own queue of pending requests
-(one scheduler per GPU, "multiple concurrent schedulers"), so a
-round is weak-scaled: each rank contributes nq requests.
+global_capacity / world.  Only stage 1 (similarity + top-k) is partitioned.
 
-Per round (only stage 1 is partitioned; stages 2-4 run on the queue owner):
-  1. all-gather the queries of every rank's queue            (NCCL all_gather)
-  2. local top-k of all world*nq queries against the local shard, fused in
-     the tcgen05 kernel, with the candidates' lengths attached (ss_topk)
-  3. exchange: rank r receives, from every shard, the k candidates of its own
-     queries                                                   (NCCL all_to_all)
-  4. merge world x k candidates per query into the global top-k (ss_merge_topk)
+Single-owner round (the default, ``owner=0``; north star "the rest runs on
+the rank owning the queue", SPEC.md:468-470 orders every pending request in
+one total order):
+  1. broadcast the owner's queue (queries + inverse norms)     (NCCL broadcast)
+  2. local fused top-k of all nq queries against the local shard (ss_topk)
+  3. all-gather of k candidates per query to the owner         (NCCL all_gather)
+     -- or, ``exchange="p2p"``, the local merge kernel stores its rows
+     straight into the owner's IPC-mapped receive buffer (ss_topk_gather)
+  4. owner: merge world x k candidates per query into the global top-k
   5. fallback histogram: per-shard exact integer histograms summed
-                                                               (NCCL all_reduce)
-  6. histogram -> cost -> Gittins (ss_finish) and rank (ss_rank) for the queue.
+                                                                (NCCL all_reduce)
+  6. owner: histogram -> cost -> Gittins (ss_finish) and rank (ss_rank) of the
+     whole queue.
+Per-rank queues (``owner=None``; "multiple concurrent
+schedulers") keep the earlier weak-scaled form: every rank brings nq requests,
+the queries are all-gathered, each shard scores all of them, an all-to-all
+returns every query's candidates to its owner, which merges, finishes and
+ranks its own queue.
+
 Composites carry the global ring rank (slot - head) mod C, so tie-breaking by
 insertion_seq is identical to the single-GPU round.
-
-With ``exchange="p2p"`` stages 2 and 3 are one kernel sequence: the local
-merge kernel stores every merged row directly into its owner's receive buffer
-(``ss_topk_scatter``; the buffers are cudaMalloc'd, IPC-exported and mapped by
-every rank of the node, so the stores travel over NVLink), and a 1-element
-NCCL all_reduce is the barrier before the owners merge.  The next round's
-query all-gather orders the peers' reads of a receive buffer before it is
-overwritten, so one buffer per queue size suffices.
 """
 
 from __future__ import annotations
@@ -70,6 +69,27 @@ class ShardPlan:
         gslot = seq % self.global_capacity
         mine = (gslot // self.local_capacity) == self.rank
         return idx[mine], seq[mine], gslot[mine] - self.slot_offset
+
+
+def broadcast_queries(q: torch.Tensor, q_inv: torch.Tensor, owner: int, group=None):
+    """The owner's queue to every rank, in place (q/q_inv are the owner's
+    inputs there and same-shaped receive buffers elsewhere)."""
+    dist.broadcast(q, src=owner, group=group)
+    dist.broadcast(q_inv, src=owner, group=group)
+    return q, q_inv
+
+
+def gather_candidates(comp: torch.Tensor, ln: torch.Tensor, group=None):
+    """comp/ln [nq, k] (this shard's merged candidates for the owner's queue)
+    -> [world, nq, k] of every shard's lists (the north star's all-gather of
+    k candidates per query; only the owner reads the result)."""
+    world = dist.get_world_size(group)
+    nq, k = comp.shape
+    out_c = torch.empty((world * nq, k), dtype=comp.dtype, device=comp.device)
+    out_l = torch.empty((world * nq, k), dtype=ln.dtype, device=ln.device)
+    dist.all_gather_into_tensor(out_c, comp.contiguous(), group=group)
+    dist.all_gather_into_tensor(out_l, ln.contiguous(), group=group)
+    return out_c.view(world, nq, k), out_l.view(world, nq, k)
 
 
 def gather_queries(q: torch.Tensor, q_inv: torch.Tensor, group=None):
@@ -197,6 +217,20 @@ class PeerExchange:
         dist.all_reduce(self.flag, group=self.group)  # every shard's rows are stored
         return b["recv_c"], b["recv_l"]
 
+    def gather_topk(self, window, q, qi, cfg, owner: int):
+        """Single-owner form: this shard's merged top-k of the owner's whole
+        queue stored at [rank] of the owner's receive buffer; then the
+        barrier.  -> (comp, len) [world, nq, k] (meaningful on the owner)."""
+        from . import _lib
+
+        nq = q.shape[0]
+        b = self.buffers(nq)
+        _lib.call("ss_topk_gather", window.handle, _lib.ptr(q), _lib.ptr(qi), nq, self.k,
+                  float(np.float32(cfg.theta)), _lib.ALGO[cfg.algo], self.world, self.rank,
+                  b["comp_t"][owner], b["len_t"][owner], _lib.stream_ptr())
+        dist.all_reduce(self.flag, group=self.group)  # every shard's rows are stored
+        return b["recv_c"], b["recv_l"]
+
     def close(self):
         from . import _lib
 
@@ -211,25 +245,46 @@ class PeerExchange:
 class ShardedScheduler:
     """The scheduling round of SageScheduler, with stage 1 sharded.
 
-    Round buffers are allocated once per queue size (so a round can be
-    captured in a CUDA graph, NCCL collectives included), and the window's
-    fallback histogram is all-reduced asynchronously while the queries are
-    gathered and scored."""
+    ``owner`` = the rank that holds the queue and runs stages 2-4 for all of
+    it (single-owner round), or None for per-rank queues.  Round buffers are
+    allocated once per queue size (so a round can be captured in a CUDA
+    graph, NCCL collectives included), and the window's fallback histogram is
+    all-reduced asynchronously while the queries are scored.
 
-    def __init__(self, history: ShardedHistory, cfg, exchange: str = "nccl"):
+    The local stages are methods (``_local_topk``, ``_merge``, ``_finish``,
+    ``_rank``, ``_fallback_hist``) around one collective choreography, so the
+    CPU tests drive the same choreography over gloo with CPU restatements in their
+    place."""
+
+    def __init__(self, history: ShardedHistory, cfg, exchange: str = "nccl", owner: int | None = 0):
         if exchange not in ("nccl", "p2p"):
             raise ValueError(f"exchange must be 'nccl' or 'p2p', got {exchange!r}")
         self.h = history
         self.cfg = cfg
         self.group = history.group
+        self.world = dist.get_world_size(self.group)
+        self.rank = dist.get_rank(self.group)
+        if owner is not None and not 0 <= int(owner) < self.world:
+            raise ValueError(f"owner rank {owner} outside [0, {self.world})")
+        self.owner = None if owner is None else int(owner)
+        self.exchange = exchange
         self._bufs = {}
+        self._host = {}
         self._side = None
         self.peer = PeerExchange(cfg.k, self.group) if exchange == "p2p" else None
+
+    @property
+    def is_owner(self) -> bool:
+        return self.owner is None or self.rank == self.owner
+
+    # -- local stages (CUDA kernels through the C ABI) -----------------------
+    def _device(self):
+        return "cuda"
 
     def _buffers(self, nq: int):
         b = self._bufs.get(nq)
         if b is None:
-            c, d, P = self.cfg, "cuda", self.cfg.nbins
+            c, d, P = self.cfg, self._device(), self.cfg.nbins
             b = dict(comp=torch.empty((nq, c.k), dtype=torch.int64, device=d),
                      len=torch.empty((nq, c.k), dtype=torch.int32, device=d),
                      npts=torch.zeros(nq, dtype=torch.int32, device=d),
@@ -238,101 +293,176 @@ class ShardedScheduler:
                      pD=torch.zeros((nq, P), dtype=torch.int64, device=d),
                      used_fb=torch.zeros(nq, dtype=torch.uint8, device=d),
                      G=torch.empty(nq, dtype=torch.float64, device=d),
-                     perm=torch.empty(nq, dtype=torch.int64, device=d))
+                     perm=torch.empty(nq, dtype=torch.int64, device=d),
+                     q=torch.zeros((nq, self.h.window.dim), dtype=torch.int8, device=d),
+                     qi=torch.zeros(nq, dtype=torch.float32, device=d))
             self._bufs[nq] = b
         return b
 
-    def schedule_round(self, q, q_inv, input_len, ids=None):
-        from . import _lib
-        from .scheduler import rank as _rank
-
+    def _fallback_hist_async(self):
+        """Window law of this shard + its all-reduce, on a side stream (it
+        overlaps the scoring); returns (fb, join) -- join() orders the main
+        stream after the reduced histogram."""
         c = self.cfg
-        nq = q.shape[0]
-        out = self._buffers(nq)
-        # 5, overlapped: the window's fallback histogram and its all-reduce run
-        # on a side stream while the queries are gathered and scored
         if self._side is None:
             self._side = torch.cuda.Stream()
         main = torch.cuda.current_stream()
         self._side.wait_stream(main)
         with torch.cuda.stream(self._side):
             fb = self.h.window.fallback_hist(c.max_len, c.nbins, stream=self._side)
-            fb_work = dist.all_reduce(fb, op=dist.ReduceOp.SUM, group=self.group, async_op=True)
-        q_all, qi_all = gather_queries(q, q_inv, self.group)                    # 1
-        if self.peer is not None:                                               # 2+3 fused
-            comp_x, len_x = self.peer.scatter_topk(self.h.window, q_all, qi_all, c)
-        else:
-            comp_all, len_all = self.h.window.topk(q_all, qi_all, c.k, c.theta, c.algo)  # 2
-            comp_x, len_x = exchange_candidates(comp_all, len_all, self.group)  # 3
-        world = comp_x.shape[0]
-        comp, ln = out["comp"], out["len"]
-        _lib.call("ss_merge_topk", _lib.ptr(comp_x), _lib.ptr(len_x), world, nq, c.k,
-                  _lib.ptr(comp), _lib.ptr(ln), _lib.stream_ptr())              # 4
-        with torch.cuda.stream(self._side):
-            fb_work.wait()
-        main.wait_stream(self._side)
-        P = c.nbins
-        I = torch.as_tensor(input_len, device="cuda").to(torch.int32)
+            work = dist.all_reduce(fb, op=dist.ReduceOp.SUM, group=self.group, async_op=True)
+
+        def join():
+            with torch.cuda.stream(self._side):
+                work.wait()
+            main.wait_stream(self._side)
+        return fb, join
+
+    def _local_topk(self, q, qi):
+        c = self.cfg
+        return self.h.window.topk(q, qi, c.k, c.theta, c.algo)
+
+    def _merge(self, comp_x, len_x, comp, ln):
+        from . import _lib
+        _lib.call("ss_merge_topk", _lib.ptr(comp_x), _lib.ptr(len_x), comp_x.shape[0],
+                  comp.shape[0], self.cfg.k, _lib.ptr(comp), _lib.ptr(ln), _lib.stream_ptr())
+
+    def _finish(self, comp, ln, I, fb, out):
+        from . import _lib
+        c, nq = self.cfg, comp.shape[0]
         _lib.call("ss_finish", _lib.ptr(comp), _lib.ptr(ln), nq, c.k, c.min_matches, c.max_len,
-                  c.nbins, _lib.ptr(I), _lib.ptr(fb[0]), _lib.ptr(fb[1]), _lib.ptr(fb[2]), P,
+                  c.nbins, _lib.ptr(I), _lib.ptr(fb[0]), _lib.ptr(fb[1]), _lib.ptr(fb[2]), c.nbins,
                   _lib.ptr(out["npts"]), _lib.ptr(out["pbin"]), _lib.ptr(out["pcnt"]),
                   _lib.ptr(out["pD"]), None, _lib.ptr(out["used_fb"]), _lib.ptr(out["G"]),
-                  _lib.stream_ptr())                                            # 6
-        perm = _rank(out["G"], None if ids is None else torch.as_tensor(ids, device="cuda"),
-                     out["perm"])
+                  _lib.stream_ptr())
+
+    def _rank(self, G, ids, perm):
+        from .scheduler import rank as _rank
+        return _rank(G, ids, perm)
+
+    # -- the round -------------------------------------------------------------
+    def schedule_round(self, q, q_inv, input_len=None, ids=None, nq: int | None = None):
+        """One round.  Single-owner: every rank calls it; the owner passes its
+        queue (q, q_inv, input_len, ids), the other ranks pass q=None and the
+        queue size ``nq`` (or same-shaped placeholders).  Returns
+        (perm, G, out) on the owner and None elsewhere.  Per-rank queues:
+        every rank passes its own queue and gets its own result."""
+        if self.owner is None:
+            return self._per_rank_round(q, q_inv, input_len, ids)
+        dev = self._device()
+        if q is not None:
+            nq = int(q.shape[0])
+        if nq is None:
+            raise ValueError("non-owner ranks must pass the queue size nq")
+        out = self._buffers(nq)
+        if self.rank == self.owner:
+            qb, qib = torch.as_tensor(q, device=dev), torch.as_tensor(q_inv, device=dev)
+        else:
+            qb, qib = out["q"], out["qi"]
+        fb, join = self._fallback_hist_async()                                  # 5 (overlapped)
+        broadcast_queries(qb, qib, self.owner, self.group)                      # 1
+        if self.peer is not None:                                               # 2+3 fused
+            comp_x, len_x = self.peer.gather_topk(self.h.window, qb, qib, self.cfg, self.owner)
+        else:
+            comp_l, len_l = self._local_topk(qb, qib)                           # 2
+            comp_x, len_x = gather_candidates(comp_l, len_l, self.group)        # 3
+        join()
+        if self.rank != self.owner:
+            return None
+        comp, ln = out["comp"], out["len"]
+        self._merge(comp_x, len_x, comp, ln)                                    # 4
+        I = torch.as_tensor(input_len, device=dev).to(torch.int32)
+        self._finish(comp, ln, I, fb, out)                                      # 6
+        perm = self._rank(out["G"], None if ids is None else torch.as_tensor(ids, device=dev),
+                          out["perm"])
         return perm, out["G"], out
 
-    def schedule_round_host(self, q, q_inv, input_len, ids, G_out, perm_out):
+    def _per_rank_round(self, q, q_inv, input_len, ids):
+        nq = q.shape[0]
+        out = self._buffers(nq)
+        fb, join = self._fallback_hist_async()                                  # 5 (overlapped)
+        q_all, qi_all = gather_queries(q, q_inv, self.group)                    # 1
+        if self.peer is not None:                                               # 2+3 fused
+            comp_x, len_x = self.peer.scatter_topk(self.h.window, q_all, qi_all, self.cfg)
+        else:
+            comp_all, len_all = self._local_topk(q_all, qi_all)                 # 2
+            comp_x, len_x = exchange_candidates(comp_all, len_all, self.group)  # 3
+        comp, ln = out["comp"], out["len"]
+        self._merge(comp_x, len_x, comp, ln)                                    # 4
+        join()
+        I = torch.as_tensor(input_len, device=self._device()).to(torch.int32)
+        self._finish(comp, ln, I, fb, out)                                      # 6
+        perm = self._rank(out["G"], None if ids is None else torch.as_tensor(ids, device="cuda"),
+                          out["perm"])
+        return perm, out["G"], out
+
+    def schedule_round_host(self, q, q_inv, input_len, ids, G_out, perm_out, nq: int | None = None):
         """The round from (pinned) host buffers, as an engine calls it once per
-        iteration: H2D of this rank's queue into static device buffers, the
-        captured round (collectives included), D2H of the index and order
-        into ``G_out`` / ``perm_out``, synchronise.  Collective: every rank
-        calls it with the same queue size.  The first call per queue size
-        captures the round (eager rounds if capture is unavailable)."""
-        t = [x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x))
-             for x in (q, q_inv, input_len, ids)]
-        nq = t[0].shape[0]
-        if not hasattr(self, "_host"):
-            self._host = {}
-        st = self._host.get(nq)
+        iteration: H2D of the queue into static device buffers, the captured
+        round (collectives included), D2H of the index and order into
+        ``G_out`` / ``perm_out``, synchronise.  Collective: every rank calls
+        it (single-owner: non-owners pass None for the buffers and the queue
+        size ``nq``).  The round is captured per (queue size, bank head): the
+        kernels take the ring head as a launch scalar, so a push re-captures."""
+        have = q is not None
+        t = ([x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x))
+              for x in (q, q_inv, input_len)] if have else [])
+        has_ids = have and ids is not None
+        if has_ids:
+            t.append(ids if isinstance(ids, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(ids)))
+        if have:
+            nq = int(t[0].shape[0])
+        if nq is None:
+            raise ValueError("non-owner ranks must pass the queue size nq")
+        key = (nq, self.h.head, has_ids)
+        st = self._host.get(key)
         if st is None:
+            self._host = {k: v for k, v in self._host.items() if k[0] != nq}  # drop stale heads
             dev = [torch.empty(x.shape, dtype=x.dtype, device="cuda") for x in t]
             for d, x in zip(dev, t):
                 d.copy_(x)
+            args = self._round_args(dev, has_ids, nq)
             try:
-                g, res = self.capture_round(*dev)
+                g, res = self.capture_round(*args[0], **args[1])
             except Exception:  # noqa: BLE001 -- NCCL without graph support: eager rounds
                 torch.cuda.synchronize()
                 g, res = None, None
-            st = self._host[nq] = (dev, g, res)
+            st = self._host[key] = (dev, g, res)
         dev, g, res = st
         for d, x in zip(dev, t):
             d.copy_(x, non_blocking=True)
         if g is not None:
             g.replay()
-            perm, G, _ = res
         else:
-            perm, G, _ = self.schedule_round(*dev)
-        G_out.copy_(G, non_blocking=True)
-        perm_out.copy_(perm, non_blocking=True)
+            a, kw = self._round_args(dev, has_ids, nq)
+            res = self.schedule_round(*a, **kw)
+        if res is not None:
+            perm, G, _ = res
+            G_out.copy_(G, non_blocking=True)
+            perm_out.copy_(perm, non_blocking=True)
         torch.cuda.current_stream().synchronize()
         return perm_out, G_out
+
+    def _round_args(self, dev, has_ids, nq):
+        if not dev:
+            return (None, None, None, None), {"nq": nq}
+        return (dev[0], dev[1], dev[2], dev[3] if has_ids else None), {}
 
     def close(self):
         """Release the P2P receive buffers and peer mappings (if any)."""
         if self.peer is not None:
             self.peer.close()
 
-    def capture_round(self, q, q_inv, input_len, ids=None, warmup: int = 2):
+    def capture_round(self, q, q_inv, input_len=None, ids=None, warmup: int = 2, nq=None):
         """CUDA-graph the sharded round (collectives included) for fixed input
-        buffers; returns (graph, (perm, G, out)).  Every rank must capture."""
+        buffers; returns (graph, result).  Every rank must capture."""
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(s):
             for _ in range(warmup):
-                self.schedule_round(q, q_inv, input_len, ids)
+                self.schedule_round(q, q_inv, input_len, ids, nq=nq)
         torch.cuda.current_stream().wait_stream(s)
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
-            res = self.schedule_round(q, q_inv, input_len, ids)
+            res = self.schedule_round(q, q_inv, input_len, ids, nq=nq)
         return g, res

@@ -17,7 +17,8 @@ from __future__ import annotations
 import numpy as np
 import torch
 
-__all__ = ["centroids", "make_bank_device", "make_queries", "inv_norm_np", "inv_norm_device"]
+__all__ = ["centroids", "make_bank_device", "make_bank_host", "make_queries", "inv_norm_np",
+           "inv_norm_device"]
 
 
 def centroids(n_clusters: int, dim: int, seed: int) -> np.ndarray:
@@ -59,6 +60,28 @@ def make_bank_device(n: int, dim: int, n_clusters: int, seed: int, noise: float 
         lens[s:s + m] = torch.clamp(torch.round(ln), 1, max_len).to(torch.int32)
         cl_all[s:s + m] = cl
     return emb, lens, cl_all
+
+
+def make_bank_host(n: int, dim: int, n_clusters: int, seed: int, noise: float = 0.45,
+                   max_len: int = 2048, chunk: int = 1 << 17):
+    """The same recipe as make_bank_device with numpy on the host (the CPU
+    reference arm's bank: same clusters and length laws, numpy's stream of
+    members): (emb int8 [n, dim], lens int32 [n])."""
+    cent, mu = centroids(n_clusters, dim, seed)
+    rng = np.random.default_rng(seed + 1)
+    emb = np.empty((n, dim), dtype=np.int8)
+    lens = np.empty(n, dtype=np.int32)
+    for s in range(0, n, chunk):
+        m = min(chunk, n - s)
+        cl = rng.integers(0, n_clusters, m)
+        z = rng.standard_normal((m, dim), dtype=np.float32)
+        z /= np.linalg.norm(z, axis=1, keepdims=True)
+        x = cent[cl] + noise * z
+        x /= np.linalg.norm(x, axis=1, keepdims=True)
+        emb[s:s + m] = np.rint(127.0 * x / np.abs(x).max(axis=1, keepdims=True)).astype(np.int8)
+        ln = np.exp(mu[cl] + 0.5 * rng.standard_normal(m, dtype=np.float32))
+        lens[s:s + m] = np.clip(np.rint(ln), 1, max_len).astype(np.int32)
+    return emb, lens
 
 
 def inv_norm_np(emb: np.ndarray) -> np.ndarray:

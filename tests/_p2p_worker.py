@@ -1,10 +1,11 @@
 """Worker of test_gpu_parity.test_sharded_p2p_two_ranks_one_gpu (not a test module).
 
 Two ranks share cuda:0 (gloo carries the control collectives: NCCL refuses two
-ranks on one device).  Each rank holds half of the ring and its own queue; the
-round uses the fused P2P merge + exchange, whose stores cross the process
-boundary through the IPC mapping.  Every rank checks its queue's Gittins
-indices and order against the single-GPU round over the whole bank.
+ranks on one device).  Each rank holds half of the ring.  Mode "per-rank":
+each rank has its own queue; mode "owner" (argv[1]): rank 1 owns the whole
+queue.  The round uses the fused P2P merge + exchange, whose stores cross the
+process boundary through the IPC mapping.  Every queue owner checks its
+Gittins indices and order against the single-GPU round over the whole bank.
 """
 
 import os
@@ -37,18 +38,33 @@ def main():
     I = torch.as_tensor(np.random.default_rng(rank).integers(1, 4097, nq).astype(np.int32),
                         device="cuda")
     ids = torch.arange(rank * nq, (rank + 1) * nq, device="cuda")
-    ss = ShardedScheduler(sh, cfg, exchange="p2p")
+    mode = sys.argv[1] if len(sys.argv) > 1 else "per-rank"
+    if mode == "owner":  # rank 1 owns the whole queue (both halves)
+        q = torch.as_tensor(emb[n:n + world * nq], device="cuda")
+        qi = torch.as_tensor(O.inv_norm(emb[n:n + world * nq]), device="cuda")
+        I = torch.as_tensor(np.random.default_rng(7).integers(1, 4097, world * nq).astype(np.int32),
+                            device="cuda")
+        ids = torch.arange(world * nq, device="cuda")
+        ss = ShardedScheduler(sh, cfg, exchange="p2p", owner=1)
+    else:
+        ss = ShardedScheduler(sh, cfg, exchange="p2p", owner=None)
+    mine = mode != "owner" or rank == 1
     for _ in range(3):  # receive buffers reused across rounds
-        p1, G1, _ = ss.schedule_round(q, qi, I, ids)
+        if mine:
+            p1, G1, _ = ss.schedule_round(q, qi, I, ids)
+        else:
+            assert ss.schedule_round(None, None, nq=world * nq) is None
         torch.cuda.synchronize()
         dist.barrier()
-    # the peer's shard really delivered rows into this rank's receive buffer
-    recv = ss.peer.buffers(nq)["recv_c"]
-    delivered = bool(recv[1 - rank].ne(0).any()) and bool(recv[rank].ne(0).any())
-    w = HistoryWindow(n, dim)
-    w.push(emb[:n], lens[:n])
-    p0, G0, _ = SageScheduler(w, cfg).schedule_round(q, qi, I, ids)
-    ok = delivered and torch.equal(G1, G0) and torch.equal(p1, p0)
+    ok = True
+    if mine:
+        # the peer's shard really delivered rows into this rank's receive buffer
+        recv = ss.peer.buffers(q.shape[0])["recv_c"]
+        delivered = bool(recv[1 - rank].ne(0).any()) and bool(recv[rank].ne(0).any())
+        w = HistoryWindow(n, dim)
+        w.push(emb[:n], lens[:n])
+        p0, G0, _ = SageScheduler(w, cfg).schedule_round(q, qi, I, ids)
+        ok = delivered and torch.equal(G1, G0) and torch.equal(p1, p0)
     ss.peer.close()
     dist.barrier()
     dist.destroy_process_group()

@@ -34,6 +34,43 @@ def test_match_pmfs_bit_exact_vs_reference(cuda, golden):
         assert np.array_equal(mas[q, :k], g["mp_mas"][q, :k])
 
 
+def test_match_pmfs_theta_compared_in_f64(cuda, golden):
+    """A Python-float theta that is not an f32 value (0.7): numba promotes
+    the f32 sim to f64 for the compare, so a sim equal to f32(0.7) (just
+    below 0.7) does not match; an np.float32 theta matches it."""
+    from paper_2603_07917_b200 import _kernels
+    t32 = np.float32(0.7)
+    sims = np.array([[t32, np.nextafter(t32, np.float32(2)), np.float32(0.5)]], np.float32)
+    lens = np.array([3, 5, 9], np.int64)
+    for theta, want in ((0.7, [5]), (t32, [3, 5])):
+        sup = np.zeros((1, 16))
+        mas = np.zeros((1, 16))
+        sz = np.zeros(1, np.int64)
+        _kernels.match_pmfs(sims, lens, theta, 16, sup, mas, sz)
+        assert list(sup[0, :sz[0]]) == want, theta
+        ref = _ref_kernels()
+        if ref is not None:
+            s2, m2, z2 = np.zeros((1, 16)), np.zeros((1, 16)), np.zeros(1, np.int64)
+            ref.match_pmfs(sims, lens, theta, 16, s2, m2, z2)
+            assert np.array_equal(s2, sup) and np.array_equal(m2, mas) and np.array_equal(z2, sz)
+
+
+def _ref_kernels():
+    """The unmodified reference module when baseline/_ref is installed (numba)."""
+    import os
+    import sys
+    ref = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "baseline", "_ref")
+    if not os.path.isdir(ref):
+        return None
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    try:
+        from servesim import _kernels
+        return _kernels
+    except Exception:
+        return None
+
+
 def test_match_pmfs_out_of_range_len_raises(cuda):
     from paper_2603_07917_b200 import _kernels as K
     sims = np.ones((1, 3), np.float32)
@@ -225,7 +262,11 @@ def test_topk_pure_large_bank_bit_exact(cuda, theta):
 
 @pytest.mark.parametrize("algo", ["scan", "tcgen05"])
 def test_topk_edges(cuda, algo):
-    """ragged nq, partially filled ring, ties, degenerate query, k > rows."""
+    """ragged nq (1 and 3: the streaming tcgen05 kernel; 129: the A-in-TMEM
+    kernel with a one-query second tile), partially filled ring, exact
+    duplicates (ties broken by the larger insertion_seq), a
+    degenerate zero query, theta = 0.9, k > rows.  Only k > 64 leaves the
+    tcgen05 kernels (their heap capacity); everything else must run there."""
     from paper_2603_07917_b200.history import HistoryWindow
     rng = np.random.default_rng(11)
     dim = 384
@@ -234,23 +275,102 @@ def test_topk_edges(cuda, algo):
     L = rng.integers(1, 2049, 300).astype(np.int32)
     w = HistoryWindow(1000, dim)  # 700 empty slots
     w.push(base, L)
+    ran = 0
     for nq in (1, 3, 129):
         q = rng.integers(-20, 21, (nq, dim)).astype(np.int8)
         q[0] = base[5]
         if nq > 1:
             q[1] = 0  # degenerate (zero) query: no neighbours
+        if nq > 2:
+            q[2] = base[100]  # a duplicate of the query above: the same 11-way tie
         qi = O.inv_norm(q)
-        for k, theta in ((16, -1.0), (256, -1.0), (8, 0.9)):
-            try:
-                comp, _ = w.topk(q, qi, k, theta, algo)
-            except NotImplementedError:
-                pytest.skip(f"{algo} not available")
+        for k, theta in ((16, -1.0), (64, -1.0), (256, -1.0), (8, 0.9), (64, 0.9), (32, 0.0)):
+            if algo == "tcgen05" and k > 64:
+                with pytest.raises(NotImplementedError):
+                    w.topk(q, qi, k, theta, algo)
+                continue
+            comp, _ = w.topk(q, qi, k, theta, algo)
             keys = O.scores(q, qi, base, O.inv_norm(base))
             seq = np.arange(300)
             ref = [O.select_topk(keys[i], seq, k, theta) for i in range(nq)]
             _check_topk(w, comp, keys, seq, ref, k)
+            # the tie: the 11 identical rows come newest first
+            key0, gseq0, _ = w.decode(comp[:1])
+            assert gseq0[0, 0].item() == 109 and key0[0, 0].item() == pytest.approx(1.0, abs=1e-6)
             if nq > 1:
                 assert int((comp[1] != 0).sum()) == 0
+            ran += 1
+    assert ran == 3 * (5 if algo == "tcgen05" else 6)
+
+
+def _oracle_topk_chunked(q, qi, bank_emb_dev, bank_lens, k, theta, chunk=1 << 20):
+    """Exact oracle top-k of a few queries against a bank too large to score
+    whole on the host: per chunk, the rows at or above the chunk's k-th key
+    (ties included) go to a candidate pool, whose select_topk is the global
+    one (the pool holds every row of the global top-k)."""
+    n = bank_emb_dev.shape[0]
+    pool_k = [[] for _ in range(q.shape[0])]
+    pool_s = [[] for _ in range(q.shape[0])]
+    for s in range(0, n, chunk):
+        e = bank_emb_dev[s:s + chunk].cpu().numpy()
+        keys = O.scores(q, qi, e, O.inv_norm(e))
+        for i in range(q.shape[0]):
+            row = keys[i]
+            ok = np.flatnonzero(row >= np.float32(theta)) if theta > -1.0 else np.arange(row.size)
+            if ok.size > k:
+                kth = np.partition(-row[ok], k - 1)[k - 1]
+                ok = ok[-row[ok] <= kth]
+            pool_k[i].append(row[ok])
+            pool_s[i].append(ok + s)
+    out = []
+    for i in range(q.shape[0]):
+        kv, sv = np.concatenate(pool_k[i]), np.concatenate(pool_s[i])
+        sel = O.select_topk(kv, sv, k, theta)
+        out.append((sv[sel], kv[sel]))
+    return out
+
+
+@pytest.mark.parametrize("theta", [0.8, -1.0])
+def test_round_c4_shape_sampled(cuda, theta):
+    """BASELINE configs[3] on one GPU: a 16M-row bank and an 8192-request
+    round (64 query tiles, a multi-wave grid of the A-in-TMEM kernel).  For
+    32 sampled requests the neighbour lists (insertion_seq and key) and the
+    Gittins indices equal the oracle's bit for bit; the permutation orders
+    every request by (G, id)."""
+    from paper_2603_07917_b200.history import HistoryWindow
+    from paper_2603_07917_b200.scheduler import RoundConfig, SageScheduler
+    from paper_2603_07917_b200.synthetic import make_bank_device, make_queries
+    n, dim, nq, k, nbins = 1 << 24, 384, 8192, 64, 128
+    emb, lens, _ = make_bank_device(n, dim, 4096, 0)
+    w = HistoryWindow(n, dim)
+    w.push(emb, lens)
+    bl = lens.cpu().numpy()
+    del lens
+    q, qi, I, ids = make_queries(nq, dim, 4096, 0, qseed=4000)
+    cfg = RoundConfig(k=k, theta=theta, min_matches=20, max_len=2048, nbins=nbins)
+    perm, G, _ = SageScheduler(w, cfg).schedule_round(_t(q), _t(qi), _t(I), _t(ids))
+    G, perm = G.cpu().numpy(), perm.cpu().numpy()
+    assert np.array_equal(perm, O.rank(G, ids))
+    comp, ln = w.topk(q, qi, k, theta)
+    key, gseq, _ = w.decode(comp)
+    key, gseq, ln = key.cpu().numpy(), gseq.cpu().numpy(), ln.cpu().numpy()
+    smp = np.sort(np.random.default_rng(5).choice(nq, 32, replace=False))
+    ref = _oracle_topk_chunked(q[smp], qi[smp], emb, bl, k, theta)
+    del emb
+    fb = O.bin_hist(bl, 2048, nbins)
+    n_topk = 0
+    for j, i in enumerate(smp):
+        rs, rk = ref[j]
+        m = rs.size
+        assert np.array_equal(gseq[i, :m], rs) and np.array_equal(key[i, :m], rk), i
+        assert np.all(gseq[i, m:] == -1)
+        assert np.array_equal(ln[i, :m], bl[rs]), i
+        used_fb = m < 20
+        h = fb if used_fb else O.bin_hist(bl[rs], 2048, nbins)
+        _, c, D = O.hist_to_points(*h, I[i])
+        assert G[i] == O.gittins_points(c, D), i
+        n_topk += not used_fb
+    assert n_topk >= 16  # the top-k path, not only the fallback
 
 
 # ------------------------------------------------- full round (stages 1-4) --
@@ -600,15 +720,20 @@ def test_rank_special_values(cuda, n):
 
 
 # ---------------------------------------------------- sharded round (N=1) ---
+@pytest.mark.parametrize("owner", [0, None])
 @pytest.mark.parametrize("exchange", ["nccl", "p2p"])
-def test_sharded_round_world1_equals_single_gpu(cuda, exchange):
-    """The multi-GPU round (query all-gather, candidate all-to-all or the fused
-    P2P merge + exchange, merge, histogram all-reduce) run as a 1-rank NCCL
-    group equals the fused single-GPU round bit for bit."""
+def test_sharded_round_world1_equals_single_gpu(cuda, exchange, owner):
+    """The multi-GPU round run as a 1-rank NCCL group equals the fused
+    single-GPU round bit for bit: single owner (query broadcast, local top-k,
+    candidate all-gather or the fused P2P gather, merge, histogram
+    all-reduce) and per-rank queues (query all-gather, all-to-all or P2P
+    scatter).  The host-buffer call is replayed from its captured graph, and
+    a push between two host calls (the ring head moves) is honoured."""
     import socket
 
     import torch.distributed as dist
 
+    from paper_2603_07917_b200.history import HistoryWindow
     from paper_2603_07917_b200.scheduler import RoundConfig, SageScheduler
     from paper_2603_07917_b200.sharded import ShardedHistory, ShardedScheduler
     with socket.socket() as s:
@@ -617,15 +742,15 @@ def test_sharded_round_world1_equals_single_gpu(cuda, exchange):
     dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
                             device_id=torch.device("cuda:0"))
     try:
-        n, dim, nq = 20_000, 384, 200
-        emb, lens, _, _ = O.make_bank(n + nq, dim, 50, 9)
+        n, dim, nq, extra = 20_000, 384, 200, 300
+        emb, lens, _, _ = O.make_bank(n + nq + extra, dim, 50, 9)
         cfg = RoundConfig(k=32, theta=0.8, nbins=64)
         sh = ShardedHistory(n, dim)
         sh.push(torch.as_tensor(emb[:n], device="cuda"), torch.as_tensor(lens[:n], device="cuda"))
-        q, qi = emb[n:], O.inv_norm(emb[n:])
+        q, qi = emb[n:n + nq], O.inv_norm(emb[n:n + nq])
         I = np.random.default_rng(0).integers(1, 4097, nq).astype(np.int32)
         ids = np.arange(nq)
-        ss = ShardedScheduler(sh, cfg, exchange=exchange)
+        ss = ShardedScheduler(sh, cfg, exchange=exchange, owner=owner)
         p1, G1, _ = ss.schedule_round(_t(q), _t(qi), _t(I), _t(ids))
         p1, G1 = p1.clone(), G1.clone()
         # the host-buffer call (captured round + copies), twice: same answer
@@ -637,15 +762,60 @@ def test_sharded_round_world1_equals_single_gpu(cuda, exchange):
             ss.schedule_round_host(q, qi, I, ids.astype(np.int64), hG, hp)
             assert torch.equal(hG, G1.cpu()) and torch.equal(hp, p1.cpu())
         if ss.peer is not None:
-            p1, G1 = p1.clone(), G1.clone()
             p1b, G1b, _ = ss.schedule_round(_t(q), _t(qi), _t(I), _t(ids))  # buffers reused
             assert torch.equal(G1b, G1) and torch.equal(p1b, p1)
-            ss.peer.close()
-        w, *_ = _bank(n, dim, 50, 9, nq)
+        w = HistoryWindow(n, dim)
+        w.push(emb[:n], lens[:n])
         p0, G0, _ = SageScheduler(w, cfg).schedule_round(_t(q), _t(qi), _t(I), _t(ids))
         assert torch.equal(G1, G0) and torch.equal(p1, p0)
+        # rolling inserts (wrap the ring by `extra` rows, identical prompts
+        # among them so the insertion_seq tie rule matters): the host call
+        # re-captures for the new head and still equals the single-GPU round
+        new_e = emb[n + nq:n + nq + extra].copy()
+        new_e[: nq // 2] = q[: nq // 2]  # exact duplicates of queries -> ties on cos 1.0
+        new_l = lens[n + nq:n + nq + extra]
+        sh.push(torch.as_tensor(new_e, device="cuda"), torch.as_tensor(new_l, device="cuda"))
+        w.push(new_e, new_l)
+        hG.zero_()
+        ss.schedule_round_host(q, qi, I, ids.astype(np.int64), hG, hp)
+        p2, G2, _ = SageScheduler(w, cfg).schedule_round(_t(q), _t(qi), _t(I), _t(ids))
+        assert torch.equal(hG, G2.cpu()) and torch.equal(hp, p2.cpu())
+        if ss.peer is not None:
+            ss.peer.close()
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_topk_gather_shards_equal_single_bank(cuda, world):
+    """ss_topk_gather addressing (single-owner exchange), all ranks simulated
+    in one process: every shard stores its merged rows for the owner's whole
+    queue at [r][q] of the owner's buffer; merging that buffer gives the
+    single-bank top-k, lengths included, bit for bit."""
+    from paper_2603_07917_b200 import _lib
+    from paper_2603_07917_b200.history import HistoryWindow
+    from paper_2603_07917_b200.sharded import ShardPlan
+    n, dim, nq, k = 9_000, 384, 150, 32
+    emb, lens, _, _ = O.make_bank(n + nq, dim, 40, 6)
+    q = _t(emb[n:])
+    qi = _t(O.inv_norm(emb[n:]))
+    recv_c = torch.full((world, nq, k), -7, dtype=torch.int64, device="cuda")
+    recv_l = torch.full((world, nq, k), -7, dtype=torch.int32, device="cuda")
+    for r in range(world):
+        plan = ShardPlan(n, world, r)
+        w = HistoryWindow(plan.local_capacity, dim, global_capacity=n, slot_offset=plan.slot_offset)
+        idx, seq, slot = plan.route(0, n)
+        w.write(_t(emb[idx]), _t(lens[idx]), _t(seq), _t(slot))
+        w.set_head(n)
+        _lib.call("ss_topk_gather", w.handle, _lib.ptr(q), _lib.ptr(qi), nq, k, 0.6, 0, world, r,
+                  _lib.ptr(recv_c), _lib.ptr(recv_l), _lib.stream_ptr())
+    out_c = torch.empty((nq, k), dtype=torch.int64, device="cuda")
+    out_l = torch.empty((nq, k), dtype=torch.int32, device="cuda")
+    _lib.call("ss_merge_topk", _lib.ptr(recv_c), _lib.ptr(recv_l), world, nq, k,
+              _lib.ptr(out_c), _lib.ptr(out_l), _lib.stream_ptr())
+    full, *_ = _bank(n, dim, 40, 6, nq)
+    c0, l0 = full.topk(q, qi, k, 0.6)
+    assert torch.equal(out_c, c0) and torch.equal(out_l, l0)
 
 
 @pytest.mark.parametrize("world,algo", [(2, "auto"), (3, "auto"), (2, "scan")])
@@ -692,9 +862,11 @@ def test_topk_scatter_shards_equal_single_bank(cuda, world, algo):
                   0.5, 0, world, 0, tc, tl, _lib.stream_ptr())
 
 
-def test_sharded_p2p_two_ranks_one_gpu(cuda):
+@pytest.mark.parametrize("mode", ["owner", "per-rank"])
+def test_sharded_p2p_two_ranks_one_gpu(cuda, mode):
     """World-2 round with the fused P2P merge + exchange, both ranks on cuda:0
-    (tests/_p2p_worker.py): each rank's result equals the single-GPU round."""
+    (tests/_p2p_worker.py): the queue owner's result equals the single-GPU
+    round (single owner: rank 1 holds the whole queue)."""
     import pathlib
     import socket
     import subprocess
@@ -705,7 +877,7 @@ def test_sharded_p2p_two_ranks_one_gpu(cuda):
         port = s.getsockname()[1]
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
                         "--nproc-per-node=2", "--master-addr=127.0.0.1", f"--master-port={port}",
-                        str(root / "tests" / "_p2p_worker.py")], cwd=str(root),
+                        str(root / "tests" / "_p2p_worker.py"), mode], cwd=str(root),
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, (r.stdout[-2000:], r.stderr[-4000:])
 

@@ -115,3 +115,134 @@ def test_gloo_world2_exchange_equals_global_topk():
         p.join(timeout=300)
     results = dict(q.get(timeout=10) for _ in range(2))
     assert results == {0: True, 1: True}
+
+
+# ------------------------------------------- single-owner round (gloo, CPU) ---
+class _FakeWindow:
+    def __init__(self, dim):
+        self.dim = dim
+
+
+class _FakeHistory:
+    """The shard as the oracle sees it (no GPU): rows [lo, hi) of the global bank."""
+
+    def __init__(self, bank_e, bank_l, lo, hi, head, cap):
+        self.group = None
+        self.window = _FakeWindow(bank_e.shape[1])
+        self.e, self.l, self.lo, self.hi = bank_e[lo:hi], bank_l[lo:hi], lo, hi
+        self.seq = np.arange(lo, hi)
+        self.head, self.cap = head, cap
+        self.all_l = bank_l
+
+
+def _oracle_sharded_cls():
+    from paper_2603_07917_b200.sharded import ShardedScheduler
+
+    class OracleSharded(ShardedScheduler):
+        """ShardedScheduler's own choreography (broadcast, all-gather,
+        all-reduce, owner-only stages) with the oracle as the local stages."""
+
+        def _device(self):
+            return "cpu"
+
+        def _fallback_hist_async(self):
+            c = self.cfg
+            fb = torch.as_tensor(np.stack(O.bin_hist(self.h.l, c.max_len, c.nbins)))
+            work = dist.all_reduce(fb, op=dist.ReduceOp.SUM, group=self.group, async_op=True)
+            return fb, work.wait
+
+        def _local_topk(self, q, qi):
+            c, h = self.cfg, self.h
+            q, qi = q.numpy(), qi.numpy()
+            keys = O.scores(q, qi, h.e, O.inv_norm(h.e))
+            comp = np.zeros((q.shape[0], c.k), np.uint64)
+            ln = np.zeros((q.shape[0], c.k), np.int32)
+            for i in range(q.shape[0]):
+                sel = O.select_topk(keys[i], h.seq, c.k, c.theta)
+                comp[i, :sel.size] = composites(keys[i], h.seq, sel, h.head, h.cap)
+                ln[i, :sel.size] = h.l[sel]
+            return torch.as_tensor(comp.view(np.int64)), torch.as_tensor(ln)
+
+        def _merge(self, comp_x, len_x, comp, ln):
+            cx = comp_x.numpy().view(np.uint64)
+            lx = len_x.numpy()
+            for i in range(comp.shape[0]):
+                allc, alll = cx[:, i, :].reshape(-1), lx[:, i, :].reshape(-1)
+                order = sorted(np.flatnonzero(allc), key=lambda j: -int(allc[j]))[:self.cfg.k]
+                row = np.zeros(self.cfg.k, np.uint64)
+                row[:len(order)] = allc[order]
+                comp[i] = torch.as_tensor(row.view(np.int64))
+                lr = np.zeros(self.cfg.k, np.int32)
+                lr[:len(order)] = alll[order]
+                ln[i] = torch.as_tensor(lr)
+
+        def _finish(self, comp, ln, I, fb, out):
+            c = self.cfg
+            fbn = tuple(fb.numpy())
+            for i in range(comp.shape[0]):
+                m = int((comp[i] != 0).sum())
+                used = m < c.min_matches
+                h = fbn if used else O.bin_hist(ln[i, :m].numpy(), c.max_len, c.nbins)
+                _, cc, D = O.hist_to_points(*h, int(I[i]))
+                out["G"][i] = O.gittins_points(cc, D)
+                out["used_fb"][i] = int(used)
+
+        def _rank(self, G, ids, perm):
+            perm[:] = torch.as_tensor(O.rank(G.numpy(), ids.numpy()))
+            return perm
+
+    return OracleSharded
+
+
+def _owner_worker(rank, world, port, result_q):
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    try:
+        from paper_2603_07917_b200.scheduler import RoundConfig
+        dim, n_total, nq, k, theta, nbins = 128, 6000, 40, 16, 0.6, 64
+        emb, lens, _, _ = O.make_bank(n_total + nq, dim, 30, seed=9)
+        bank_e, bank_l = emb[:n_total], lens[:n_total]
+        plan = ShardPlan(n_total, world, rank)
+        lo, hi = plan.slot_offset, plan.slot_offset + plan.local_capacity
+        hist = _FakeHistory(bank_e, bank_l, lo, hi, n_total, n_total)
+        cfg = RoundConfig(k=k, theta=theta, min_matches=5, max_len=2048, nbins=nbins)
+        owner = world - 1  # not rank 0: the owner index is honoured
+        sched = _oracle_sharded_cls()(hist, cfg, owner=owner)
+        I = np.random.default_rng(4).integers(1, 4097, nq).astype(np.int32)
+        ids = np.arange(nq, dtype=np.int64)
+        q = emb[n_total:]
+        if rank == owner:
+            res = sched.schedule_round(torch.as_tensor(q), torch.as_tensor(O.inv_norm(q)),
+                                       torch.as_tensor(I), torch.as_tensor(ids))
+            perm, G, _ = res
+            keys = O.scores(q, O.inv_norm(q), bank_e, O.inv_norm(bank_e))
+            ref = O.predict_round(keys, np.arange(n_total), bank_l, I, k, theta, 5, 2048, nbins,
+                                  window_lens=bank_l)
+            Gr = np.array([r["G"] for r in ref])
+            ok = np.array_equal(G.numpy(), Gr) and np.array_equal(perm.numpy(), O.rank(Gr, ids))
+            ok &= sum(r["used_fallback"] for r in ref) < nq  # the top-k path is exercised
+        else:
+            ok = sched.schedule_round(None, None, nq=nq) is None
+        result_q.put((rank, bool(ok)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_single_owner_round_equals_single_bank(world):
+    """ShardedScheduler.schedule_round (single owner, the north star's
+    broadcast -> local top-k -> all-gather -> owner merge/finish/rank) over
+    gloo: the owner's Gittins indices and order equal the single-bank oracle
+    round bit for bit; non-owners return None."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_owner_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+    results = dict(q.get(timeout=10) for _ in range(world))
+    assert results == {r: True for r in range(world)}
