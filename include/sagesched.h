@@ -84,11 +84,15 @@ int ss_embed_accumulate_batch(const int64_t* tokens, const int64_t* offsets,
                               int64_t n, uint64_t salt, int32_t dim,
                               double* out, void* stream);
 
-/* Same hash, emitted straight into the bank's int8 layout plus fp32 inverse
- * norm.  |bucket| > 127 -> SS_ERR_RANGE.  Synchronises. */
-int ss_embed_quantize_batch(const int64_t* tokens, const int64_t* offsets,
-                            int64_t n, uint64_t salt, int32_t dim,
-                            int8_t* out_emb, float* out_inv_norm, void* stream);
+/* Same hash (_kernels.py:82-95), emitted as the exact integer vector in int16
+ * plus its fp32 inverse norm (IEEE 1/sqrt of the exact int64 sum of squares)
+ * for the bank.  Buckets beyond int8 (long prompts that
+ * repeat a token or bigram > 127 times) are kept exactly; *n_wide (host
+ * pointer, may be NULL) receives how many rows do not fit int8.  |bucket| >
+ * 32767 -> SS_ERR_RANGE.  Synchronises. */
+int ss_embed_quantize_batch(const int64_t* tokens, const int64_t* offsets, int64_t n,
+                            uint64_t salt, int32_t dim, int16_t* out_emb, float* out_inv_norm,
+                            int64_t* n_wide, void* stream);
 
 /* --------------------------------------------------- reference cost.py --- */
 /* cost.cost_distribution (cost.py:97-118), batched: len_support f64[n,stride]
@@ -110,6 +114,17 @@ int ss_bank_destroy(ss_bank_t* h);
  * 1/sqrt).  lens must lie in [1, 65535].  Async. */
 int ss_bank_push(ss_bank_t* h, const int8_t* emb, const float* inv_norm,
                  const int32_t* lens, int64_t n, void* stream);
+/* push of int16 feature-hash rows (ss_embed_quantize_batch output): a row
+ * that fits int8 enters the int8 plane like ss_bank_push; a "wide" row keeps
+ * its exact int16 vector in the bank's wide plane (allocated on first use,
+ * 2 * dim bytes per slot), scored exactly by the CUDA-core wide pass of every
+ * later top-k / round (one more candidate list per query).  Synchronises. */
+int ss_bank_push16(ss_bank_t* h, const int16_t* emb, const float* inv_norm,
+                   const int32_t* lens, int64_t n, void* stream);
+/* ss_bank_write with int16 rows (the sharded host's form of ss_bank_push16). */
+int ss_bank_write16(ss_bank_t* h, const int16_t* emb, const float* inv_norm,
+                    const int32_t* lens, const int64_t* seq, const int64_t* local_slot,
+                    int64_t n, void* stream);
 /* scatter-write records at explicit LOCAL slots with explicit seqs (used by
  * the sharded host, which owns the global ring head).  Async. */
 int ss_bank_write(ss_bank_t* h, const int8_t* emb, const float* inv_norm,
@@ -139,6 +154,21 @@ int ss_bank_fallback_hist(ss_bank_t* h, int32_t max_len, int32_t nbins,
 int ss_topk(ss_bank_t* h, const int8_t* q, const float* q_inv, int64_t nq,
             int32_t k, float theta, int32_t algo, uint64_t* out_comp,
             int32_t* out_len, void* stream);
+/* ss_topk for a batch holding wide queries (feature-hash vectors outside
+ * int8): rows wide_idx[0..n_wide) of the batch are scored with their exact
+ * int16 vectors wide_q_emb [n_wide, dim] and inverse norms wide_q_inv (their
+ * q / q_inv entries are ignored), everything else as ss_topk.  Async. */
+int ss_topk_wide(ss_bank_t* h, const int8_t* q, const float* q_inv, int64_t nq, int64_t n_wide,
+                 const int64_t* wide_idx, const int16_t* wide_q_emb, const float* wide_q_inv,
+                 int32_t k, float theta, int32_t algo, uint64_t* out_comp, int32_t* out_len,
+                 void* stream);
+/* query_similar in full: EVERY record of the window with
+ * key >= theta (theta = -1: the whole window), ordered by key desc, then
+ * insertion_seq desc.  One query, given as its exact integer vector in int16
+ * (int8 vectors widened), with its inverse norm.  out_* hold the window's
+ * capacity; *n_out (host) = number of records returned.  Synchronises. */
+int ss_query_similar(ss_bank_t* h, const int16_t* q, float q_inv, float theta, float* out_key,
+                     int64_t* out_seq, int32_t* out_len, int64_t* n_out, void* stream);
 /* The similarity kernel alone (no merge): writes the unsorted per-slice
  * partial top-k lists u64[n_slices][nq][k] into `partials` (capacity
  * max_slices slices) and the slice count into *n_slices.  Used to time the
@@ -279,6 +309,14 @@ int ss_schedule_round(ss_bank_t* h, const int8_t* q, const float* q_inv,
                       int32_t nbins, int32_t algo, int32_t P, int32_t* npts,
                       int32_t* pbin, int32_t* pcnt, int64_t* pD, uint8_t* used_fb,
                       double* G, int64_t* perm, void* stream);
+/* ss_schedule_round with wide queries (see ss_topk_wide). */
+int ss_schedule_round_wide(ss_bank_t* h, const int8_t* q, const float* q_inv,
+                           const int32_t* input_len, const int64_t* ids, int64_t nq, int64_t n_wide,
+                           const int64_t* wide_idx, const int16_t* wide_q_emb,
+                           const float* wide_q_inv, int32_t k, float theta, int32_t min_matches,
+                           int32_t max_len, int32_t nbins, int32_t algo, int32_t P, int32_t* npts,
+                           int32_t* pbin, int32_t* pcnt, int64_t* pD, uint8_t* used_fb, double* G,
+                           int64_t* perm, void* stream);
 /* Same round from HOST buffers (the plugin call a scheduler makes): copies
  * q/q_inv/input_len/ids host->device, runs the round, copies G and perm
  * device->host, and synchronises the stream. */

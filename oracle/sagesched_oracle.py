@@ -179,7 +179,7 @@ def cost_vector(kind: str, I: float, lengths, w_in=1.0, w_out=2.0):
 def inv_norm(emb_i8) -> np.ndarray:
     """fp32 1/||x|| of integer vectors, IEEE sqrt and divide; NaN for 0."""
     x = np.asarray(emb_i8).astype(np.int64)
-    ss = (x * x).sum(axis=1).astype(F32)  # exact: < 2^24
+    ss = (x * x).sum(axis=1).astype(F32)  # exact below 2^24 (int8 rows), else one rounding
     with np.errstate(divide="ignore", invalid="ignore"):
         r = F32(1.0) / np.sqrt(ss)
     r[ss == 0] = np.nan
@@ -194,11 +194,17 @@ def ring_rel(slot, head, capacity):
 def scores(q_i8, q_inv, w_i8, w_inv) -> np.ndarray:
     """key[q, j] = fl32(fl32(f32(dot) * inv_w[j]) * inv_q[q]).
 
-    The dot product is computed through fp32 BLAS, which is exact here:
+    int8 vectors: the dot product goes through fp32 BLAS, which is exact:
     every partial sum of int8*int8 products is an integer of magnitude
-    < 384*127^2 < 2^24.
+    < 384*127^2 < 2^24.  Wider integer vectors (feature-hash counts of long
+    prompts, _kernels.py:82-95): the exact int64 dot, then one correctly
+    rounded conversion to f32.
     """
-    d = np.asarray(q_i8, F32) @ np.asarray(w_i8, F32).T
+    q, w = np.asarray(q_i8), np.asarray(w_i8)
+    if q.dtype == np.int8 and w.dtype == np.int8:
+        d = q.astype(F32) @ w.astype(F32).T
+    else:
+        d = (q.astype(np.int64) @ w.astype(np.int64).T).astype(F32)
     s = d * np.asarray(w_inv, F32)[None, :]
     return (s * np.asarray(q_inv, F32)[:, None]).astype(F32)
 

@@ -29,11 +29,13 @@ SIGNATURES = {
     "ss_gittins_min_batch": (C.c_int, [P, P, P, I64, I64, P, P]),
     "ss_gittins_dist_batch": (C.c_int, [P, P, P, P, P, I64, I64, P, P]),
     "ss_embed_accumulate_batch": (C.c_int, [P, P, I64, U64, I32, P, P]),
-    "ss_embed_quantize_batch": (C.c_int, [P, P, I64, U64, I32, P, P, P]),
+    "ss_embed_quantize_batch": (C.c_int, [P, P, I64, U64, I32, P, P, C.POINTER(I64), P]),
     "ss_cost_distribution_batch": (C.c_int, [I32, F64, F64, P, P, P, I64, I64, P, P]),
     "ss_bank_create": (C.c_int, [C.POINTER(P), I32, I64, I32, I64, I64]),
     "ss_bank_destroy": (C.c_int, [P]),
     "ss_bank_push": (C.c_int, [P, P, P, P, I64, P]),
+    "ss_bank_push16": (C.c_int, [P, P, P, P, I64, P]),
+    "ss_bank_write16": (C.c_int, [P, P, P, P, P, P, I64, P]),
     "ss_bank_write": (C.c_int, [P, P, P, P, P, P, I64, P]),
     "ss_bank_set_head": (C.c_int, [P, I64]),
     "ss_bank_info": (C.c_int, [P, C.POINTER(I64), C.POINTER(I64), C.POINTER(I64), C.POINTER(I32)]),
@@ -41,6 +43,8 @@ SIGNATURES = {
     "ss_bank_sync_check": (C.c_int, [P, P]),
     "ss_bank_fallback_hist": (C.c_int, [P, I32, I32, P, P, P, P]),
     "ss_topk": (C.c_int, [P, P, P, I64, I32, F32, I32, P, P, P]),
+    "ss_topk_wide": (C.c_int, [P, P, P, I64, I64, P, P, P, I32, F32, I32, P, P, P]),
+    "ss_query_similar": (C.c_int, [P, P, F32, F32, P, P, P, C.POINTER(I64), P]),
     "ss_topk_partials": (C.c_int, [P, P, P, I64, I32, F32, I32, P, I32, C.POINTER(I32), P]),
     "ss_merge_topk": (C.c_int, [P, P, I32, I64, I32, P, P, P]),
     "ss_topk_scatter": (C.c_int, [P, P, P, I64, I32, F32, I32, I32, I32, P, P, P]),
@@ -65,6 +69,8 @@ SIGNATURES = {
                                   I32, F32, I32, I32, I32, I32, C.POINTER(I64), C.POINTER(I64), P]),
     "ss_schedule_round": (C.c_int, [P, P, P, P, P, I64, I32, F32, I32, I32, I32, I32, I32,
                                     P, P, P, P, P, P, P, P]),
+    "ss_schedule_round_wide": (C.c_int, [P, P, P, P, P, I64, I64, P, P, P, I32, F32, I32, I32, I32,
+                                         I32, I32, P, P, P, P, P, P, P, P]),
     "ss_schedule_round_host": (C.c_int, [P, P, P, P, P, I64, I32, F32, I32, I32, I32, I32,
                                          P, P, P]),
 }

@@ -11,16 +11,25 @@
 
 namespace ss {
 
-// one warp per record: 16-byte vector copy of the int8 row, then inverse
-// norm (IEEE 1/sqrt, bit-identical to numpy float32), length and seq.
+// one warp per record: 16-byte vector copy of the row, then inverse norm
+// (IEEE 1/sqrt of the exact integer sum of squares, bit-identical to numpy
+// float32), length and seq.  T = int8: the row goes to the int8 plane.
+// T = int16 (feature-hash vectors of long prompts, whose buckets may exceed
+// the int8 range, _kernels.py:82-95): a row that fits int8 is narrowed into
+// the int8 plane; a row that does not ("wide") leaves a zero row and a NaN
+// inverse norm there -- the tensor-core kernels never match it -- and its
+// exact int16 vector and inverse norm go to the bank's wide plane, flagged
+// per slot, where the CUDA-core wide pass (k_wide.cu) scores it.  Every
+// write of a normal row clears the slot's wide flag.
+template <typename T>
 __global__ void __launch_bounds__(256)
 k_bank_write(int8_t* __restrict__ emb, float* __restrict__ inv, int32_t* __restrict__ lens,
              int64_t* __restrict__ seq, int32_t* __restrict__ len_cnt, int dim,
-             const int8_t* __restrict__ src_emb, const float* __restrict__ src_inv,
+             const T* __restrict__ src_emb, const float* __restrict__ src_inv,
              const int32_t* __restrict__ src_lens, const int64_t* __restrict__ src_seq,
              const int64_t* __restrict__ src_slot, int64_t n, int64_t first_seq,
              int64_t capacity, int64_t skip, int* __restrict__ err,
-             const int64_t* __restrict__ src_idx) {
+             const int64_t* __restrict__ src_idx, WidePlane wp) {
   const int lane = threadIdx.x & 31;
   const int64_t r = skip + (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (r >= n) return;
@@ -31,15 +40,53 @@ k_bank_write(int8_t* __restrict__ emb, float* __restrict__ inv, int32_t* __restr
     if (lane == 0) atomicExch(err, SS_ERR_ARG);
     return;
   }
-  const int4* src = reinterpret_cast<const int4*>(src_emb + rs * dim);
-  int4* dst = reinterpret_cast<int4*>(emb + slot * dim);
-  int ss2 = 0;
-  for (int w = lane; w < dim / 16; w += 32) {
-    int4 v = src[w];
-    dst[w] = v;
-    const int* vi = reinterpret_cast<const int*>(&v);
+  bool wide = false;
+  long long ss2 = 0;
+  if constexpr (sizeof(T) == 1) {
+    const int4* src = reinterpret_cast<const int4*>(src_emb + rs * dim);
+    int4* dst = reinterpret_cast<int4*>(emb + slot * dim);
+    int acc = 0;
+    for (int w = lane; w < dim / 16; w += 32) {
+      int4 v = src[w];
+      dst[w] = v;
+      const int* vi = reinterpret_cast<const int*>(&v);
 #pragma unroll
-    for (int t = 0; t < 4; ++t) ss2 = __dp4a(vi[t], vi[t], ss2);
+      for (int t = 0; t < 4; ++t) acc = __dp4a(vi[t], vi[t], acc);
+    }
+    ss2 = acc;
+  } else {
+    // 8 int16 per 16-byte load; the row fits int8 iff every |x| <= 127
+    const int4* src = reinterpret_cast<const int4*>(src_emb + rs * dim);
+    bool fits = true;
+    for (int w = lane; w < dim / 8; w += 32) {
+      const int4 v = src[w];
+      const int16_t* x = reinterpret_cast<const int16_t*>(&v);
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        fits &= (x[t] >= -127 && x[t] <= 127);
+        ss2 += (long long)x[t] * x[t];
+      }
+    }
+    wide = !__all_sync(0xffffffffu, fits);
+    if (wide && !wp.flag) {  // no wide plane allocated: refuse
+      if (lane == 0) atomicExch(err, SS_ERR_RANGE);
+      return;
+    }
+    for (int w = lane; w < dim / 8; w += 32) {
+      const int4 v = src[w];
+      const int16_t* x = reinterpret_cast<const int16_t*>(&v);
+      if (wide) {
+        reinterpret_cast<int4*>(wp.emb + slot * dim)[w] = v;
+        reinterpret_cast<uint2*>(emb + slot * dim)[w] = make_uint2(0u, 0u);
+      } else {
+        uint32_t lo = 0, hi = 0;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) lo |= (uint32_t)(uint8_t)(int8_t)x[t] << (8 * t);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) hi |= (uint32_t)(uint8_t)(int8_t)x[4 + t] << (8 * t);
+        reinterpret_cast<uint2*>(emb + slot * dim)[w] = make_uint2(lo, hi);
+      }
+    }
   }
   for (int o = 16; o > 0; o >>= 1) ss2 += __shfl_xor_sync(0xffffffffu, ss2, o);
   if (lane == 0) {
@@ -54,22 +101,38 @@ k_bank_write(int8_t* __restrict__ emb, float* __restrict__ inv, int32_t* __restr
     seq[slot] = s;
     float iv;
     if (src_inv) iv = src_inv[rs];
-    else iv = ss2 ? __fdiv_rn(1.0f, __fsqrt_rn((float)ss2)) : __int_as_float(0x7fc00000);
-    inv[slot] = iv;
+    else iv = ss2 ? __fdiv_rn(1.0f, __fsqrt_rn(__ll2float_rn(ss2))) : __int_as_float(0x7fc00000);
+    inv[slot] = wide ? __int_as_float(0x7fc00000) : iv;  // the tensor-core kernels skip wide rows
+    if (wp.flag) {
+      wp.flag[slot] = wide ? 1 : 0;
+      if (wide) {
+        wp.inv[slot] = iv;
+        atomicAdd(wp.count, 1);
+      }
+    }
   }
 }
 
 int launch_bank_write(int8_t* emb, float* inv, int32_t* lens, int64_t* seq, int32_t* len_cnt,
-                      int dim, const int8_t* src_emb, const float* src_inv,
+                      int dim, const void* src_emb, int src_bytes, const float* src_inv,
                       const int32_t* src_lens, const int64_t* src_seq, const int64_t* src_slot,
                       int64_t n, int64_t first_seq, int64_t capacity, int64_t skip, int* err,
-                      cudaStream_t st, const int64_t* src_idx) {
+                      cudaStream_t st, const int64_t* src_idx, const WidePlane* wp) {
   int64_t m = n - skip;
   if (m <= 0) return SS_OK;
+  const WidePlane w = wp ? *wp : WidePlane{};
   count_launch();
-  k_bank_write<<<(unsigned)((m + 7) / 8), 256, 0, st>>>(emb, inv, lens, seq, len_cnt, dim, src_emb,
-                                                          src_inv, src_lens, src_seq, src_slot,
-                                                          n, first_seq, capacity, skip, err, src_idx);
+  const unsigned grid = (unsigned)((m + 7) / 8);
+  if (src_bytes == 2)
+    k_bank_write<int16_t><<<grid, 256, 0, st>>>(emb, inv, lens, seq, len_cnt, dim,
+                                                static_cast<const int16_t*>(src_emb), src_inv,
+                                                src_lens, src_seq, src_slot, n, first_seq, capacity,
+                                                skip, err, src_idx, w);
+  else
+    k_bank_write<int8_t><<<grid, 256, 0, st>>>(emb, inv, lens, seq, len_cnt, dim,
+                                               static_cast<const int8_t*>(src_emb), src_inv,
+                                               src_lens, src_seq, src_slot, n, first_seq, capacity,
+                                               skip, err, src_idx, w);
   SS_LAUNCH_CHECK();
   return SS_OK;
 }

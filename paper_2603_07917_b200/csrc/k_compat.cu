@@ -183,7 +183,7 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
 template <bool QUANT>
 __global__ void __launch_bounds__(128)
 k_embed(const int64_t* __restrict__ tokens, const int64_t* __restrict__ offsets, int64_t n,
-        uint64_t salt, int dim, double* __restrict__ out_f64, int8_t* __restrict__ out_i8,
+        uint64_t salt, int dim, double* __restrict__ out_f64, int16_t* __restrict__ out_i16,
         float* __restrict__ out_inv, int* __restrict__ err) {
   extern __shared__ int s_acc[];  // [4][dim]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -218,32 +218,40 @@ k_embed(const int64_t* __restrict__ tokens, const int64_t* __restrict__ offsets,
   if (!QUANT) {
     for (int d = lane; d < dim; d += 32) out_f64[p * dim + d] = (double)acc[d];
   } else {
-    int ss2 = 0;
+    // the exact integer vector as int16 (the bank keeps it in its int8 plane
+    // when every bucket fits, in its wide plane otherwise; err[1] counts the
+    // rows that do not fit int8); inverse norm of the exact sum of squares
+    long long ss2 = 0;
+    bool fits = true;
     for (int d = lane; d < dim; d += 32) {
       int v = acc[d];
-      if (v > 127 || v < -127) atomicExch(err, SS_ERR_RANGE);
-      v = max(-127, min(127, v));
-      out_i8[p * dim + d] = (int8_t)v;
-      ss2 += v * v;
+      if (v > 32767 || v < -32767) atomicExch(err, SS_ERR_RANGE);
+      v = max(-32767, min(32767, v));
+      fits &= (v >= -127 && v <= 127);
+      out_i16[p * dim + d] = (int16_t)v;
+      ss2 += (long long)v * v;
     }
     for (int o = 16; o > 0; o >>= 1) ss2 += __shfl_xor_sync(0xffffffffu, ss2, o);
-    if (lane == 0)
-      out_inv[p] = ss2 ? __fdiv_rn(1.0f, __fsqrt_rn((float)ss2)) : __int_as_float(0x7fc00000);
+    const bool wide = !__all_sync(0xffffffffu, fits);
+    if (lane == 0) {
+      out_inv[p] = ss2 ? __fdiv_rn(1.0f, __fsqrt_rn(__ll2float_rn(ss2))) : __int_as_float(0x7fc00000);
+      if (wide) atomicAdd(err + 1, 1);
+    }
   }
 }
 
 int launch_embed(const int64_t* tokens, const int64_t* offsets, int64_t n, uint64_t salt,
-                 int dim, double* out_f64, int8_t* out_i8, float* out_inv, int* err,
+                 int dim, double* out_f64, int16_t* out_i16, float* out_inv, int* err,
                  cudaStream_t st) {
   if (n <= 0) return SS_OK;
   size_t smem = (size_t)4 * dim * sizeof(int);
   if (smem > 200 * 1024) return set_error(SS_ERR_UNSUPPORTED, "dim %d too large", dim);
   unsigned grid = (unsigned)((n + 3) / 4);
   count_launch();
-  if (out_i8) {
+  if (out_i16) {
     if (smem > 48 * 1024)
       SS_CUDA_TRY(cudaFuncSetAttribute(k_embed<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_embed<true><<<grid, 128, smem, st>>>(tokens, offsets, n, salt, dim, nullptr, out_i8, out_inv, err);
+    k_embed<true><<<grid, 128, smem, st>>>(tokens, offsets, n, salt, dim, nullptr, out_i16, out_inv, err);
   } else {
     if (smem > 48 * 1024)
       SS_CUDA_TRY(cudaFuncSetAttribute(k_embed<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -57,7 +57,8 @@ int pick_slices(int64_t qtiles, int64_t tiles, int sms) {
   return (int)best;
 }
 
-// per-device sticky error flag for handle-less synchronous entry points
+// per-device sticky error flag for handle-less synchronous entry points,
+// followed by one scratch counter (device_err_flag() + 1)
 static int* device_err_flag() {
   static std::mutex mu;
   static int* flags[64] = {nullptr};
@@ -65,8 +66,8 @@ static int* device_err_flag() {
   cudaGetDevice(&dev);
   std::lock_guard<std::mutex> lk(mu);
   if (!flags[dev]) {
-    if (cudaMalloc(&flags[dev], sizeof(int)) != cudaSuccess) return nullptr;
-    cudaMemset(flags[dev], 0, sizeof(int));
+    if (cudaMalloc(&flags[dev], 2 * sizeof(int)) != cudaSuccess) return nullptr;
+    cudaMemset(flags[dev], 0, 2 * sizeof(int));
   }
   return flags[dev];
 }
@@ -114,6 +115,11 @@ struct ss_bank {
   uint32_t* gslots = nullptr;  // TS kernel pure top-k: per-slice published bounds
   int64_t gslots_cap = 0;
   int8_t* qscratch = nullptr;  // 128 x dim: single-tile query spread (k_topk_tc)
+  // wide plane (first int16 push): exact vectors of rows outside int8
+  WidePlane wp;
+  int64_t* wlist = nullptr;  // [cap] compacted wide slots (per wide pass)
+  int* wlist_count = nullptr;
+  bool any_wide = false;     // a wide row has been written: rounds run the wide pass
   // side stream of the fused round: the fallback histogram runs concurrently
   // with the similarity kernel (fork/join by events; captured as two graph
   // branches when the caller's stream is being captured)
@@ -124,7 +130,7 @@ struct ss_bank {
   // once the same call repeats: key = every scalar and pointer baked into it
   struct HostRoundKey {
     int64_t nq, head;
-    int32_t k, min_matches, max_len, nbins, algo;
+    int32_t k, min_matches, max_len, nbins, algo, any_wide;
     float theta;
     const void* ptr[6];
     uint64_t ws_gen;
@@ -226,17 +232,22 @@ int ss_embed_accumulate_batch(const int64_t* tokens, const int64_t* offsets, int
 }
 
 int ss_embed_quantize_batch(const int64_t* tokens, const int64_t* offsets, int64_t n,
-                            uint64_t salt, int32_t dim, int8_t* out_emb, float* out_inv_norm,
-                            void* stream) {
+                            uint64_t salt, int32_t dim, int16_t* out_emb, float* out_inv_norm,
+                            int64_t* n_wide, void* stream) {
   if (n < 0 || dim < 1 || !out_emb || !out_inv_norm) return set_error(SS_ERR_ARG, "embed_quantize: bad args");
+  if (n_wide) *n_wide = 0;
   if (n == 0) return SS_OK;
   cudaStream_t st = (cudaStream_t)stream;
   int* err = device_err_flag();
   if (!err) return set_error(SS_ERR_CUDA, "error flag alloc failed");
+  SS_CUDA_TRY(cudaMemsetAsync(err + 1, 0, sizeof(int), st));
   int rc = launch_embed(tokens, offsets, n, salt, dim, nullptr, out_emb, out_inv_norm, err, st);
   if (rc) return rc;
-  int e = read_and_clear(err, st);
-  if (e == SS_ERR_RANGE) return set_error(SS_ERR_RANGE, "embed_quantize: a bucket exceeds int8 range");
+  int cnt = 0;
+  SS_CUDA_TRY(cudaMemcpyAsync(&cnt, err + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+  int e = read_and_clear(err, st);  // synchronises
+  if (e == SS_ERR_RANGE) return set_error(SS_ERR_RANGE, "embed_quantize: a bucket exceeds the int16 range");
+  if (n_wide) *n_wide = cnt;
   return e;
 }
 
@@ -313,6 +324,12 @@ int ss_bank_destroy(ss_bank_t* h) {
   cudaFree(h->ws);
   cudaFree(h->gslots);
   cudaFree(h->qscratch);
+  cudaFree(h->wp.emb);
+  cudaFree(h->wp.inv);
+  cudaFree(h->wp.flag);
+  cudaFree(h->wp.count);
+  cudaFree(h->wlist);
+  cudaFree(h->wlist_count);
   if (h->host_exec) cudaGraphExecDestroy(h->host_exec);
   if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
@@ -329,8 +346,9 @@ int ss_bank_push(ss_bank_t* h, const int8_t* emb, const float* inv_norm, const i
     return set_error(SS_ERR_ARG, "bank_push on a shard: use ss_bank_write with the global head");
   if (n == 0) return SS_OK;
   int64_t skip = n > h->cap ? n - h->cap : 0;
-  int rc = launch_bank_write(h->emb, h->inv, h->lens, h->seq, h->len_cnt, h->dim, emb, inv_norm, lens, nullptr,
-                             nullptr, n, h->head, h->cap, skip, h->d_err, (cudaStream_t)stream);
+  int rc = launch_bank_write(h->emb, h->inv, h->lens, h->seq, h->len_cnt, h->dim, emb, 1, inv_norm,
+                             lens, nullptr, nullptr, n, h->head, h->cap, skip, h->d_err,
+                             (cudaStream_t)stream, nullptr, h->wp.flag ? &h->wp : nullptr);
   if (rc) return rc;
   h->head += n;
   return SS_OK;
@@ -339,8 +357,74 @@ int ss_bank_push(ss_bank_t* h, const int8_t* emb, const float* inv_norm, const i
 int ss_bank_write(ss_bank_t* h, const int8_t* emb, const float* inv_norm, const int32_t* lens,
                   const int64_t* seq, const int64_t* local_slot, int64_t n, void* stream) {
   if (!h || n < 0 || !seq || !local_slot) return set_error(SS_ERR_ARG, "bank_write: bad args");
-  return launch_bank_write(h->emb, h->inv, h->lens, h->seq, h->len_cnt, h->dim, emb, inv_norm, lens, seq,
-                           local_slot, n, 0, h->cap, 0, h->d_err, (cudaStream_t)stream);
+  return launch_bank_write(h->emb, h->inv, h->lens, h->seq, h->len_cnt, h->dim, emb, 1, inv_norm,
+                           lens, seq, local_slot, n, 0, h->cap, 0, h->d_err, (cudaStream_t)stream,
+                           nullptr, h->wp.flag ? &h->wp : nullptr);
+}
+
+static int ensure_wide(ss_bank* h) {
+  if (h->wp.flag) return SS_OK;
+  DeviceGuard g(h->device);
+  WidePlane w;
+  cudaError_t e = cudaMalloc(&w.emb, (size_t)h->cap * h->dim * 2);
+  if (e == cudaSuccess) e = cudaMalloc(&w.inv, (size_t)h->cap * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&w.flag, (size_t)h->cap);
+  if (e == cudaSuccess) e = cudaMalloc(&w.count, sizeof(int));
+  if (e == cudaSuccess) e = cudaMalloc(&h->wlist, (size_t)h->cap * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&h->wlist_count, sizeof(int));
+  if (e == cudaSuccess) e = cudaMemset(w.flag, 0, (size_t)h->cap);
+  if (e == cudaSuccess) e = cudaMemset(w.count, 0, sizeof(int));
+  if (e != cudaSuccess) {
+    cudaFree(w.emb); cudaFree(w.inv); cudaFree(w.flag); cudaFree(w.count);
+    cudaFree(h->wlist); cudaFree(h->wlist_count);
+    h->wlist = nullptr;
+    h->wlist_count = nullptr;
+    return set_error(SS_ERR_CUDA, "wide plane allocation (%lld rows): %s", (long long)h->cap,
+                     cudaGetErrorString(e));
+  }
+  h->wp = w;
+  return SS_OK;
+}
+
+// after an int16 write: did any wide row land? (rounds then run the wide pass)
+static int note_wide(ss_bank* h, cudaStream_t st) {
+  int c = 0;
+  SS_CUDA_TRY(cudaMemcpyAsync(&c, h->wp.count, sizeof(int), cudaMemcpyDeviceToHost, st));
+  SS_CUDA_TRY(cudaStreamSynchronize(st));
+  if (c > 0 && !h->any_wide) {
+    h->any_wide = true;
+    ++h->ws_gen;  // a captured host round lacks the wide pass: re-capture
+  }
+  return SS_OK;
+}
+
+int ss_bank_push16(ss_bank_t* h, const int16_t* emb, const float* inv_norm, const int32_t* lens,
+                   int64_t n, void* stream) {
+  if (!h || n < 0) return set_error(SS_ERR_ARG, "bank_push16: bad args");
+  if (h->gcap != h->cap || h->slot_offset != 0)
+    return set_error(SS_ERR_ARG, "bank_push16 on a shard: use ss_bank_write16 with the global head");
+  if (n == 0) return SS_OK;
+  if (int rc = ensure_wide(h)) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t skip = n > h->cap ? n - h->cap : 0;
+  int rc = launch_bank_write(h->emb, h->inv, h->lens, h->seq, h->len_cnt, h->dim, emb, 2, inv_norm,
+                             lens, nullptr, nullptr, n, h->head, h->cap, skip, h->d_err, st,
+                             nullptr, &h->wp);
+  if (rc) return rc;
+  h->head += n;
+  return note_wide(h, st);
+}
+
+int ss_bank_write16(ss_bank_t* h, const int16_t* emb, const float* inv_norm, const int32_t* lens,
+                    const int64_t* seq, const int64_t* local_slot, int64_t n, void* stream) {
+  if (!h || n < 0 || !seq || !local_slot) return set_error(SS_ERR_ARG, "bank_write16: bad args");
+  if (n == 0) return SS_OK;
+  if (int rc = ensure_wide(h)) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = launch_bank_write(h->emb, h->inv, h->lens, h->seq, h->len_cnt, h->dim, emb, 2, inv_norm,
+                             lens, seq, local_slot, n, 0, h->cap, 0, h->d_err, st, nullptr, &h->wp);
+  if (rc) return rc;
+  return note_wide(h, st);
 }
 
 int ss_bank_set_head(ss_bank_t* h, int64_t global_head) {
@@ -405,35 +489,91 @@ static int topk_plan(ss_bank* h, const TopkArgs& a, int32_t& algo, int& slices) 
   return SS_OK;
 }
 
-static size_t topk_ws_need(ss_bank* h, int64_t nq, int32_t k, int32_t algo) {
+// the wide pass runs when the bank holds (or held) a wide row or the batch
+// has wide queries: one more candidate list per query
+static bool wide_on(const ss_bank* h, const WideQ& wq) { return h->any_wide || wq.n > 0; }
+
+static WideBank wide_bank(ss_bank* h) {
+  WideBank b;
+  b.any = h->any_wide;
+  b.plane = h->wp;
+  b.list = h->wlist;
+  b.list_count = h->wlist_count;
+  b.bank_lens = h->lens;
+  return b;
+}
+
+// workspace after the round buffers: [partials: (slices + wide) lists][wide pass scratch]
+static size_t topk_ws_need(ss_bank* h, int64_t nq, int32_t k, int32_t algo, const WideQ& wq) {
   TopkArgs a{nullptr, nullptr, nq, h->emb, h->inv, h->cap, h->dim, k, 0.f, h->head, h->gcap,
              h->slot_offset};
   a.inv_padded = true;  // the bank pads inv with one NaN tile
   int slices = 1;
   if (topk_plan(h, a, algo, slices)) return 0;
-  return align_up((size_t)slices * nq * k * 8);
+  const bool wide = wide_on(h, wq);
+  size_t b = align_up((size_t)(slices + (wide ? 1 : 0)) * nq * k * 8);
+  if (wide) b += align_up((size_t)nq * 4) + wide_ws_bytes(wq, nq, k, h->cap, sm_count(h->device));
+  return b;
+}
+
+// q_inv with the wide queries' entries set to NaN (the tensor-core kernels
+// must not score their int8 stand-in rows)
+__global__ void k_mask_qinv(const float* __restrict__ src, int64_t nq, float* __restrict__ dst) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nq;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+__global__ void k_mask_qinv_set(const int64_t* __restrict__ idx, int64_t n, float* __restrict__ dst) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[idx[i]] = __int_as_float(0x7fc00000);
+}
+
+// stage 1 (+ the wide pass) into `partials` [lists][nq][k]; returns the list count
+static int stage1(ss_bank* h, TopkArgs& a, int32_t algo, int slices, const WideQ& wq,
+                  uint64_t* partials, char* scratch, cudaStream_t st, int* nlists) {
+  const bool wide = wide_on(h, wq);
+  *nlists = slices + (wide ? 1 : 0);
+  if (wide && wq.n > 0) {
+    float* qinv = reinterpret_cast<float*>(scratch);
+    scratch += align_up((size_t)a.nq * 4);
+    count_launch();
+    k_mask_qinv<<<(unsigned)std::min<int64_t>((a.nq + 255) / 256, 1024), 256, 0, st>>>(a.q_inv, a.nq,
+                                                                                    qinv);
+    count_launch();
+    k_mask_qinv_set<<<(unsigned)((wq.n + 255) / 256), 256, 0, st>>>(wq.idx, wq.n, qinv);
+    SS_LAUNCH_CHECK();
+    a.q_inv = qinv;
+  } else if (wide) {
+    scratch += align_up((size_t)a.nq * 4);
+  }
+  int rc = (algo == SS_ALGO_TCGEN05) ? launch_topk_tc(a, partials, slices, st)
+                                     : launch_topk_scan(a, partials, slices, st);
+  if (rc || !wide) return rc;
+  return launch_wide_pass(wide_bank(h), a, wq, partials + (size_t)slices * a.nq * a.k, scratch,
+                          h->device, st);
 }
 
 static int topk_impl(ss_bank* h, const int8_t* q, const float* q_inv, int64_t nq, int32_t k,
                      float theta, int32_t algo, uint64_t* out_comp, int32_t* out_len,
-                     size_t ws_offset, cudaStream_t st, const PeerOut* po = nullptr) {
+                     size_t ws_offset, cudaStream_t st, const PeerOut* po = nullptr,
+                     const WideQ& wq = WideQ{}) {
   if (k < 1 || k > 256) return set_error(SS_ERR_ARG, "k must lie in [1, 256], got %d", k);
   if (nq < 0) return set_error(SS_ERR_ARG, "nq < 0");
   if (nq == 0) return SS_OK;
   TopkArgs a{q, q_inv, nq, h->emb, h->inv, h->cap, h->dim, k, theta, h->head, h->gcap,
              h->slot_offset};
   a.inv_padded = true;  // the bank pads inv with one NaN tile
-  a.gslots = gslots_reserve(h, nq, theta);
   a.qscratch = h->qscratch;
   int slices = 1;
   if (int rc = topk_plan(h, a, algo, slices)) return rc;
-  size_t need = ws_offset + align_up((size_t)slices * nq * k * 8);
-  if (int rc = ws_reserve(h, need)) return rc;
+  if (int rc = ws_reserve(h, ws_offset + topk_ws_need(h, nq, k, algo, wq))) return rc;
+  a.gslots = gslots_reserve(h, nq, theta);  // after any workspace move
+  const bool wide = wide_on(h, wq);
   uint64_t* partials = reinterpret_cast<uint64_t*>((char*)h->ws + ws_offset);
-  int rc = (algo == SS_ALGO_TCGEN05) ? launch_topk_tc(a, partials, slices, st)
-                                     : launch_topk_scan(a, partials, slices, st);
-  if (rc) return rc;
-  return launch_merge(partials, nullptr, slices, nq, k, out_comp, out_len, h->lens, h->head,
+  char* scratch = (char*)partials + align_up((size_t)(slices + (wide ? 1 : 0)) * nq * k * 8);
+  int nlists = slices;
+  if (int rc = stage1(h, a, algo, slices, wq, partials, scratch, st, &nlists)) return rc;
+  return launch_merge(partials, nullptr, nlists, nq, k, out_comp, out_len, h->lens, h->head,
                       h->gcap, h->slot_offset, st, po);
 }
 
@@ -441,6 +581,28 @@ int ss_topk(ss_bank_t* h, const int8_t* q, const float* q_inv, int64_t nq, int32
             int32_t algo, uint64_t* out_comp, int32_t* out_len, void* stream) {
   if (!h || !out_comp || !out_len) return set_error(SS_ERR_ARG, "topk: null args");
   return topk_impl(h, q, q_inv, nq, k, theta, algo, out_comp, out_len, 0, (cudaStream_t)stream);
+}
+
+static int wide_q(int64_t n_wide, const int64_t* idx, const int16_t* wq, const float* winv,
+                  WideQ* out) {
+  if (n_wide < 0 || (n_wide > 0 && (!idx || !wq || !winv)))
+    return set_error(SS_ERR_ARG, "wide queries: bad args (n=%lld)", (long long)n_wide);
+  out->n = n_wide;
+  out->idx = idx;
+  out->q = wq;
+  out->inv = winv;
+  return SS_OK;
+}
+
+int ss_topk_wide(ss_bank_t* h, const int8_t* q, const float* q_inv, int64_t nq, int64_t n_wide,
+                 const int64_t* wide_idx, const int16_t* wide_q_emb, const float* wide_q_inv,
+                 int32_t k, float theta, int32_t algo, uint64_t* out_comp, int32_t* out_len,
+                 void* stream) {
+  if (!h || !out_comp || !out_len) return set_error(SS_ERR_ARG, "topk_wide: null args");
+  WideQ wq;
+  if (int rc = wide_q(n_wide, wide_idx, wide_q_emb, wide_q_inv, &wq)) return rc;
+  return topk_impl(h, q, q_inv, nq, k, theta, algo, out_comp, out_len, 0, (cudaStream_t)stream,
+                   nullptr, wq);
 }
 
 int ss_topk_scatter(ss_bank_t* h, const int8_t* q, const float* q_inv, int64_t nq, int32_t k,
@@ -519,6 +681,39 @@ int ss_ipc_open(const uint8_t* handle_host, void** out) {
 
 int ss_ipc_close(void* ptr) {
   if (ptr) SS_CUDA_TRY(cudaIpcCloseMemHandle(ptr));
+  return SS_OK;
+}
+
+int ss_query_similar(ss_bank_t* h, const int16_t* q, float q_inv, float theta, float* out_key,
+                     int64_t* out_seq, int32_t* out_len, int64_t* n_out, void* stream) {
+  if (!h || !q || !out_key || !out_seq || !out_len || !n_out)
+    return set_error(SS_ERR_ARG, "query_similar: null args");
+  *n_out = 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t cap = h->cap;
+  // workspace: G f64[cap] | id i64[cap] | perm i64[cap] | count | rank ws
+  const size_t oG = 0, oid = align_up((size_t)cap * 8), operm = oid + align_up((size_t)cap * 8),
+               ocnt = operm + align_up((size_t)cap * 8), orank = ocnt + 256,
+               end = orank + align_up((size_t)rank_workspace_bytes(cap));
+  if (int rc = ws_reserve(h, end)) return rc;
+  char* w = (char*)h->ws;
+  TopkArgs a{nullptr, nullptr, 1, h->emb, h->inv, h->cap, h->dim, 1, theta, h->head, h->gcap,
+             h->slot_offset};
+  double* G = reinterpret_cast<double*>(w + oG);
+  int64_t* id = reinterpret_cast<int64_t*>(w + oid);
+  int64_t* perm = reinterpret_cast<int64_t*>(w + operm);
+  int* cnt = reinterpret_cast<int*>(w + ocnt);
+  if (int rc = launch_query_all(a, h->seq, wide_bank(h), q, q_inv, G, id, cnt, st)) return rc;
+  int m = 0;
+  SS_CUDA_TRY(cudaMemcpyAsync(&m, cnt, sizeof(int), cudaMemcpyDeviceToHost, st));
+  SS_CUDA_TRY(cudaStreamSynchronize(st));
+  if (m > 0) {
+    if (int rc = launch_rank(G, id, m, perm, w + orank, (int64_t)rank_workspace_bytes(m), st)) return rc;
+    if (int rc = launch_query_gather(G, id, perm, m, h->seq, h->lens, a, out_key, out_seq, out_len, st))
+      return rc;
+    SS_CUDA_TRY(cudaStreamSynchronize(st));
+  }
+  *n_out = m;
   return SS_OK;
 }
 
@@ -617,14 +812,14 @@ static int round_impl(ss_bank* h, const int8_t* q, const float* q_inv, const int
                       int32_t max_len, int32_t nbins, int32_t algo, int32_t P, int32_t* npts,
                       int32_t* pbin, int32_t* pcnt, int64_t* pD, uint8_t* used_fb, double* G,
                       int64_t* perm, size_t extra_front, cudaStream_t st, bool do_rank = true,
-                      double* G_mirror = nullptr) {
+                      double* G_mirror = nullptr, const WideQ& wq = WideQ{}) {
   if (int rc = check_bins(max_len, nbins)) return rc;
   if (P < nbins) return set_error(SS_ERR_ARG, "P (%d) must be >= nbins (%d)", P, nbins);
   if (h->head <= 0) return set_error(SS_ERR_EMPTY, "cold start: the history window is empty");
   if (nq == 0) return SS_OK;
   RoundLayout L = round_layout(nq, k, nbins);
   size_t base = extra_front;
-  if (int rc = ws_reserve(h, base + L.end + topk_ws_need(h, nq, k, algo))) return rc;
+  if (int rc = ws_reserve(h, base + L.end + topk_ws_need(h, nq, k, algo, wq))) return rc;
   char* ws = (char*)h->ws + base;
   uint64_t* comp = reinterpret_cast<uint64_t*>(ws + L.comp);
   int32_t* len = reinterpret_cast<int32_t*>(ws + L.len);
@@ -640,6 +835,7 @@ static int round_impl(ss_bank* h, const int8_t* q, const float* q_inv, const int
   int slices = 1;
   if (int rc = topk_plan(h, a, algo, slices)) return rc;
   uint64_t* partials = reinterpret_cast<uint64_t*>((char*)h->ws + base + L.end);
+  char* scratch = (char*)partials + align_up((size_t)(slices + (wide_on(h, wq) ? 1 : 0)) * nq * k * 8);
   // fork: the window's fallback law (1 CTA) overlaps the similarity kernel,
   // which leaves SMs free (slices x query tiles <= the SM count)
   SS_CUDA_TRY(cudaEventRecord(h->ev_fork, st));
@@ -647,11 +843,11 @@ static int round_impl(ss_bank* h, const int8_t* q, const float* q_inv, const int
   int rc = launch_fallback_hist(h->len_cnt, max_len, nbins, fb, fb + nbins, fb + 2 * nbins, h->side);
   if (rc) return rc;
   SS_CUDA_TRY(cudaEventRecord(h->ev_join, h->side));
-  rc = (algo == SS_ALGO_TCGEN05) ? launch_topk_tc(a, partials, slices, st)
-                                 : launch_topk_scan(a, partials, slices, st);
+  int nlists = slices;
+  rc = stage1(h, a, algo, slices, wq, partials, scratch, st, &nlists);
   SS_CUDA_TRY(cudaStreamWaitEvent(st, h->ev_join, 0));  // join before any early return
   if (rc) return rc;
-  rc = launch_merge_finish(partials, slices, nq, k, h->lens, h->head, h->gcap, h->slot_offset, comp,
+  rc = launch_merge_finish(partials, nlists, nq, k, h->lens, h->head, h->gcap, h->slot_offset, comp,
                            len, min_matches, max_len, nbins, input_len, fb, fb + nbins,
                            fb + 2 * nbins, P, npts, pbin, pcnt, pD, nullptr, used_fb, G, st,
                            G_mirror);
@@ -670,6 +866,21 @@ int ss_schedule_round(ss_bank_t* h, const int8_t* q, const float* q_inv, const i
   if (!h) return set_error(SS_ERR_ARG, "null bank");
   return round_impl(h, q, q_inv, input_len, ids, nq, k, theta, min_matches, max_len, nbins, algo, P,
                     npts, pbin, pcnt, pD, used_fb, G, perm, 0, (cudaStream_t)stream);
+}
+
+int ss_schedule_round_wide(ss_bank_t* h, const int8_t* q, const float* q_inv,
+                           const int32_t* input_len, const int64_t* ids, int64_t nq, int64_t n_wide,
+                           const int64_t* wide_idx, const int16_t* wide_q_emb,
+                           const float* wide_q_inv, int32_t k, float theta, int32_t min_matches,
+                           int32_t max_len, int32_t nbins, int32_t algo, int32_t P, int32_t* npts,
+                           int32_t* pbin, int32_t* pcnt, int64_t* pD, uint8_t* used_fb, double* G,
+                           int64_t* perm, void* stream) {
+  if (!h) return set_error(SS_ERR_ARG, "null bank");
+  WideQ wq;
+  if (int rc = wide_q(n_wide, wide_idx, wide_q_emb, wide_q_inv, &wq)) return rc;
+  return round_impl(h, q, q_inv, input_len, ids, nq, k, theta, min_matches, max_len, nbins, algo, P,
+                    npts, pbin, pcnt, pD, used_fb, G, perm, 0, (cudaStream_t)stream, true, nullptr,
+                    wq);
 }
 
 static bool is_pinned(const void* p) {
@@ -714,7 +925,7 @@ static int host_round_enqueue(ss_bank* h, const int8_t* q_host, const float* q_i
   size_t oG = o; o += align_up((size_t)nq * 8);
   size_t operm = o; o += align_up((size_t)nq * 8);
   RoundLayout L = round_layout(nq, k, nbins);
-  if (int rc = ws_reserve(h, o + L.end + topk_ws_need(h, nq, k, algo))) return rc;
+  if (int rc = ws_reserve(h, o + L.end + topk_ws_need(h, nq, k, algo, WideQ{}))) return rc;
   char* w = (char*)h->ws;
   SS_CUDA_TRY(cudaMemcpyAsync(w + oq, q_host, (size_t)nq * h->dim, cudaMemcpyHostToDevice, st));
   SS_CUDA_TRY(cudaMemcpyAsync(w + oqi, q_inv_host, (size_t)nq * 4, cudaMemcpyHostToDevice, st));
@@ -751,6 +962,7 @@ int ss_schedule_round_host(ss_bank_t* h, const int8_t* q_host, const float* q_in
   memset(&key, 0, sizeof(key));
   key.nq = nq; key.head = h->head; key.k = k; key.min_matches = min_matches;
   key.max_len = max_len; key.nbins = nbins; key.algo = algo; key.theta = theta;
+  key.any_wide = h->any_wide;
   const void* ptrs[6] = {q_host, q_inv_host, input_len_host, ids_host, G_host, perm_host};
   memcpy(key.ptr, ptrs, sizeof(ptrs));
   key.ws_gen = h->ws_gen;
@@ -816,9 +1028,9 @@ int bank_push_gather(ss_bank* h, const int8_t* src_emb, const float* src_inv,
     return set_error(SS_ERR_ARG, "push on a shard: use ss_bank_write with the global head");
   if (n <= 0) return SS_OK;
   const int64_t skip = n > h->cap ? n - h->cap : 0;
-  int rc = launch_bank_write(h->emb, h->inv, h->lens, h->seq, h->len_cnt, h->dim, src_emb, src_inv,
-                             src_lens, nullptr, nullptr, n, h->head, h->cap, skip, h->d_err, st,
-                             src_idx);
+  int rc = launch_bank_write(h->emb, h->inv, h->lens, h->seq, h->len_cnt, h->dim, src_emb, 1,
+                             src_inv, src_lens, nullptr, nullptr, n, h->head, h->cap, skip,
+                             h->d_err, st, src_idx, h->wp.flag ? &h->wp : nullptr);
   if (rc) return rc;
   h->head += n;
   return SS_OK;

@@ -42,20 +42,47 @@ int launch_gittins_dist(const double* support, const double* masses, const int64
                         const double* attained, const double* outlived, int64_t n,
                         int64_t stride, double* out, int* err, int ref_mode, cudaStream_t st);
 int launch_embed(const int64_t* tokens, const int64_t* offsets, int64_t n, uint64_t salt,
-                 int dim, double* out_f64, int8_t* out_i8, float* out_inv, int* err,
+                 int dim, double* out_f64, int16_t* out_i16, float* out_inv, int* err,
                  cudaStream_t st);
 int launch_cost_dist(int kind, double w_in, double w_out, const double* I, const double* ls,
                      const int64_t* npts, int64_t n, int64_t stride, double* out,
                      cudaStream_t st);
 
-// bank maintenance (k_bank.cu)
+// The bank's wide plane (lazily allocated on the first int16 push): exact
+// int16 vectors of rows whose feature-hash buckets exceed int8, per slot.
+struct WidePlane {
+  int16_t* emb = nullptr;   // [cap, dim]
+  float* inv = nullptr;     // [cap] true inverse norm of a wide row
+  uint8_t* flag = nullptr;  // [cap] 1 = the slot holds a wide row
+  int* count = nullptr;     // device counter of wide rows written (host reads it after a push)
+};
+
+// bank maintenance (k_bank.cu); src_bytes = 1 (int8 rows) or 2 (int16 rows)
 int launch_bank_write(int8_t* emb, float* inv, int32_t* lens, int64_t* seq, int32_t* len_cnt,
-                      int dim, const int8_t* src_emb, const float* src_inv,
+                      int dim, const void* src_emb, int src_bytes, const float* src_inv,
                       const int32_t* src_lens, const int64_t* src_seq, const int64_t* src_slot,
                       int64_t n, int64_t first_seq, int64_t capacity, int64_t skip, int* err,
-                      cudaStream_t st, const int64_t* src_idx = nullptr);
+                      cudaStream_t st, const int64_t* src_idx = nullptr,
+                      const WidePlane* wp = nullptr);
 int launch_fallback_hist(const int32_t* len_cnt, int max_len, int nbins, int64_t* cnt,
                          int64_t* sv, int64_t* sv2, cudaStream_t st);
+
+// wide queries of a batch (feature-hash vectors outside int8): their indices
+// in the batch, exact int16 vectors and inverse norms (k_wide.cu)
+struct WideQ {
+  int64_t n = 0;
+  const int64_t* idx = nullptr;  // [n] query indices
+  const int16_t* q = nullptr;    // [n, dim]
+  const float* inv = nullptr;    // [n]
+};
+// the bank's side of the wide pass
+struct WideBank {
+  bool any = false;          // the bank has received a wide row
+  WidePlane plane;
+  int64_t* list = nullptr;   // [cap] scratch: compacted wide slots
+  int* list_count = nullptr;
+  const int32_t* bank_lens = nullptr;
+};
 
 // similarity + top-k
 struct TopkArgs {
@@ -92,6 +119,19 @@ bool topk_tc_supported(const TopkArgs& a);
 bool topk_ts_supported(const TopkArgs& a);
 int topk_ts_lists(const TopkArgs& a, int device);
 int launch_topk_ts(const TopkArgs& a, uint64_t* partials, int n_lists, cudaStream_t st);
+
+// the wide pass (k_wide.cu): one more candidate list per query, written to
+// list_out [nq][k]; ws of wide_ws_bytes()
+size_t wide_ws_bytes(const WideQ& wq, int64_t nq, int k, int64_t n_rows, int sms);
+int launch_wide_pass(const WideBank& wb, const TopkArgs& a, const WideQ& wq, uint64_t* list_out,
+                     void* ws, int device, cudaStream_t st);
+
+// query_similar of one query over the whole bank (k_wide.cu)
+int launch_query_all(const TopkArgs& a, const int64_t* seq, const WideBank& wb, const int16_t* q16,
+                     float iq, double* G, int64_t* id, int* count, cudaStream_t st);
+int launch_query_gather(const double* G, const int64_t* id, const int64_t* perm, int64_t m,
+                        const int64_t* seq, const int32_t* lens, const TopkArgs& a, float* key,
+                        int64_t* out_seq, int32_t* out_len, cudaStream_t st);
 
 // Receive buffers of every rank for the fused merge + exchange (k_merge with
 // po.world > 0): rank r's [world][nq_local][k] rows, IPC-mapped into this process.

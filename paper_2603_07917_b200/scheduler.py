@@ -21,7 +21,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .history import HistoryWindow
+from .history import HistoryWindow, _as_vectors, split_wide
 
 __all__ = ["BatchPlan", "pack_batch", "RoundConfig", "PredictState", "RequestTable", "SageScheduler", "rank"]
 
@@ -161,7 +161,7 @@ class SageScheduler:
     # ---------------------------------------------------------- stages 1-3 --
     def predict(self, q, q_inv, input_len, stream=None) -> PredictState:
         c = self.cfg
-        q = torch.as_tensor(q, device="cuda").to(torch.int8).contiguous()
+        q = _as_vectors(q)  # int8, or int16 exact counts (wide pass)
         q_inv = torch.as_tensor(q_inv, device="cuda").to(torch.float32).contiguous()
         I = torch.as_tensor(input_len, device="cuda").to(torch.int32).contiguous()
         if len(self.window) == 0:
@@ -221,11 +221,25 @@ class SageScheduler:
     def schedule_round(self, q, q_inv, input_len, ids=None, out=None, stream=None):
         """One fused round for a batch of pending requests (device tensors).
 
-        Returns (perm int64 [n], G float64 [n], PredictState-like buffers)."""
+        Returns (perm int64 [n], G float64 [n], PredictState-like buffers).
+        int16 queries (exact feature-hash counts beyond int8) run the wide
+        pass for the rows that need it (ss_schedule_round_wide)."""
         c = self.cfg
         n = q.shape[0]
         if out is None:
             out = self.round_buffers(n)
+        if q.dtype != torch.int8:
+            q8, qi, widx, wq, winv = split_wide(_as_vectors(q), q_inv)
+            if widx is not None:
+                _lib.call("ss_schedule_round_wide", self.window.handle, _lib.ptr(q8), _lib.ptr(qi),
+                          _lib.ptr(input_len), _lib.ptr(ids), n, widx.numel(), _lib.ptr(widx),
+                          _lib.ptr(wq), _lib.ptr(winv), c.k, float(np.float32(c.theta)),
+                          c.min_matches, c.max_len, c.nbins, _lib.ALGO[c.algo], c.nbins,
+                          _lib.ptr(out["npts"]), _lib.ptr(out["pbin"]), _lib.ptr(out["pcnt"]),
+                          _lib.ptr(out["pD"]), _lib.ptr(out["used_fb"]), _lib.ptr(out["G"]),
+                          _lib.ptr(out["perm"]), _lib.stream_ptr(stream))
+                return out["perm"], out["G"], out
+            q = q8
         _lib.call("ss_schedule_round", self.window.handle, _lib.ptr(q), _lib.ptr(q_inv),
                   _lib.ptr(input_len), _lib.ptr(ids), n, c.k, float(np.float32(c.theta)),
                   c.min_matches, c.max_len, c.nbins, _lib.ALGO[c.algo], c.nbins,

@@ -117,6 +117,119 @@ def test_embed_quantize_and_push(cuda):
     assert np.array_equal(gi[~np.isnan(ri)], ri[~np.isnan(ri)])
 
 
+def _long_prompts(rng, n_normal, dim=384):
+    """Normal prompts plus long ones that repeat a token 300-600 times (their
+    feature-hash buckets leave the int8 range, _kernels.py:82-95)."""
+    normal = [rng.integers(0, 50000, int(rng.integers(5, 200))) for _ in range(n_normal)]
+    longp = []
+    for j in range(6):
+        tok = int(rng.integers(0, 50000))
+        body = np.concatenate([np.full(300 + 50 * j, tok), rng.integers(0, 50000, 40 + j)])
+        longp.append(body)
+    return normal, longp
+
+
+def test_embed_wide_prompt_exact(cuda):
+    """A prompt with 300+ repeats of one token: the device embedding keeps the
+    exact counts (int16), equal to the reference embed_accumulate, with the
+    inverse norm of the exact sum of squares."""
+    from paper_2603_07917_b200.history import DEFAULT_SALT, embed_batch
+    rng = np.random.default_rng(8)
+    normal, longp = _long_prompts(rng, 10)
+    prompts = normal + longp
+    e, inv = embed_batch(prompts, DEFAULT_SALT, 384)
+    assert e.dtype == torch.int16
+    ref = np.stack([O.embed_accumulate(p, DEFAULT_SALT, 384) for p in prompts]).astype(np.int64)
+    assert np.abs(ref[len(normal):]).max() >= 300
+    assert np.array_equal(e.cpu().numpy().astype(np.int64), ref)
+    assert np.array_equal(inv.cpu().numpy(), O.inv_norm(ref))
+    e8, _ = embed_batch(normal, DEFAULT_SALT, 384)  # no wide row: the int8 layout
+    assert e8.dtype == torch.int8 and np.array_equal(e8.cpu().numpy(), ref[:len(normal)])
+
+
+@pytest.mark.parametrize("theta", [0.3, -1.0])
+def test_wide_rows_and_queries_bit_exact(cuda, theta):
+    """embed -> push -> top-k / round with long prompts on both sides: wide
+    rows in the bank (among int8 rows), wide queries in the batch (among int8
+    queries), near-duplicates of the wide prompts so that wide rows are the
+    true neighbours; neighbour lists and Gittins indices equal the oracle's
+    bit for bit (the TS kernel at nq > 128, the streaming kernel below)."""
+    from paper_2603_07917_b200.history import DEFAULT_SALT, HistoryWindow, embed_batch
+    from paper_2603_07917_b200.scheduler import RoundConfig, SageScheduler
+    rng = np.random.default_rng(12)
+    n = 5000
+    bank_e, bank_l, _, _ = O.make_bank(n, 384, 40, 2)
+    normal, longp = _long_prompts(rng, 4)
+    le, _ = embed_batch(longp, DEFAULT_SALT, 384)
+    le = le.cpu().numpy()
+    # bank: int8 rows, then the long prompts and perturbed copies of them
+    wide_rows = np.concatenate([le, le + rng.integers(-3, 4, le.shape), le * 2]).astype(np.int16)
+    rows = np.concatenate([bank_e.astype(np.int16), wide_rows])
+    lens = np.concatenate([bank_l, rng.integers(1, 2049, wide_rows.shape[0]).astype(np.int32)])
+    w = HistoryWindow(rows.shape[0] + 64, 384)
+    w.push(bank_e[:2500], bank_l[:2500])              # int8 push
+    w.push(rows[2500:], lens[2500:])                  # int16 push: int8 rows + wide rows
+    seq = np.arange(rows.shape[0])
+    rinv = O.inv_norm(rows)
+    for nq in (40, 300):
+        q8 = O.make_bank(nq, 384, 40, 2 + nq)[0].astype(np.int16)
+        q = np.concatenate([le.astype(np.int16), (le[:3] + 1).astype(np.int16), q8])[:nq]
+        qi = O.inv_norm(q)
+        keys = O.scores(q, qi, rows, rinv)
+        comp, ln = w.topk(q, qi, 32, theta)
+        key, gseq, _ = w.decode(comp)
+        key, gseq, ln = key.cpu().numpy(), gseq.cpu().numpy(), ln.cpu().numpy()
+        for i in range(nq):
+            sel = O.select_topk(keys[i], seq, 32, theta)
+            m = sel.size
+            assert np.array_equal(gseq[i, :m], seq[sel]), (nq, i)
+            assert np.array_equal(key[i, :m], keys[i, sel]), (nq, i)
+            assert np.array_equal(ln[i, :m], lens[sel]), (nq, i)
+        # the wide rows are found: the first query's best neighbour is its own prompt
+        assert gseq[0, 0] >= n
+        I = rng.integers(1, 4097, nq).astype(np.int32)
+        ids = np.arange(nq, dtype=np.int64)
+        cfg = RoundConfig(k=32, theta=theta, min_matches=10, max_len=2048, nbins=64)
+        perm, G, _ = SageScheduler(w, cfg).schedule_round(_t(q), _t(qi), _t(I), _t(ids))
+        ref = O.predict_round(keys, seq, lens, I, 32, theta, 10, 2048, 64, window_lens=lens)
+        Gr = np.array([r["G"] for r in ref])
+        assert np.array_equal(G.cpu().numpy(), Gr)
+        assert np.array_equal(perm.cpu().numpy(), O.rank(Gr, ids))
+    # an int8 push over a wide slot clears it (the ring wraps onto the wide rows)
+    w2 = HistoryWindow(8, 384)
+    w2.push(wide_rows[:4], np.arange(1, 5, dtype=np.int32))
+    w2.push(bank_e[:8], bank_l[:8])  # evicts every wide row
+    qq = wide_rows[:1]
+    c2, _ = w2.topk(qq, O.inv_norm(qq), 8, -1.0)
+    _, s2, _ = w2.decode(c2)
+    assert sorted(s2[0].cpu().numpy().tolist()) == list(range(4, 12))
+
+
+@pytest.mark.parametrize("theta", [0.8, 0.0, -1.0])
+def test_query_similar_returns_every_match(cuda, theta):
+    """query_similar returns ALL records with cos >=
+    theta (theta = -1: the whole window) ordered by cos desc, ties by the
+    larger insertion_seq -- beyond any top-k cap -- on a wrapped ring with
+    exact duplicates and a wide row."""
+    from paper_2603_07917_b200.history import HistoryWindow, query_similar
+    n, cap = 12_000, 10_000
+    emb, lens, _, _ = O.make_bank(n + 1, 384, 20, 4)
+    emb[3000:3030] = emb[n]  # 30 exact duplicates of the query (ties), inside the live window
+    rows = emb[:n].astype(np.int16)
+    rows[5000] = rows[5000] * 3  # a wide row (|x| up to 381)
+    w = HistoryWindow(cap, 384)
+    w.push(rows, lens[:n])
+    live = np.arange(n - cap, n)
+    q = emb[n]
+    keys = O.scores(q[None], O.inv_norm(q[None]), rows[live], O.inv_norm(rows[live]))[0]
+    seq, cos, ln = query_similar(w, q, O.inv_norm(q[None])[0], theta)
+    ref = O.query_similar(keys, live, theta)
+    assert seq.size == ref.size and (theta > -1.0 or seq.size == cap)
+    assert ref.size > 256 or theta > 0.5
+    assert np.array_equal(seq, live[ref]) and np.array_equal(cos, keys[ref])
+    assert np.array_equal(ln, lens[live[ref]])
+
+
 def test_cost_distribution_vs_reference(cuda, golden):
     from paper_2603_07917_b200.cost import ResourceBound, cost_distribution
     from paper_2603_07917_b200.distribution import DiscreteDistribution
