@@ -63,6 +63,7 @@ __device__ __forceinline__ void rt_offer(const RunTopk& r, uint64_t c) {
 }
 
 // all threads; leaves the top-k (descending, 0-padded) in sel[0..kpad)
+// and its size in *r.cnt
 __device__ void rt_compact(const RunTopk& r, int k, int kpad, int32_t* pay, uint64_t* sel,
                            int32_t* spay, int* hist, int* misc) {
   __syncthreads();
@@ -78,6 +79,13 @@ __device__ void rt_compact(const RunTopk& r, int k, int kpad, int32_t* pay, uint
     if (kept == k) *r.floor_c = sel[k - 1];
   }
   __syncthreads();
+}
+
+// a candidate list as the merges read it: its m entries first, then zeros;
+// ascending, so a full list is a min-heap with its minimum at entry 0 (the
+// k-th-best bound k_merge_finish_w takes from entry 0)
+__device__ __forceinline__ void write_list(const uint64_t* sel_desc, int m, int k, uint64_t* out) {
+  for (int i = threadIdx.x; i < k; i += blockDim.x) out[i] = (i < m) ? sel_desc[m - 1 - i] : 0ull;
 }
 
 __device__ __forceinline__ uint64_t wide_comp(long long dot, float iw, float iq, float theta,
@@ -136,7 +144,7 @@ k_wide_rows(const int8_t* __restrict__ q, const float* __restrict__ q_inv, int64
     }
   }
   rt_compact(rt, k, kpad, pay, sel, spay, hist, misc);
-  for (int i = threadIdx.x; i < k; i += blockDim.x) out[qi * k + i] = sel[i];
+  write_list(sel, cnt, k, out + qi * k);
 }
 
 // Wide queries x one row range of the bank (int8 rows of the main plane, the
@@ -221,19 +229,26 @@ k_wide_scan(const int8_t* __restrict__ emb, const float* __restrict__ inv,
     }
     for (int j = 0; j < nwq; ++j) {
       rt_compact(RunTopk{cand[j], &cnt[j], &floor_c[j]}, k, kpad, pay, sel, spay, hist, misc);
-      uint64_t* o = out + ((int64_t)blockIdx.x * n_wq + w0 + j) * k;
-      for (int i = threadIdx.x; i < k; i += blockDim.x) o[i] = sel[i];
+      write_list(sel, cnt[j], k, out + ((int64_t)blockIdx.x * n_wq + w0 + j) * k);
     }
     __syncthreads();
   }
 }
 
-// merged wide-query rows -> their query's list
+// merged wide-query rows (descending, zero-padded) -> their query's list
 __global__ void k_wide_scatter(const uint64_t* __restrict__ src, const int64_t* __restrict__ idx,
                                int n, int k, uint64_t* __restrict__ out) {
+  __shared__ int m;
   const int w = blockIdx.x;
   if (w >= n) return;
-  for (int i = threadIdx.x; i < k; i += blockDim.x) out[idx[w] * k + i] = src[(int64_t)w * k + i];
+  const uint64_t* row = src + (int64_t)w * k;
+  if (threadIdx.x == 0) {
+    int c = 0;
+    while (c < k && row[c] != 0ull) ++c;
+    m = c;
+  }
+  __syncthreads();
+  write_list(row, m, k, out + idx[w] * k);
 }
 
 static int wide_scan_ctas(int64_t n_rows, int sms) {

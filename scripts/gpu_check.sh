@@ -3,7 +3,7 @@
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/gpu.txt 2>&1
-timeout 1500 python -m pytest tests -m gpu -x -q ${PYTEST_ARGS} > gpurun_out/pytest.log 2>&1
+if [ -n "$PYTEST_K" ]; then timeout 1500 python -m pytest tests -m gpu -q -k "$PYTEST_K" > gpurun_out/pytest.log 2>&1; else timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest.log 2>&1; fi
 echo "pytest rc=$?" >> gpurun_out/pytest.log
 tail -3 gpurun_out/pytest.log
 if [ -z "$NO_BENCH" ]; then
