@@ -262,9 +262,12 @@ def gittins_points(c, D, I=None, g=0, bucket=200):
 
     attained a = cost(I, g) = g^2/2 + I*g, 2a = A2 = g*g + 2*I*g (int64).
     survivors: s_k > a  <=>  D_k > A2 * c_k          (SPEC.md:338)
-    ratio_k  = (0.5*(P'_k - A2*C'_k) + ((D_k - A2*c_k)*0.5/c_k)*(T'-C'_k)) / C'_k
+    d_k = D_k - A2*c_k, P'_k / C'_k prefix sums over survivors, T' = C'_last:
+    ratio_k  = (0.5*P'_k + (d_k/(2 c_k))*(T'-C'_k)) / C'_k      (_kernels.py:113
+             = (P'_k*c_k + d_k*(T'-C'_k)) / (2*c_k*C'_k)          with masses c/T')
+    evaluated in that second form: exact int64 sums, f64 products, ONE divide.
     none survive -> cost(I, g+bucket) - cost(I, g)
-    Same operation order as the CUDA kernel (no FMA), so bit-identical.
+    Same operation order as the CUDA kernels (no FMA), so bit-identical.
     """
     c = np.asarray(c, np.int64)
     D = np.asarray(D, np.int64)
@@ -278,9 +281,8 @@ def gittins_points(c, D, I=None, g=0, bucket=200):
     C = np.cumsum(cs)
     P = np.cumsum(Ds)
     T = C[-1]
-    sk = (Ds.astype(F64) * 0.5) / cs.astype(F64)
-    num = P.astype(F64) * 0.5 + sk * (T - C).astype(F64)
-    ratio = num / C.astype(F64)
+    num = P.astype(F64) * cs.astype(F64) + Ds.astype(F64) * (T - C).astype(F64)
+    ratio = num / ((2.0 * cs.astype(F64)) * C.astype(F64))
     return float(ratio.min())
 
 

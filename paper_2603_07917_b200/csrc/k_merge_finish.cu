@@ -134,11 +134,19 @@ int launch_decode(const uint64_t* comp, int64_t n, int64_t head, int64_t capacit
 // exact integer-count Gittins over a sorted sparse law (one warp).
 //   D_k = sum v^2 + 2 I sum v over bin k  (so c_k s_k = D_k / 2 exactly)
 //   attained 2a = A2 = g^2 + 2 I g; survivors D_k > A2 c_k (a suffix)
-//   ratio_k = (0.5 P'_k + ((D_k - A2 c_k) 0.5 / c_k) (T' - C'_k)) / C'_k
-//   P'_k = sum_{j<=k surv} (D_j - A2 c_j), C'_k = sum c_j, T' = C'_last
-// All integer sums are exact, the fp64 ops are explicit _rn (no FMA
-// contraction) in the same order as oracle.gittins_points -> bit-identical.
+//   ratio_k = (0.5 P'_k + s'_k (T' - C'_k)) / C'_k,  s'_k = d_k / (2 c_k),
+//           = (P'_k c_k + d_k (T' - C'_k)) / (2 c_k C'_k)   (one divide)
+//   d_k = D_k - A2 c_k, P'_k = sum_{j<=k surv} d_j, C'_k = sum c_j, T' = C'_last
+// -- the algebra of _kernels.py:110-115 (cum_xp + s (1 - cum_p)) / cum_p with
+// masses c/T'.  Integer sums are exact; the fp64 ops are explicit _rn (no FMA
+// contraction) in the order of oracle.gittins_points -> bit-identical.
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ double gittins_ratio(long long P, long long C, long long T, long long ck,
+                                                long long dk) {
+  const double num = __dadd_rn(__dmul_rn((double)P, (double)ck), __dmul_rn((double)dk, (double)(T - C)));
+  return __ddiv_rn(num, __dmul_rn(2.0 * (double)ck, (double)C));
+}
+
 __device__ double warp_gittins_exact(const int32_t* c, const int64_t* D, int np, long long A2,
                                      int I, int g, int bucket, int lane) {
   int first = np;
@@ -167,12 +175,7 @@ __device__ double warp_gittins_exact(const int32_t* c, const int64_t* D, int np,
     }
     long long C = warp_incl_scan_i64(ck, lane) + Cc;
     long long P = warp_incl_scan_i64(dk, lane) + Pc;
-    if (k < np) {
-      double sk = __ddiv_rn(__dmul_rn((double)dk, 0.5), (double)ck);
-      double num = __dadd_rn(__dmul_rn((double)P, 0.5), __dmul_rn(sk, (double)(T - C)));
-      double r = __ddiv_rn(num, (double)C);
-      best = fmin(best, r);
-    }
+    if (k < np) best = fmin(best, gittins_ratio(P, C, T, ck, dk));
     Cc = __shfl_sync(0xffffffffu, C, 31);
     Pc = __shfl_sync(0xffffffffu, P, 31);
   }
@@ -739,11 +742,20 @@ int launch_merge_finish(const uint64_t* partials, int nlists, int64_t nq, int k,
 // is warp-converged.
 // ---------------------------------------------------------------------------
 constexpr int RF_GL = 8;
+constexpr int RF_R = 8;  // chunks of RF_GL points kept in registers between the passes
 
 __device__ __forceinline__ long long grp_incl_scan_i64(long long v, int gl) {
 #pragma unroll
   for (int o = 1; o < RF_GL; o <<= 1) {
     const long long t = __shfl_up_sync(0xffffffffu, v, o, RF_GL);
+    if (gl >= o) v += t;
+  }
+  return v;
+}
+__device__ __forceinline__ int grp_incl_scan_i32(int v, int gl) {
+#pragma unroll
+  for (int o = 1; o < RF_GL; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, v, o, RF_GL);
     if (gl >= o) v += t;
   }
   return v;
@@ -773,34 +785,57 @@ k_refresh(int64_t n, const int32_t* __restrict__ I, const int32_t* __restrict__ 
   const long long A2 = (long long)g * g + 2 * Ii * g;
   const int32_t* c = pcnt + (live ? i : 0) * (int64_t)P;
   const int64_t* D = pD + (live ? i : 0) * (int64_t)P;
-  // pass 1: total surviving count
+  // pass 1: the surviving (c_k, d_k = D_k - A2 c_k) -- the first RF_R chunks
+  // kept in registers -- and their total count T (one read of the law)
+  int cr[RF_R];
+  long long dr[RF_R];
   long long T = 0;
-  for (int b = 0; b < npmax; b += RF_GL) {
+#pragma unroll
+  for (int j = 0; j < RF_R; ++j) {
+    const int k = j * RF_GL + gl;
+    int ck = 0;
+    long long dk = 0;
+    if (k < np) {
+      const int cv = c[k];
+      const long long dv = D[k] - A2 * cv;
+      if (dv > 0) { ck = cv; dk = dv; }
+    }
+    cr[j] = ck;
+    dr[j] = dk;
+    T += ck;
+  }
+  for (int b = RF_R * RF_GL; b < npmax; b += RF_GL) {  // long laws: the rest is re-read below
     const int k = b + gl;
     if (k < np) {
-      const long long ck = c[k];
-      if (D[k] > A2 * ck) T += ck;
+      const int cv = c[k];
+      if (D[k] > A2 * cv) T += cv;
     }
   }
   T = grp_sum_i64(T);
   // pass 2: prefix sums and the ratio at every surviving point
   long long Cc = 0, Pc = 0;
   double best = INFINITY;
-  for (int b = 0; b < npmax; b += RF_GL) {
+#pragma unroll
+  for (int j = 0; j < RF_R; ++j) {
+    if (j * RF_GL >= npmax) break;  // warp-uniform
+    const long long C = grp_incl_scan_i32(cr[j], gl) + Cc;
+    const long long Pp = grp_incl_scan_i64(dr[j], gl) + Pc;
+    if (cr[j] > 0) best = fmin(best, gittins_ratio(Pp, C, T, cr[j], dr[j]));
+    Cc = __shfl_sync(0xffffffffu, C, RF_GL - 1, RF_GL);
+    Pc = __shfl_sync(0xffffffffu, Pp, RF_GL - 1, RF_GL);
+  }
+  for (int b = RF_R * RF_GL; b < npmax; b += RF_GL) {
     const int k = b + gl;
-    long long ck = 0, dk = 0;
+    int ck = 0;
+    long long dk = 0;
     if (k < np) {
-      const long long cv = c[k];
+      const int cv = c[k];
       const long long dv = D[k] - A2 * cv;
       if (dv > 0) { ck = cv; dk = dv; }
     }
-    const long long C = grp_incl_scan_i64(ck, gl) + Cc;
+    const long long C = grp_incl_scan_i32(ck, gl) + Cc;
     const long long Pp = grp_incl_scan_i64(dk, gl) + Pc;
-    if (ck > 0) {
-      const double sk = __ddiv_rn(__dmul_rn((double)dk, 0.5), (double)ck);
-      const double num = __dadd_rn(__dmul_rn((double)Pp, 0.5), __dmul_rn(sk, (double)(T - C)));
-      best = fmin(best, __ddiv_rn(num, (double)C));
-    }
+    if (ck > 0) best = fmin(best, gittins_ratio(Pp, C, T, ck, dk));
     Cc = __shfl_sync(0xffffffffu, C, RF_GL - 1, RF_GL);
     Pc = __shfl_sync(0xffffffffu, Pp, RF_GL - 1, RF_GL);
   }

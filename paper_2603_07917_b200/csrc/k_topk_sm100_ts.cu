@@ -50,12 +50,39 @@ __device__ __forceinline__ void bar_expect(uint64_t* b, uint32_t bytes) {
 __device__ __forceinline__ void bar_arrive(uint64_t* b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(b)) : "memory");
 }
-__device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity) {
+#ifndef SS_TS_SLEEP
+#define SS_TS_SLEEP 1
+#endif
+// waits with a suspend-time hint (the thread sleeps in the barrier instead of
+// spinning) -- the epilogue warps' form -- and without (the single-thread
+// producer / MMA issuer, whose wake-up latency would delay the pipeline)
+__device__ __forceinline__ void bar_wait_sleep(uint64_t* b, uint32_t parity) {
   asm volatile(
       "{\n.reg .pred p;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
       "@!p bra W_%=;\n}\n" ::"r"(su32(b)),
-      "r"(parity), "r"(0x989680)  // suspend-time hint: sleep in the barrier, do not spin
+      "r"(parity), "r"(0x989680)
       : "memory");
+}
+__device__ __forceinline__ void bar_wait_spin(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra W_%=;\n}\n" ::"r"(su32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity) {
+#if SS_TS_SLEEP == 1
+  bar_wait_sleep(b, parity);
+#else
+  bar_wait_spin(b, parity);
+#endif
+}
+__device__ __forceinline__ void bar_wait_epi(uint64_t* b, uint32_t parity) {
+#if SS_TS_SLEEP >= 1
+  bar_wait_sleep(b, parity);
+#else
+  bar_wait_spin(b, parity);
+#endif
 }
 __device__ __forceinline__ void tma2d(void* dst, const CUtensorMap* m, uint64_t* b, int c0, int c1) {
   asm volatile(
@@ -383,7 +410,7 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
           if (m != 0u && m != ~0u) thr = fmaxf(thr, s_threshold(f32_unorder(m), iq));
         }
       }
-      bar_wait(&ifull[sl], (t / ISLOTS) & 1);
+      bar_wait_epi(&ifull[sl], (t / ISLOTS) & 1);
       {
         // NaN (zero row / past the end) never passes the exact test: leave it
         // out of the bounds
@@ -403,7 +430,7 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
         }
       }
       __syncwarp();
-      bar_wait(&tfull[acc], (t / NACC) & 1);
+      bar_wait_epi(&tfull[acc], (t / NACC) & 1);
       fence_after();
       const uint32_t tbase = tmem + lane_base + acc * BN + grp * HALF;
       // pull my chunks into registers, then hand the accumulator back

@@ -28,8 +28,9 @@ def main():
     ap.add_argument("--algo", default="tcgen05")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--time", action="store_true")
+    ap.add_argument("--lib", default=None, help="an experiment build of libsagesched.so")
     a = ap.parse_args()
-    _lib.load()
+    _lib.load(a.lib)
     emb, lens, _ = make_bank_device(a.rows, 384, 4096, 0)
     w = HistoryWindow(a.rows, 384)
     w.push(emb, lens)

@@ -33,7 +33,7 @@ __host__ __device__ constexpr uint32_t idesc(int n) {
   return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
 }
 
-__global__ void __launch_bounds__(128, 1) k_mma_peak(int tiles, int n, int a_tmem) {
+__global__ void __launch_bounds__(128, 1) k_mma_peak(int tiles, int n, int a_tmem, int nacc) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;                  // NKB x 16 KB
@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(128, 1) k_mma_peak(int tiles, int n, int a_tme
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t tmem = s_tmem;
-  const int acols = 2 * n;  // two accumulators, A (TS form) after them
+  const int acols = nacc * n;  // accumulators, A (TS form) after them
   if (a_tmem) {
     // every warp writes its lane quarter of A (96 columns of 4 int8)
     const int w = threadIdx.x >> 5;
@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(128, 1) k_mma_peak(int tiles, int n, int a_tme
   if (threadIdx.x == 0) {
     const uint32_t id = idesc(n);
     for (int t = 0; t < tiles; ++t) {
-      const uint32_t d = tmem + (t & 1) * n;
+      const uint32_t d = tmem + (t % nacc) * n;
       for (int kb = 0; kb < NKB; ++kb) {
 #pragma unroll
         for (int kk = 0; kk < BK / UK; ++kk) {
@@ -126,12 +126,14 @@ __global__ void __launch_bounds__(128, 1) k_mma_peak(int tiles, int n, int a_tme
 extern "C" {
 // ops per launch = 2 * 128 * n * DIM * tiles * n_cta
 int mma_peak_run(int n_cta, int tiles, int n, int a_in_tmem, void* stream) {
-  if (n < 8 || n > 256 || n % 16 || (a_in_tmem && 2 * n + DIM / 4 > 512)) return 1;
+  // as many accumulators (<= 2) as fit beside A
+  const int nacc = (!a_in_tmem || 2 * n + DIM / 4 <= 512) ? 2 : 1;
+  if (n < 8 || n > 256 || n % 16 || (a_in_tmem && nacc * n + DIM / 4 > 512)) return 1;
   const size_t smem = 1024 + (size_t)NKB * BM * BK + (size_t)NKB * n * BK;
   if (cudaFuncSetAttribute(k_mma_peak, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess)
     return 2;
-  k_mma_peak<<<n_cta, 128, smem, (cudaStream_t)stream>>>(tiles, n, a_in_tmem);
+  k_mma_peak<<<n_cta, 128, smem, (cudaStream_t)stream>>>(tiles, n, a_in_tmem, nacc);
   return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
 int mma_peak_dim(void) { return DIM; }
