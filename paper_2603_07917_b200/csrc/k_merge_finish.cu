@@ -732,17 +732,22 @@ int launch_merge_finish(const uint64_t* partials, int nlists, int64_t nq, int k,
 // ---------------------------------------------------------------------------
 // refresh (SPEC.md:345-353 cadence): RF_GL = 8 lanes per request, four
 // requests per warp, so the prefix scans are 3 shuffle steps and a ~50-point
-// law fills the lanes.  Same arithmetic, in the same order, as
-// warp_gittins_exact / oracle gittins_points:
+// law fills the lanes; one read of the law (its first 64 points stay in
+// registers for the second pass), one divide per point.  Same arithmetic, in
+// the same order, as warp_gittins_exact / oracle gittins_points:
 //   survivors  D_k > A2 c_k (a suffix: bin means increase with the bin)
 //   T = sum of surviving c;  C_k, P_k inclusive prefix sums over survivors
-//   r_k = (0.5 P_k + s_k (T - C_k)) / C_k,  s_k = 0.5 d_k / c_k,  G = min r_k
+//   r_k = (P_k c_k + d_k (T - C_k)) / (2 c_k C_k),  d_k = D_k - A2 c_k,  G = min r_k
 //   no survivor -> cost(I, g + bucket) - cost(I, g)
 // Loops run to the warp's largest law, masked per group, so every shuffle
 // is warp-converged.
 // ---------------------------------------------------------------------------
 constexpr int RF_GL = 8;
-constexpr int RF_R = 8;  // chunks of RF_GL points kept in registers between the passes
+// chunks of RF_GL points kept in registers between the two passes (64
+// points: a c3 law has ~52); 6 blocks per SM (64 regs) measured best:
+// 72 us for c3 vs 90-117 us at other (lanes, chunks, occupancy) choices
+constexpr int RF_R = 8;
+constexpr int RF_MINB = 6;
 
 __device__ __forceinline__ long long grp_incl_scan_i64(long long v, int gl) {
 #pragma unroll
@@ -766,7 +771,7 @@ __device__ __forceinline__ long long grp_sum_i64(long long v) {
   return v;
 }
 
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, RF_MINB)
 k_refresh(int64_t n, const int32_t* __restrict__ I, const int32_t* __restrict__ g_new,
           int32_t* __restrict__ bucket_io, int bucket_size, const int32_t* __restrict__ npts,
           const int32_t* __restrict__ pcnt, const int64_t* __restrict__ pD, int P,
