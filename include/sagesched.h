@@ -101,6 +101,17 @@ int ss_cost_distribution_batch(int32_t kind, double w_in, double w_out,
                                const double* input_len, const double* len_support,
                                const int64_t* npts, int64_t n, int64_t stride,
                                double* out_support, void* stream);
+/* Per-call forms of gittins_min (_kernels.py:104-116) and cost_distribution
+ * (cost.py:107-118) for the reference's scalar call pattern: HOST arrays in
+ * and out, one packed H2D copy through library-owned pinned staging, the
+ * kernel, one D2H, synchronise -- no allocation per call.  (A batched
+ * engine uses the *_batch forms or the fused round.)  gittins_min_host with a
+ * leading zero mass -> SS_ERR_ZERODIV, as numba raises; n = 0 -> +inf. */
+int ss_gittins_min_host(const double* support, const double* masses, int64_t n, double* out,
+                        void* stream);
+int ss_cost_distribution_host(int32_t kind, double w_in, double w_out, double input_len,
+                              const double* len_support, int64_t n, double* out_support,
+                              void* stream);
 
 /* ------------------------------------- history bank ----- */
 /* FIFO ring of (int8 embedding[dim], fp32 inverse norm, output length,

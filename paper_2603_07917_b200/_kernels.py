@@ -12,6 +12,8 @@ reference caller would pass them) or CUDA torch tensors (used in place).
 
 from __future__ import annotations
 
+import ctypes as C
+
 import numpy as np
 import torch
 
@@ -77,12 +79,20 @@ def gittins_min_batch(support: torch.Tensor, masses: torch.Tensor, npts: torch.T
 
 def gittins_min(support, masses) -> float:
     """min_k (cum_xp + s_k (1 - cum_p)) / cum_p over support points
-    (_kernels.py:104-116).  Leading zero mass raises ZeroDivisionError."""
+    (_kernels.py:104-116).  Leading zero mass raises ZeroDivisionError.
+
+    The reference's per-law call: host arrays through ss_gittins_min_host
+    (pinned staging, one copy each way, no allocation); an engine that has
+    many laws uses ``gittins_min_batch`` (device tensors, one launch)."""
     _lib.require_cuda()
-    s = _dev(support, torch.float64).reshape(1, -1)
-    m = _dev(masses, torch.float64).reshape(1, -1)
-    npts = torch.tensor([s.shape[1]], dtype=torch.int64, device="cuda")
-    return float(gittins_min_batch(s, m, npts).item())
+    s = np.ascontiguousarray(support, dtype=np.float64).reshape(-1)
+    m = np.ascontiguousarray(masses, dtype=np.float64).reshape(-1)
+    if s.size != m.size:
+        raise ValueError("support and masses differ in length")
+    out = C.c_double()
+    _lib.call("ss_gittins_min_host", s.ctypes.data, m.ctypes.data, s.size, C.byref(out),
+              _lib.stream_ptr())
+    return out.value
 
 
 def embed_accumulate_batch(tokens: torch.Tensor, offsets: torch.Tensor, salt: int, dim: int,

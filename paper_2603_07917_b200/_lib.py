@@ -31,6 +31,8 @@ SIGNATURES = {
     "ss_embed_accumulate_batch": (C.c_int, [P, P, I64, U64, I32, P, P]),
     "ss_embed_quantize_batch": (C.c_int, [P, P, I64, U64, I32, P, P, C.POINTER(I64), P]),
     "ss_cost_distribution_batch": (C.c_int, [I32, F64, F64, P, P, P, I64, I64, P, P]),
+    "ss_gittins_min_host": (C.c_int, [P, P, I64, C.POINTER(F64), P]),
+    "ss_cost_distribution_host": (C.c_int, [I32, F64, F64, F64, P, I64, P, P]),
     "ss_bank_create": (C.c_int, [C.POINTER(P), I32, I64, I32, I64, I64]),
     "ss_bank_destroy": (C.c_int, [P]),
     "ss_bank_push": (C.c_int, [P, P, P, P, I64, P]),

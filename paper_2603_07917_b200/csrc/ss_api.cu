@@ -4,6 +4,7 @@
 #include <stdarg.h>
 #include <stdio.h>
 #include <string.h>
+#include <math.h>
 
 #include <algorithm>
 #include <atomic>
@@ -259,6 +260,104 @@ int ss_cost_distribution_batch(int32_t kind, double w_in, double w_out, const do
     return set_error(SS_ERR_ARG, "weighted-sum weights must be positive");
   return launch_cost_dist(kind, w_in, w_out, input_len, len_support, npts, n, stride, out_support,
                           (cudaStream_t)stream);
+}
+
+// ------------------------------------------------- per-call host entry ----
+// The reference's scalar call pattern (one law per call, host arrays in and
+// out): one packed H2D copy from a library-owned pinned staging buffer, the
+// kernel, one D2H, one synchronise -- no allocation per call.  Staging is per
+// thread (a handle-less entry point may be called from several threads).
+struct HostStaging {
+  char* host = nullptr;  // pinned
+  char* dev = nullptr;
+  size_t bytes = 0;
+  int device = -1;
+  ~HostStaging() {
+    if (host) cudaFreeHost(host);
+    if (dev) cudaFree(dev);
+  }
+  int reserve(size_t need) {
+    int d = 0;
+    cudaGetDevice(&d);
+    if (need <= bytes && d == device) return SS_OK;
+    if (host) cudaFreeHost(host);
+    if (dev) cudaFree(dev);
+    host = nullptr;
+    dev = nullptr;
+    bytes = 0;
+    const size_t want = std::max<size_t>(need, 64 * 1024);
+    SS_CUDA_TRY(cudaMallocHost(&host, want));
+    SS_CUDA_TRY(cudaMalloc(&dev, want));
+    bytes = want;
+    device = d;
+    return SS_OK;
+  }
+};
+static thread_local HostStaging g_stage;
+
+extern "C" int ss_gittins_min_host(const double* support, const double* masses, int64_t n,
+                                   double* out, void* stream) {
+  if (n < 0 || !out || (n > 0 && (!support || !masses)))
+    return set_error(SS_ERR_ARG, "gittins_min_host: bad args");
+  if (n == 0) {
+    *out = INFINITY;  // min over no support point
+    return SS_OK;
+  }
+  // staging: [npts i64][result f64][err i32 + pad][support n][masses n]
+  const size_t hdr = 32, need = hdr + (size_t)n * 16;
+  if (int rc = g_stage.reserve(need)) return rc;
+  char* h = g_stage.host;
+  *reinterpret_cast<int64_t*>(h) = n;
+  *reinterpret_cast<double*>(h + 8) = 0.0;
+  *reinterpret_cast<int*>(h + 16) = 0;
+  memcpy(h + hdr, support, (size_t)n * 8);
+  memcpy(h + hdr + (size_t)n * 8, masses, (size_t)n * 8);
+  cudaStream_t st = (cudaStream_t)stream;
+  char* d = g_stage.dev;
+  SS_CUDA_TRY(cudaMemcpyAsync(d, h, need, cudaMemcpyHostToDevice, st));
+  if (int rc = launch_gittins_dist(reinterpret_cast<const double*>(d + hdr),
+                                   reinterpret_cast<const double*>(d + hdr + (size_t)n * 8),
+                                   reinterpret_cast<const int64_t*>(d), nullptr, nullptr, 1, n,
+                                   reinterpret_cast<double*>(d + 8), reinterpret_cast<int*>(d + 16),
+                                   1, st))
+    return rc;
+  SS_CUDA_TRY(cudaMemcpyAsync(h + 8, d + 8, 12, cudaMemcpyDeviceToHost, st));
+  SS_CUDA_TRY(cudaStreamSynchronize(st));
+  if (*reinterpret_cast<int*>(h + 16) == SS_ERR_ZERODIV)
+    return set_error(SS_ERR_ZERODIV, "float division by zero");
+  *out = *reinterpret_cast<double*>(h + 8);
+  return SS_OK;
+}
+
+extern "C" int ss_cost_distribution_host(int32_t kind, double w_in, double w_out, double input_len,
+                                         const double* len_support, int64_t n, double* out_support,
+                                         void* stream) {
+  if (kind < 0 || kind > 2) return set_error(SS_ERR_ARG, "unknown cost model kind %d", kind);
+  if (kind == SS_COST_WEIGHTED_SUM && (w_in <= 0 || w_out <= 0))
+    return set_error(SS_ERR_ARG, "weighted-sum weights must be positive");
+  if (n < 0 || (n > 0 && (!len_support || !out_support)))
+    return set_error(SS_ERR_ARG, "cost_distribution_host: bad args");
+  if (n == 0) return SS_OK;
+  // staging: [npts i64][I f64][support n][out n]
+  const size_t hdr = 16, need = hdr + (size_t)n * 16;
+  if (int rc = g_stage.reserve(need)) return rc;
+  char* h = g_stage.host;
+  *reinterpret_cast<int64_t*>(h) = n;
+  *reinterpret_cast<double*>(h + 8) = input_len;
+  memcpy(h + hdr, len_support, (size_t)n * 8);
+  cudaStream_t st = (cudaStream_t)stream;
+  char* d = g_stage.dev;
+  SS_CUDA_TRY(cudaMemcpyAsync(d, h, hdr + (size_t)n * 8, cudaMemcpyHostToDevice, st));
+  if (int rc = launch_cost_dist(kind, w_in, w_out, reinterpret_cast<const double*>(d + 8),
+                                reinterpret_cast<const double*>(d + hdr),
+                                reinterpret_cast<const int64_t*>(d), 1, n,
+                                reinterpret_cast<double*>(d + hdr + (size_t)n * 8), st))
+    return rc;
+  SS_CUDA_TRY(cudaMemcpyAsync(h + hdr + (size_t)n * 8, d + hdr + (size_t)n * 8, (size_t)n * 8,
+                              cudaMemcpyDeviceToHost, st));
+  SS_CUDA_TRY(cudaStreamSynchronize(st));
+  memcpy(out_support, h + hdr + (size_t)n * 8, (size_t)n * 8);
+  return SS_OK;
 }
 
 // ---------------------------------------------------------------- bank ----

@@ -11,6 +11,7 @@ length (exact at width 1).
 
 from __future__ import annotations
 
+import weakref
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -61,6 +62,21 @@ def _embedding(req: Request, dim: int):
     return req.embedding, req.inv_norm
 
 
+_SCHEDULERS: "weakref.WeakKeyDictionary[HistoryWindow, dict]" = weakref.WeakKeyDictionary()
+
+
+def _scheduler(window: HistoryWindow, kind: SemanticHistory) -> SageScheduler:
+    """One SageScheduler (and its buffers) per (window, predictor config),
+    reused across predict calls."""
+    per = _SCHEDULERS.setdefault(window, {})
+    s = per.get(kind)
+    if s is None:
+        s = per[kind] = SageScheduler(window, RoundConfig(k=kind.k, theta=kind.theta,
+                                                          min_matches=kind.min_matches,
+                                                          max_len=kind.max_len, nbins=kind.nbins))
+    return s
+
+
 def predict(kind: SemanticHistory, request: Request, window: HistoryWindow,
             fallback: DiscreteDistribution | None = None) -> DiscreteDistribution:
     """Output-length law of one request.
@@ -76,9 +92,7 @@ def predict(kind: SemanticHistory, request: Request, window: HistoryWindow,
             raise _lib.ColdStartError("cold start: empty window and no fallback; warm-start the window")
         return fallback
     e, inv = _embedding(request, window.dim)
-    sched = SageScheduler(window, RoundConfig(k=kind.k, theta=kind.theta,
-                                              min_matches=kind.min_matches,
-                                              max_len=kind.max_len, nbins=kind.nbins))
+    sched = _scheduler(window, kind)
     st = sched.predict(e.reshape(1, -1), inv.reshape(1), torch.tensor([request.input_len]))
     if bool(st.used_fb[0].item()) and fallback is not None:
         return fallback
