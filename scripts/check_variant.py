@@ -1,0 +1,57 @@
+"""Bit-compare an experiment build's stage-1 partial lists with the default
+build's on the c2 shape (and a ragged one): each process dumps sorted lists.
+
+    python scripts/check_variant.py build_exp/NAME/libsagesched.so
+"""
+import ctypes as C
+import os
+import subprocess
+import sys
+
+import numpy as np
+
+
+def dump(lib, out, nq, rows, theta):
+    import torch
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from paper_2603_07917_b200 import _lib
+    from paper_2603_07917_b200.history import HistoryWindow
+    from paper_2603_07917_b200.synthetic import make_bank_device, make_queries
+    _lib.load(lib or None)
+    emb, lens, _ = make_bank_device(rows, 384, 4096, 0)
+    w = HistoryWindow(rows, 384)
+    w.push(emb, lens)
+    q, qi, _, _ = make_queries(nq, 384, 4096, 0, 1000)
+    dq, dqi = torch.as_tensor(q, device="cuda"), torch.as_tensor(qi, device="cuda")
+    part = torch.zeros(1024 * nq * 64, dtype=torch.int64, device="cuda")
+    ns = C.c_int32()
+    res = []
+    for rep in range(3):
+        part.zero_()
+        _lib.call("ss_topk_partials", w.handle, dq.data_ptr(), dqi.data_ptr(), nq, 64,
+                  float(np.float32(theta)), _lib.ALGO["tcgen05"], part.data_ptr(), 1024,
+                  C.byref(ns), _lib.stream_ptr())
+        torch.cuda.synchronize()
+        p = part[: ns.value * nq * 64].view(ns.value, nq, 64).cpu().numpy().view(np.uint64)
+        res.append(np.sort(p, axis=2))
+    np.save(out, np.stack(res))
+
+
+if __name__ == "__main__":
+    if sys.argv[1] == "--dump":
+        dump(sys.argv[2], sys.argv[3], int(sys.argv[4]), int(sys.argv[5]), float(sys.argv[6]))
+        sys.exit(0)
+    lib = sys.argv[1]
+    ok = True
+    for nq, rows, theta in ((1024, 1 << 20, 0.8), (1024, 1 << 20, -1.0), (333, 200_003, 0.8), (2048, 1 << 20, 0.5)):
+        outs = []
+        for tag, l in (("ref", ""), ("exp", lib)):
+            f = f"/tmp/cv_{tag}.npy"
+            subprocess.run([sys.executable, __file__, "--dump", l, f, str(nq), str(rows), str(theta)], check=True)
+            outs.append(np.load(f))
+        a, b = outs
+        same = a.shape == b.shape and all(np.array_equal(a[0], b[i]) for i in range(3))
+        print(f"nq={nq} rows={rows} theta={theta}: {'IDENTICAL' if same else 'DIFFERENT'} "
+              f"(slices {a.shape[1]} vs {b.shape[1]})", flush=True)
+        ok &= same
+    sys.exit(0 if ok else 1)
