@@ -2,21 +2,24 @@
 //
 // Same math and parity contract as k_topk_sm100.cu (tcgen05.mma kind::i8,
 // exact int32 dots, fused per-query top-k), restructured so the epilogue is
-// two warps per SM sub-partition and overlaps the MMA:
+// three warps per SM sub-partition and overlaps the MMA:
 //   * A (128 queries x dim int8) is written once into TMEM columns
 //     [A_COL, A_COL + dim/4) by the epilogue warps (tcgen05.st); the MMA
 //     reads it there ("TS" form), so no shared memory holds A;
-//   * 8 epilogue warps, two per TMEM lane quarter, split every tile's 256
-//     columns in halves; the two warps serving a query share its heap under
-//     a per-query shared-memory lock (inserts are rare), so one heap set and
-//     four 32 KB bank stages fit;
-//   * two accumulators of BN columns (BN = 208 beside dim 384, 192 beside
-//     dim 512: the widest double buffer that fits next to A in 512 TMEM
-//     columns): each epilogue warp pulls its BN/2 columns into registers,
-//     releases the accumulator at once, and filters from registers while the
-//     MMA of the next tile runs.
-// Warps: 0 TMA producer (bank tiles), 1 TMEM allocator + MMA issuer,
-// 2..9 epilogue (group g = (warp-2)/4 owns columns [g*BN/2, (g+1)*BN/2)).
+//   * two accumulators of BN = 192 columns (2 x 192 + 96 = 480 TMEM columns
+//     at dim 384; 2 x 192 + 128 = 512 at dim 512): each epilogue warp pulls
+//     its 64 columns into registers, releases the accumulator at once, and
+//     filters from registers while the MMA of the next tile runs;
+//   * 12 epilogue warps, three per TMEM lane quarter, split every tile's 192
+//     columns in thirds; the three warps serving a query share its heap under
+//     a per-query shared-memory lock (inserts are rare).  Three warps per
+//     sub-partition (instead of two with 104 columns each) hide the filter's
+//     latency chains; 64 data registers per thread keep the kernel at
+//     <= 128 registers for 448 threads;
+//   * bank tiles come through a two-tile ring (RING, below) so the MMA issuer
+//     waits once per tile.
+// Warps: 0 TMA producer (bank tiles + inverse norms), 1 TMEM allocator + MMA
+// issuer, 2..13 epilogue (group g = (warp-2)/4 owns columns [64g, 64g + 64)).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <stdlib.h>
@@ -32,9 +35,11 @@ namespace ss {
 namespace ts {
 
 constexpr int BM = 128;          // queries (TMEM lanes)
+constexpr int BN = 192;          // bank rows per tile (UMMA N): 2 x 192 accumulator columns + A's dim / 4 <= 512
 constexpr int BK = 128;          // bytes per K-block (128B swizzle atom)
 constexpr int UK = 32;           // int8 K per MMA
-constexpr int EPI_WARPS = 8;
+constexpr int EPW = 3;                // epilogue warps per TMEM lane quarter
+constexpr int EPI_WARPS = 4 * EPW;    // 12
 constexpr int THREADS = 64 + EPI_WARPS * 32;
 constexpr int KMAX = 64;
 constexpr int ISLOTS = 4;  // inverse-norm ring (tiles)
@@ -255,7 +260,19 @@ __device__ __noinline__ float insert_locked(uint32_t mask, const float* sl, floa
 constexpr int SHARE_EVERY = 2;
 constexpr int NACC = 2;  // accumulators: the MMA of tile t+1 runs while tile t drains
 
-template <int BN, bool SHARE>
+// RING selects the bank-tile pipeline:
+//   RING = true (tile ring, the default where it fits in shared memory): two
+//     whole-tile stages; the MMA issuer waits ONCE per tile, on a barrier
+//     that completes when the tile's K-blocks have landed AND the epilogue has
+//     released the accumulator the tile will overwrite (the epilogue warps
+//     arrive on it).  Issuing one tcgen05.mma takes the issuing thread about
+//     as long as the MMA runs, so every barrier wait between MMAs is a bubble
+//     in the tensor pipe (profiles/r2c_ts_ablation.md): per-K-block waits cost
+//     ~30% of the kernel.  The producer still refills each K-block part as
+//     soon as the MMAs that read it retire (per-part empty barriers).
+//   RING = false: a ring of `stages` K-block stages, waited per K-block (for
+//     shapes whose two tiles do not fit, e.g. dim 512).
+template <int BN, bool SHARE, bool RING>
 __global__ void __launch_bounds__(THREADS, 1)
 k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
           const float* __restrict__ q_inv, int64_t nq, const float* __restrict__ inv, int64_t n_rows,
@@ -264,35 +281,37 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
           uint32_t* __restrict__ gslots, int rshare) {
   constexpr int A_COL = NACC * BN;
   constexpr int B_STAGE = BN * BK;
-  constexpr int HALF = BN / 2;     // columns per epilogue warp per tile
-  constexpr int CPW = HALF / 32;   // full 32-column chunks per epilogue warp per tile
-  constexpr int TAIL = HALF % 32;  // + one 8-column chunk (BN = 208)
-  static_assert(CPW == 3 && (TAIL == 0 || TAIL == 8), "tile shape");
+  constexpr int IS = ISLOTS;       // inverse-norm ring slots
+  constexpr int CW = BN / EPW;     // columns per epilogue warp per tile
+  static_assert(CW == 64, "tile shape: two 32-column chunks per epilogue warp");
   constexpr uint32_t IDESC = idesc(BN);
+  const int nkb = dim / BK;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sB = smem;                                                    // stages x BN x 128 B
-  uint64_t* s_heap = reinterpret_cast<uint64_t*>(sB + stages * B_STAGE);  // [k][128]
+  uint64_t* s_heap = reinterpret_cast<uint64_t*>(sB + (RING ? NACC * nkb : stages) * B_STAGE);  // [k][128]
   uint64_t* s_hroot = s_heap + (size_t)k * BM;                           // [128]
   int* s_hcnt = reinterpret_cast<int*>(s_hroot + BM);                    // [128]
   int* s_hlock = s_hcnt + BM;                                            // [128]
   float* s_inv = reinterpret_cast<float*>(s_hlock + BM);                 // [ISLOTS][256]
-  float* s_ib = s_inv + ISLOTS * 256;                                    // [8 warps][16]
+  float* s_ib = s_inv + IS * 256;                                        // [8 warps][16]
   uint64_t* bars = reinterpret_cast<uint64_t*>(s_ib + EPI_WARPS * 16);
+  // barriers: RING -- full[2] (a tile's parts landed + its accumulator
+  // released), empty[2 * nkb] (one per K-block part); else full/empty[stages]
+  const int nfull = RING ? NACC : stages, nempty = RING ? NACC * nkb : stages;
   uint64_t* a_full = bars;
   uint64_t* full = bars + 1;
-  uint64_t* empty = full + stages;
-  uint64_t* tfull = empty + stages;
-  uint64_t* tempty = tfull + NACC;
-  uint64_t* ifull = tempty + NACC;   // [ISLOTS] tile's inverse norms landed
-  uint64_t* iempty = ifull + ISLOTS; // [ISLOTS] consumed by every epilogue warp
-  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(iempty + ISLOTS);
+  uint64_t* empty = full + nfull;
+  uint64_t* tfull = empty + nempty;
+  uint64_t* tempty = tfull + NACC;   // (RING: unused -- the release goes to full)
+  uint64_t* ifull = tempty + NACC;   // [IS] tile's inverse norms landed
+  uint64_t* iempty = ifull + IS;     // [IS] consumed by every epilogue warp
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(iempty + IS);
   // SHARE: this slice's top-R keys per query, after everything else
   uint32_t* s_rtop = s_tmem + 4;  // [128][4]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int qt = blockIdx.x, slice = blockIdx.y;
-  const int nkb = dim / BK;
   const int64_t tile0 = (int64_t)slice * tiles_per_slice;
   const int64_t total_tiles = (n_rows + BN - 1) / BN;
   const int ntiles = (int)max((int64_t)0, min(total_tiles, tile0 + tiles_per_slice) - tile0);
@@ -300,9 +319,11 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
   if (threadIdx.x == 0) {
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmB) : "memory");
     bar_init(a_full, 4);  // the 4 warps writing A into TMEM
-    for (int s = 0; s < stages; ++s) { bar_init(&full[s], 1); bar_init(&empty[s], 1); }
+    // RING: the producer's expect_tx arrival + every epilogue warp's release
+    for (int s = 0; s < nfull; ++s) bar_init(&full[s], RING ? 1 + EPI_WARPS : 1);
+    for (int s = 0; s < nempty; ++s) bar_init(&empty[s], 1);
     for (int b = 0; b < NACC; ++b) { bar_init(&tfull[b], 1); bar_init(&tempty[b], EPI_WARPS); }
-    for (int b = 0; b < ISLOTS; ++b) { bar_init(&ifull[b], 1); bar_init(&iempty[b], EPI_WARPS); }
+    for (int b = 0; b < IS; ++b) { bar_init(&ifull[b], 1); bar_init(&iempty[b], EPI_WARPS); }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   for (int i = threadIdx.x; i < BM; i += blockDim.x) { s_hcnt[i] = 0; s_hroot[i] = 0; s_hlock[i] = 0; }
@@ -326,18 +347,40 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
         // the tile's BN inverse norms into the ring (the bank pads inv with
         // one NaN tile, so the copy never leaves the allocation); the
         // epilogue then issues no global loads in its tile loop
-        const int sl = t % ISLOTS;
-        bar_wait(&iempty[sl], ((t / ISLOTS) & 1) ^ 1);
-        bar_expect(&ifull[sl], BN * 4);
-        bulk_g2s(s_inv + sl * 256, inv + row0, BN * 4, &ifull[sl]);
-        for (int kb = 0; kb < nkb; ++kb, ++it) {
-          const int s = it % stages;
-          bar_wait(&empty[s], ((it / stages) & 1) ^ 1);
-          bar_expect(&full[s], B_STAGE);
-          tma2d(sB + s * B_STAGE, &tmB, &full[s], kb * BK, row0);
+        const int sl = t % IS;
+        if constexpr (!RING) {
+          bar_wait(&iempty[sl], ((t / IS) & 1) ^ 1);
+          bar_expect(&ifull[sl], BN * 4);
+          bulk_g2s(s_inv + sl * 256, inv + row0, BN * 4, &ifull[sl]);
+        }
+        if constexpr (RING) {
+          // part kb of stage t & 1 is free once tile t - 2's K-block kb MMAs
+          // retired; the tile's one expect_tx arrival follows the first such
+          // wait (so it cannot land in the previous phase of full)
+          const int st = t & 1;
+          const uint32_t par = ((t >> 1) & 1) ^ 1;
+          for (int kb = 0; kb < nkb; ++kb) {
+            bar_wait(&empty[st * nkb + kb], par);
+            if (kb == 0) bar_expect(&full[st], (uint32_t)(nkb * B_STAGE));
+            tma2d(sB + (st * nkb + kb) * B_STAGE, &tmB, &full[st], kb * BK, row0);
+          }
+          // the norms after the tile's bank parts: with two slots, the slot
+          // frees only when the epilogue is done with tile t - 2, which must
+          // not hold back the bank loads
+          bar_wait(&iempty[sl], ((t / IS) & 1) ^ 1);
+          bar_expect(&ifull[sl], BN * 4);
+          bulk_g2s(s_inv + sl * 256, inv + row0, BN * 4, &ifull[sl]);
+        } else {
+          for (int kb = 0; kb < nkb; ++kb, ++it) {
+            const int s = it % stages;
+            bar_wait(&empty[s], ((it / stages) & 1) ^ 1);
+            bar_expect(&full[s], B_STAGE);
+            tma2d(sB + s * B_STAGE, &tmB, &full[s], kb * BK, row0);
+          }
         }
       }
-      for (int i = max(0, it - stages); i < it; ++i) bar_wait(&empty[i % stages], (i / stages) & 1);
+      if constexpr (!RING)
+        for (int i = max(0, it - stages); i < it; ++i) bar_wait(&empty[i % stages], (i / stages) & 1);
     }
   } else if (warp == 1) {
     // ------------------------------------------------------- MMA issuer ----
@@ -348,19 +391,33 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
       int it = 0;
       for (int t = 0; t < ntiles; ++t) {
         const int acc = t % NACC;
-        // every epilogue warp has pulled tile t - NACC out of this accumulator
-        bar_wait(&tempty[acc], ((t / NACC) & 1) ^ 1);
-        fence_after();
         const uint32_t dacc = tmem + acc * BN;
-        for (int kb = 0; kb < nkb; ++kb, ++it) {
-          const int s = it % stages;
-          bar_wait(&full[s], (it / stages) & 1);
+        if constexpr (RING) {
+          // one wait per tile: its parts landed and accumulator acc released
+          bar_wait_spin(&full[acc], (t >> 1) & 1);
           fence_after();
+          for (int kb = 0; kb < nkb; ++kb) {
+            const uint32_t bst = b_base + (acc * nkb + kb) * B_STAGE;
 #pragma unroll
-          for (int kk = 0; kk < BK / UK; ++kk)
-            mma_ts(dacc, tmem + A_COL + (kb * (BK / UK) + kk) * (UK / 4),
-                   desc_sw128(b_base + s * B_STAGE + kk * UK), IDESC, (kb | kk) != 0);
-          commit(&empty[s]);
+            for (int kk = 0; kk < BK / UK; ++kk)
+              mma_ts(dacc, tmem + A_COL + (kb * (BK / UK) + kk) * (UK / 4), desc_sw128(bst + kk * UK),
+                     IDESC, (kb | kk) != 0);
+            commit(&empty[acc * nkb + kb]);
+          }
+        } else {
+          // every epilogue warp has pulled tile t - NACC out of this accumulator
+          bar_wait(&tempty[acc], ((t / NACC) & 1) ^ 1);
+          fence_after();
+          for (int kb = 0; kb < nkb; ++kb, ++it) {
+            const int s = it % stages;
+            bar_wait(&full[s], (it / stages) & 1);
+            fence_after();
+#pragma unroll
+            for (int kk = 0; kk < BK / UK; ++kk)
+              mma_ts(dacc, tmem + A_COL + (kb * (BK / UK) + kk) * (UK / 4),
+                     desc_sw128(b_base + s * B_STAGE + kk * UK), IDESC, (kb | kk) != 0);
+            commit(&empty[s]);
+          }
         }
         commit(&tfull[acc]);
       }
@@ -368,7 +425,7 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
   } else {
     // --------------------------------------------------------- epilogue ----
     const int ew = warp - 2;                // 0..7
-    const int grp = ew >> 2;                // column half of each tile
+    const int grp = ew >> 2;                // column third of each tile
     const int quarter = warp & 3;           // TMEM lane quarter
     const int qrow = quarter * 32 + lane;
     const int64_t q = (int64_t)qt * BM + qrow;
@@ -391,14 +448,18 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
       __syncwarp();
       if (lane == 0) bar_arrive(a_full);
     }
+    if constexpr (RING) {
+      // both accumulators start free: release them for tiles 0 and 1
+      if (lane == 0) { bar_arrive(&full[0]); bar_arrive(&full[1]); }
+    }
     const float iq = (q < nq) ? q_inv[q] : __int_as_float(0x7fc00000);
     uint64_t* heap = s_heap + qrow;  // shared by the two column-half warps of this quarter
     float* cib = s_ib + ew * 16;  // [max inv_w of half 0..7][min inv_w of half 0..7]
     float thr = (iq == iq) ? s_threshold(theta, iq) : INFINITY;
     for (int t = 0; t < ntiles; ++t) {
-      const int64_t row0 = (tile0 + t) * BN + grp * HALF;  // first bank row of my columns
-      const int acc = t % NACC, sl = t % ISLOTS;
-      const float* ciw = s_inv + sl * 256 + grp * HALF;
+      const int64_t row0 = (tile0 + t) * BN + grp * CW;  // first bank row of my columns
+      const int acc = t % NACC, sl = t % IS;
+      const float* ciw = s_inv + sl * 256 + grp * CW;
       if constexpr (SHARE) {
         // minimum over the slices' published R-th best keys (independent
         // loads; their latency overlaps the wait for this tile's MMA), every
@@ -410,12 +471,12 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
           if (m != 0u && m != ~0u) thr = fmaxf(thr, s_threshold(f32_unorder(m), iq));
         }
       }
-      bar_wait_epi(&ifull[sl], (t / ISLOTS) & 1);
+      bar_wait_epi(&ifull[sl], (t / IS) & 1);
       {
         // NaN (zero row / past the end) never passes the exact test: leave it
         // out of the bounds
         const float NaNf = __int_as_float(0x7fc00000);  // ignored by fmaxf / fminf
-        const float4 w4 = (lane * 4 < HALF) ? reinterpret_cast<const float4*>(ciw)[lane]
+        const float4 w4 = (lane * 4 < CW) ? reinterpret_cast<const float4*>(ciw)[lane]
                                             : make_float4(NaNf, NaNf, NaNf, NaNf);
         float hi = fmaxf(fmaxf(fmaxf(w4.x, w4.y), fmaxf(w4.z, w4.w)), 0.f);
         float lo = fminf(fminf(fminf(w4.x, w4.y), fminf(w4.z, w4.w)), INFINITY);
@@ -424,7 +485,7 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
           hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
           lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
         }
-        if ((lane & 3) == 0 && lane * 4 < HALF) {
+        if ((lane & 3) == 0 && lane * 4 < CW) {
           cib[lane >> 2] = hi;
           cib[8 + (lane >> 2)] = lo;
         }
@@ -432,20 +493,22 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
       __syncwarp();
       bar_wait_epi(&tfull[acc], (t / NACC) & 1);
       fence_after();
-      const uint32_t tbase = tmem + lane_base + acc * BN + grp * HALF;
+      const uint32_t tbase = tmem + lane_base + acc * BN + grp * CW;
       // pull my chunks into registers, then hand the accumulator back
-      int v0[32], v1[32], v2[32], vt[TAIL ? TAIL : 1];
+      int v0[32], v1[32];
       ld32_async(tbase, v0);
       ld32_async(tbase + 32, v1);
-      ld32_async(tbase + 64, v2);
-      if constexpr (TAIL == 8) ld8_async(tbase + 96, vt);
       wait_ld(v0);
       wait_ld(v1);
-      wait_ld(v2);
-      if constexpr (TAIL == 8) wait_ld8(vt);
       fence_before();
       __syncwarp();
-      if (lane == 0) bar_arrive(&tempty[acc]);
+      if (lane == 0) bar_arrive(RING ? &full[acc] : &tempty[acc]);  // accumulator free for tile t + 2
+#ifdef SS_ABLATE_FILTER  // scripts/exp_build.sh ablation: pull + release only, no filter
+      if (v0[0] == 0x7fffffff && v1[5] == 0x7fffffff) thr = -thr;
+      __syncwarp();
+      if (lane == 0) bar_arrive(&iempty[sl]);
+      continue;
+#endif
       // Filter per 16-column half: a half can only hold a score >= thr if
       // fl(fl(max dot) * (max inv_w)) >= thr (or the min inv_w when every dot
       // is negative) -- monotone rounding makes this a superset test, so the
@@ -508,43 +571,32 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
         }
       };
       auto chunk = [&](const auto& v, const int c) {
-        constexpr int W = sizeof(v) / sizeof(v[0]);  // 32, or 8 for the N=208 tail
-        if constexpr (W == 32) {
-          const int a0 = __vimax3_s32(v[0], v[1], v[2]), a1 = __vimax3_s32(v[3], v[4], v[5]);
-          const int a2 = __vimax3_s32(v[6], v[7], v[8]), a3 = __vimax3_s32(v[9], v[10], v[11]);
-          const int a4 = __vimax3_s32(v[12], v[13], v[14]);
-          const int b0 = __vimax3_s32(v[16], v[17], v[18]), b1 = __vimax3_s32(v[19], v[20], v[21]);
-          const int b2 = __vimax3_s32(v[22], v[23], v[24]), b3 = __vimax3_s32(v[25], v[26], v[27]);
-          const int b4 = __vimax3_s32(v[28], v[29], v[30]);
-          const int mdl = __vimax3_s32(__vimax3_s32(a0, a1, a2), __vimax3_s32(a3, a4, v[15]), a0);
-          const int mdh = __vimax3_s32(__vimax3_s32(b0, b1, b2), __vimax3_s32(b3, b4, v[31]), b0);
-          const float bl = __fmul_rn(__int2float_rn(mdl), mdl >= 0 ? cib[2 * c] : cib[8 + 2 * c]);
-          const float bh =
-              __fmul_rn(__int2float_rn(mdh), mdh >= 0 ? cib[2 * c + 1] : cib[8 + 2 * c + 1]);
-          if constexpr (SHARE) {
-            // pure top-k: many chunks pass while the bounds rise -- one exact
-            // pass (and one heap lock) per 32 columns is cheaper there
-            if (fmaxf(bl, bh) >= thr)
-              exact(v, c, std::integral_constant<int, 0>(), std::integral_constant<int, 32>());
-          } else {
-            if (bl >= thr) exact(v, c, std::integral_constant<int, 0>(), std::integral_constant<int, 16>());
-            if (bh >= thr) exact(v, c, std::integral_constant<int, 16>(), std::integral_constant<int, 16>());
-          }
-        } else {  // the tail chunk: 8 columns (BN = 208)
-          const int md = __vimax3_s32(__vimax3_s32(v[0], v[1], v[2]), __vimax3_s32(v[3], v[4], v[5]),
-                                      max(v[6], v[7]));
-          const float bnd = __fmul_rn(__int2float_rn(md), md >= 0 ? cib[2 * c] : cib[8 + 2 * c]);
-          if (bnd >= thr) exact(v, c, std::integral_constant<int, 0>(), std::integral_constant<int, W>());
+        const int a0 = __vimax3_s32(v[0], v[1], v[2]), a1 = __vimax3_s32(v[3], v[4], v[5]);
+        const int a2 = __vimax3_s32(v[6], v[7], v[8]), a3 = __vimax3_s32(v[9], v[10], v[11]);
+        const int a4 = __vimax3_s32(v[12], v[13], v[14]);
+        const int b0 = __vimax3_s32(v[16], v[17], v[18]), b1 = __vimax3_s32(v[19], v[20], v[21]);
+        const int b2 = __vimax3_s32(v[22], v[23], v[24]), b3 = __vimax3_s32(v[25], v[26], v[27]);
+        const int b4 = __vimax3_s32(v[28], v[29], v[30]);
+        const int mdl = __vimax3_s32(__vimax3_s32(a0, a1, a2), __vimax3_s32(a3, a4, v[15]), a0);
+        const int mdh = __vimax3_s32(__vimax3_s32(b0, b1, b2), __vimax3_s32(b3, b4, v[31]), b0);
+        const float bl = __fmul_rn(__int2float_rn(mdl), mdl >= 0 ? cib[2 * c] : cib[8 + 2 * c]);
+        const float bh = __fmul_rn(__int2float_rn(mdh), mdh >= 0 ? cib[2 * c + 1] : cib[8 + 2 * c + 1]);
+        if constexpr (SHARE) {
+          // pure top-k: many chunks pass while the bounds rise -- one exact
+          // pass (and one heap lock) per 32 columns is cheaper there
+          if (fmaxf(bl, bh) >= thr)
+            exact(v, c, std::integral_constant<int, 0>(), std::integral_constant<int, 32>());
+        } else {
+          if (bl >= thr) exact(v, c, std::integral_constant<int, 0>(), std::integral_constant<int, 16>());
+          if (bh >= thr) exact(v, c, std::integral_constant<int, 16>(), std::integral_constant<int, 16>());
         }
       };
       chunk(v0, 0);
       chunk(v1, 1);
-      chunk(v2, 2);
-      if constexpr (TAIL != 0) chunk(vt, 3);
       __syncwarp();
       if (lane == 0) bar_arrive(&iempty[sl]);  // this tile's inverse norms consumed
     }
-    asm volatile("bar.sync 1, %0;\n" ::"n"(EPI_WARPS * 32) : "memory");  // both halves done
+    asm volatile("bar.sync 1, %0;\n" ::"n"(EPI_WARPS * 32) : "memory");  // every column third done
     if (grp == 0 && q < nq) {
       uint64_t* out = partials + ((int64_t)slice * nq + q) * k;
       const int hc = s_hcnt[qrow];
@@ -573,45 +625,63 @@ static PFN_cuTensorMapEncodeTiled_v12000 ts_encode() {
   return fn;
 }
 
-static size_t ts_fixed_smem(int k) {
-  return (size_t)k * ts::BM * 8 + ts::BM * 16 + ts::ISLOTS * 256 * 4 + ts::EPI_WARPS * 16 * 4 + 512 +
+static size_t ts_fixed_smem(int k, int islots) {
+  return (size_t)k * ts::BM * 8 + ts::BM * 16 + (size_t)islots * 256 * 4 + ts::EPI_WARPS * 16 * 4 + 512 +
          1024;
 }
 
-// Tile rows: the widest double buffer of accumulators that fits beside A
-// (dim / 4 TMEM columns): 2 x 208 + 96 = 512 at dim 384 (and below), 2 x 192
-// + 128 = 512 at dim 512.
-static int ts_bn(int dim) { return dim / 4 + 2 * 208 <= 512 ? 208 : 192; }
-
-static int ts_stages(int k, int bn) {
-  for (int s = 8; s >= 3; --s)
-    if (ts_fixed_smem(k) + ts::BM * 16 + (size_t)s * bn * ts::BK <= 227 * 1024) return s;
-  return 0;
+// Shape of one launch: tile rows BN (the widest double buffer of accumulators
+// that fits beside A's dim / 4 TMEM columns: 2 x 208 + 96 = 512 at dim 384
+// and below, 2 x 192 + 128 at dim 512), and the pipeline: the tile ring (two
+// whole tiles, see k_topk_ts) when it fits in shared memory, else a ring of
+// K-block stages.  Pure top-k (SHARE) needs 2 KB more for the shared bounds.
+struct TsShape {
+  int bn = 0;
+  bool ring = false;
+  int stages = 0;
+  size_t smem = 0;
+};
+static TsShape ts_shape(int dim, int k, bool share) {
+  const int nkb = dim / ts::BK;
+  const size_t extra = share ? ts::BM * 16 : 0;
+  TsShape sh;
+  if (dim / 4 + 2 * ts::BN > 512) return sh;
+  sh.bn = ts::BN;
+  const size_t fixed = ts_fixed_smem(k, ts::ISLOTS) + extra;
+  const size_t ring = fixed + (size_t)2 * nkb * ts::BN * ts::BK;
+  if (ring <= 227 * 1024) {
+    sh.ring = true; sh.stages = 2 * nkb; sh.smem = ring;
+    return sh;
+  }
+  for (int s = 8; s >= 3; --s) {
+    const size_t smem = fixed + (size_t)s * ts::BN * ts::BK;
+    if (smem <= 227 * 1024) {
+      sh.stages = s; sh.smem = smem;
+      return sh;
+    }
+  }
+  sh.bn = 0;
+  return sh;
 }
 
 bool topk_ts_supported(const TopkArgs& a) {
-  const int bn = ts_bn(a.dim);
-  if (a.dim % ts::BK || a.dim / 4 + 2 * bn > 512 || a.k < 1 || a.k > ts::KMAX) return false;
+  if (a.dim % ts::BK || a.dim < ts::BK || a.k < 1 || a.k > ts::KMAX) return false;
   if (a.n_rows >= (1LL << 31) || a.nq >= (1LL << 31)) return false;
   if (!a.inv_padded) return false;  // tiles of inverse norms are bulk-copied whole
-  return ts_stages(a.k, bn) >= 3;
+  return ts_shape(a.dim, a.k, true).bn > 0 && ts_shape(a.dim, a.k, false).bn > 0;
 }
 
 // one partial list per CTA slice
 int topk_ts_lists(const TopkArgs& a, int device) {
   const int64_t qtiles = (a.nq + ts::BM - 1) / ts::BM;
-  const int64_t tiles = (a.n_rows + ts_bn(a.dim) - 1) / ts_bn(a.dim);
+  const int bn = ts_shape(a.dim, a.k, false).bn;
+  const int64_t tiles = (a.n_rows + bn - 1) / bn;
   return pick_slices(qtiles, tiles, sm_count(device));
 }
 
 template <int BN>
-static int launch_ts_t(const TopkArgs& a, uint64_t* partials, int n_slices, cudaStream_t st) {
-  // pure top-k: share per-slice bounds (see k_topk_ts SHARE)
-  int rshare = 0;
-  if (a.gslots && a.theta <= 0.f && n_slices >= 2 && n_slices <= kMaxShareSlices) {
-    const int R = (a.k + n_slices - 1) / n_slices;
-    if (R <= 4) rshare = R;
-  }
+static int launch_ts_t(const TopkArgs& a, const TsShape& sh, int rshare, uint64_t* partials, int n_slices,
+                       cudaStream_t st) {
   auto enc = ts_encode();
   if (!enc) return set_error(SS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   CUtensorMap mb;
@@ -623,27 +693,33 @@ static int launch_ts_t(const TopkArgs& a, uint64_t* partials, int n_slices, cuda
                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_error(SS_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
-  const int stages = ts_stages(a.k, BN);
-  const size_t smem = ts_fixed_smem(a.k) + (size_t)stages * BN * ts::BK + (rshare ? ts::BM * 16 : 0);
-  auto kern = rshare ? ts::k_topk_ts<BN, true> : ts::k_topk_ts<BN, false>;
-  SS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  auto kern = rshare ? (sh.ring ? ts::k_topk_ts<BN, true, true> : ts::k_topk_ts<BN, true, false>)
+                     : (sh.ring ? ts::k_topk_ts<BN, false, true> : ts::k_topk_ts<BN, false, false>);
+  SS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh.smem));
   if (rshare)
     SS_CUDA_TRY(cudaMemsetAsync(a.gslots, 0, (size_t)n_slices * a.nq * sizeof(uint32_t), st));
   const int64_t tiles = (a.n_rows + BN - 1) / BN;
   const int64_t tps = (tiles + n_slices - 1) / n_slices;
   dim3 grid((unsigned)((a.nq + ts::BM - 1) / ts::BM), (unsigned)n_slices);
   count_launch();
-  kern<<<grid, ts::THREADS, smem, st>>>(mb, a.q, a.q_inv, a.nq, a.inv, a.n_rows, a.dim, stages, a.k,
-                                        a.theta, a.head % a.gcap, a.gcap, a.slot_offset, tps,
-                                        partials, a.gslots, rshare);
+  kern<<<grid, ts::THREADS, sh.smem, st>>>(mb, a.q, a.q_inv, a.nq, a.inv, a.n_rows, a.dim, sh.stages, a.k,
+                                           a.theta, a.head % a.gcap, a.gcap, a.slot_offset, tps,
+                                           partials, a.gslots, rshare);
   SS_LAUNCH_CHECK();
   return SS_OK;
 }
 
 int launch_topk_ts(const TopkArgs& a, uint64_t* partials, int n_lists, cudaStream_t st) {
   if (n_lists < 1) return set_error(SS_ERR_ARG, "ts: no slices");
-  return ts_bn(a.dim) == 208 ? launch_ts_t<208>(a, partials, n_lists, st)
-                             : launch_ts_t<192>(a, partials, n_lists, st);
+  // pure top-k: share per-slice bounds (see k_topk_ts SHARE)
+  int rshare = 0;
+  if (a.gslots && a.theta <= 0.f && n_lists >= 2 && n_lists <= kMaxShareSlices) {
+    const int R = (a.k + n_lists - 1) / n_lists;
+    if (R <= 4) rshare = R;
+  }
+  const TsShape sh = ts_shape(a.dim, a.k, rshare > 0);
+  if (sh.bn == ts::BN) return launch_ts_t<ts::BN>(a, sh, rshare, partials, n_lists, st);
+  return set_error(SS_ERR_UNSUPPORTED, "ts: no shape fits shared memory");
 }
 
 }  // namespace ss
