@@ -258,6 +258,39 @@ __device__ __noinline__ float insert_locked(uint32_t mask, const float* sl, floa
 // that minimum, so it bounds the global k-th key from below.  Slots that are
 // still 0 make the minimum 0 (no bound).
 constexpr int SHARE_EVERY = 2;
+// Per-tile timeline of CTA (0, 0) for scripts/trace_ts.py, compiled only with
+// -DSS_TRACE (scripts/exp_build.sh): clock64 stamps per [event][tile].
+// Epilogue warp 2 (lane 0): 1 before the accumulator wait, 2 after it; the
+// last of the 12 epilogue warps: 3 after the release, 4 after the filter;
+// MMA issuer: 5 before the tile wait, 6 after it, 7 after the tile's
+// commits; producer: 8 first part issued.  g_wtrace[e][warp][tile]: events
+// 1..4 of every epilogue warp, and (e = 4) after its inverse-norm wait.
+// (Stamps closer than a few hundred cycles are dominated by the stores.)
+#ifdef SS_TRACE
+__device__ long long g_trace[9][512];
+__device__ long long g_wtrace[5][EPI_WARPS][512];
+#define TRACE(ev, t)                                                                               \
+  do {                                                                                             \
+    if (blockIdx.x == 0 && blockIdx.y == 0 && (t) < 512) {                                         \
+      if ((ev) <= 4) {                                                                             \
+        if ((threadIdx.x & 31) == 0) {                                                             \
+          const long long c_ = clock64();                                                          \
+          g_wtrace[(ev) == 0 ? 4 : (ev) - 1][(threadIdx.x >> 5) - 2][t] = c_;                      \
+          if ((ev) >= 3)                                                                           \
+            atomicMax(reinterpret_cast<unsigned long long*>(&g_trace[ev][t]), (unsigned long long)c_); \
+          else if (threadIdx.x == 64)                                                              \
+            g_trace[ev][t] = c_;                                                                   \
+        }                                                                                          \
+      } else {                                                                                     \
+        g_trace[ev][t] = clock64();                                                                \
+      }                                                                                            \
+    }                                                                                              \
+  } while (0)
+#else
+#define TRACE(ev, t) \
+  do {               \
+  } while (0)
+#endif
 constexpr int NACC = 2;  // accumulators: the MMA of tile t+1 runs while tile t drains
 
 // RING selects the bank-tile pipeline:
@@ -363,6 +396,7 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
             bar_wait(&empty[st * nkb + kb], par);
             if (kb == 0) bar_expect(&full[st], (uint32_t)(nkb * B_STAGE));
             tma2d(sB + (st * nkb + kb) * B_STAGE, &tmB, &full[st], kb * BK, row0);
+            if (kb == 0) TRACE(8, t);
           }
           // the norms after the tile's bank parts: with two slots, the slot
           // frees only when the epilogue is done with tile t - 2, which must
@@ -394,7 +428,9 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
         const uint32_t dacc = tmem + acc * BN;
         if constexpr (RING) {
           // one wait per tile: its parts landed and accumulator acc released
+          TRACE(5, t);
           bar_wait_spin(&full[acc], (t >> 1) & 1);
+          TRACE(6, t);
           fence_after();
           for (int kb = 0; kb < nkb; ++kb) {
             const uint32_t bst = b_base + (acc * nkb + kb) * B_STAGE;
@@ -420,6 +456,7 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
           }
         }
         commit(&tfull[acc]);
+        TRACE(7, t);
       }
     }
   } else {
@@ -472,6 +509,7 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
         }
       }
       bar_wait_epi(&ifull[sl], (t / IS) & 1);
+      TRACE(0, t);
       {
         // NaN (zero row / past the end) never passes the exact test: leave it
         // out of the bounds
@@ -491,7 +529,9 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
         }
       }
       __syncwarp();
+      TRACE(1, t);
       bar_wait_epi(&tfull[acc], (t / NACC) & 1);
+      TRACE(2, t);
       fence_after();
       const uint32_t tbase = tmem + lane_base + acc * BN + grp * CW;
       // pull my chunks into registers, then hand the accumulator back
@@ -503,6 +543,7 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
       fence_before();
       __syncwarp();
       if (lane == 0) bar_arrive(RING ? &full[acc] : &tempty[acc]);  // accumulator free for tile t + 2
+      TRACE(3, t);
 #ifdef SS_ABLATE_FILTER  // scripts/exp_build.sh ablation: pull + release only, no filter
       if (v0[0] == 0x7fffffff && v1[5] == 0x7fffffff) thr = -thr;
       __syncwarp();
@@ -595,6 +636,7 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
       chunk(v1, 1);
       __syncwarp();
       if (lane == 0) bar_arrive(&iempty[sl]);  // this tile's inverse norms consumed
+      TRACE(4, t);
     }
     asm volatile("bar.sync 1, %0;\n" ::"n"(EPI_WARPS * 32) : "memory");  // every column third done
     if (grp == 0 && q < nq) {
@@ -612,6 +654,16 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
 }
 
 }  // namespace ts
+#ifdef SS_TRACE
+extern "C" int ss_exp_trace_reset(void) {
+  static long long zeros[9][512];
+  return cudaMemcpyToSymbol(ts::g_trace, zeros, sizeof(zeros)) == cudaSuccess ? 0 : 1;
+}
+extern "C" int ss_exp_trace(long long* host, long long* whost) {
+  if (cudaMemcpyFromSymbol(host, ts::g_trace, sizeof(ts::g_trace)) != cudaSuccess) return 1;
+  return cudaMemcpyFromSymbol(whost, ts::g_wtrace, sizeof(ts::g_wtrace)) == cudaSuccess ? 0 : 1;
+}
+#endif
 
 static PFN_cuTensorMapEncodeTiled_v12000 ts_encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -676,6 +728,9 @@ int topk_ts_lists(const TopkArgs& a, int device) {
   const int64_t qtiles = (a.nq + ts::BM - 1) / ts::BM;
   const int bn = ts_shape(a.dim, a.k, false).bn;
   const int64_t tiles = (a.n_rows + bn - 1) / bn;
+#ifdef SS_EXP_SLICES  // scripts/exp_build.sh ablation: a fixed slice count
+  return (int)std::min<int64_t>(SS_EXP_SLICES, tiles);
+#endif
   return pick_slices(qtiles, tiles, sm_count(device));
 }
 
