@@ -103,10 +103,16 @@ int ss_cost_distribution_batch(int32_t kind, double w_in, double w_out,
                                double* out_support, void* stream);
 /* Per-call forms of gittins_min (_kernels.py:104-116) and cost_distribution
  * (cost.py:107-118) for the reference's scalar call pattern: HOST arrays in
- * and out, one packed H2D copy through library-owned pinned staging, the
- * kernel, one D2H, synchronise -- no allocation per call.  (A batched
- * engine uses the *_batch forms or the fused round.)  gittins_min_host with a
- * leading zero mass -> SS_ERR_ZERODIV, as numba raises; n = 0 -> +inf. */
+ * and out, no allocation per call.  Up to 2048 points the inputs go into a
+ * per-thread mapped pinned slot that the kernel reads across PCIe and
+ * answers through (result + a completion flag the caller spins on: no
+ * copy-engine transfer, no stream synchronise); the call runs on the
+ * library's own per-thread stream and `stream` may be NULL (inputs and
+ * outputs are host memory, so it orders nothing).  Longer laws take one
+ * packed H2D copy, the kernel, one D2H and a synchronise on `stream`.  (A
+ * batched engine uses the *_batch forms or the fused round.)
+ * gittins_min_host with a leading zero mass -> SS_ERR_ZERODIV, as numba
+ * raises; n = 0 -> +inf. */
 int ss_gittins_min_host(const double* support, const double* masses, int64_t n, double* out,
                         void* stream);
 int ss_cost_distribution_host(int32_t kind, double w_in, double w_out, double input_len,

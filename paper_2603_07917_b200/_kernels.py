@@ -82,16 +82,18 @@ def gittins_min(support, masses) -> float:
     (_kernels.py:104-116).  Leading zero mass raises ZeroDivisionError.
 
     The reference's per-law call: host arrays through ss_gittins_min_host
-    (pinned staging, one copy each way, no allocation); an engine that has
-    many laws uses ``gittins_min_batch`` (device tensors, one launch)."""
+    (a mapped pinned slot the kernel reads and answers through, no
+    allocation); an engine that has many laws uses ``gittins_min_batch``
+    (device tensors, one launch)."""
     _lib.require_cuda()
     s = np.ascontiguousarray(support, dtype=np.float64).reshape(-1)
     m = np.ascontiguousarray(masses, dtype=np.float64).reshape(-1)
     if s.size != m.size:
         raise ValueError("support and masses differ in length")
     out = C.c_double()
-    _lib.call("ss_gittins_min_host", s.ctypes.data, m.ctypes.data, s.size, C.byref(out),
-              _lib.stream_ptr())
+    # host memory in and out: the library's own per-thread stream and mapped
+    # slot (no torch stream lookup, no copy engine, no stream sync)
+    _lib.call("ss_gittins_min_host", s.ctypes.data, m.ctypes.data, s.size, C.byref(out), None)
     return out.value
 
 

@@ -101,18 +101,12 @@ __device__ __forceinline__ double warp_incl_scan_f64(double v, int lane) {
   return v;
 }
 
-__global__ void __launch_bounds__(256)
-k_gittins_dist(const double* __restrict__ support, const double* __restrict__ masses,
-               const int64_t* __restrict__ npts, const double* __restrict__ attained,
-               const double* __restrict__ outlived, int64_t n, int64_t stride,
-               double* __restrict__ out, int* __restrict__ err, int ref_mode) {
-  const int lane = threadIdx.x & 31;
-  const int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (i >= n) return;
-  const int64_t np = npts[i];
-  const double* s = support + i * stride;
-  const double* m = masses + i * stride;
-  const double a = attained ? attained[i] : 0.0;
+// One law, one warp: min over survivors of (cum_xp + s (1 - cum_p)) / cum_p
+// (_kernels.py:104-116; conditioned on attained a and renormalised unless
+// ref_mode).  Returns the value on lane 0's `*out_i`.
+__device__ __forceinline__ void gittins_warp(const double* s, const double* m, int64_t np, double a,
+                                             const double* outlived_i, int ref_mode, double* out_i,
+                                             int* err, int lane) {
   // survivors are a suffix (support strictly increasing); find first index
   // with s > a and the survivor mass Z.
   double Z = 0.0;
@@ -132,7 +126,7 @@ k_gittins_dist(const double* __restrict__ support, const double* __restrict__ ma
     Z = 1.0;
   }
   if (first >= np) {  // outlived every hypothesis or empty
-    if (lane == 0) out[i] = (np == 0) ? INFINITY : (outlived ? outlived[i] : INFINITY);
+    if (lane == 0) *out_i = (np == 0) ? INFINITY : (outlived_i ? *outlived_i : INFINITY);
     return;
   }
   double cp = 0.0, cxp = 0.0, best = INFINITY;
@@ -154,7 +148,86 @@ k_gittins_dist(const double* __restrict__ support, const double* __restrict__ ma
     cxp = __shfl_sync(0xffffffffu, xp, 31);
   }
   best = warp_min_f64(best);
-  if (lane == 0) out[i] = best;
+  if (lane == 0) *out_i = best;
+}
+
+__global__ void __launch_bounds__(256)
+k_gittins_dist(const double* __restrict__ support, const double* __restrict__ masses,
+               const int64_t* __restrict__ npts, const double* __restrict__ attained,
+               const double* __restrict__ outlived, int64_t n, int64_t stride,
+               double* __restrict__ out, int* __restrict__ err, int ref_mode) {
+  const int lane = threadIdx.x & 31;
+  const int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (i >= n) return;
+  gittins_warp(support + i * stride, masses + i * stride, npts[i], attained ? attained[i] : 0.0,
+               outlived ? outlived + i : nullptr, ref_mode, out + i, err, lane);
+}
+
+// ------------------------------------------------------------ per call ----
+// The reference's scalar call (one law per call, host arrays in and out)
+// through mapped pinned memory: the kernel pulls the inputs across PCIe with
+// every load in flight at once (into shared memory), computes, writes the
+// result back into host memory and raises the slot's flag; the caller spins
+// on the flag.  No copy-engine transfer and no stream synchronisation.
+__device__ __forceinline__ void percall_pull(double* dst, const double* src, int64_t n) {
+  for (int64_t k = threadIdx.x; k < n; k += blockDim.x) dst[k] = src[k];
+}
+__device__ __forceinline__ void percall_raise(PerCallHdr* h, uint32_t seq) {
+  __threadfence_system();
+  *reinterpret_cast<volatile uint32_t*>(&h->flag) = seq;
+}
+
+__global__ void __launch_bounds__(128) k_gittins_percall(PerCallHdr* h, uint32_t seq) {
+  extern __shared__ double sm[];
+  const int64_t n = h->n;
+  const double* src = reinterpret_cast<const double*>(h + 1);
+  percall_pull(sm, src, 2 * n);
+  __shared__ int err;
+  __shared__ double res;
+  if (threadIdx.x == 0) err = 0;
+  __syncthreads();
+  if (threadIdx.x < 32) gittins_warp(sm, sm + n, n, 0.0, nullptr, 1, &res, &err, threadIdx.x);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    h->result = res;
+    h->err = err;
+    percall_raise(h, seq);
+  }
+}
+
+__global__ void __launch_bounds__(128) k_cost_percall(PerCallHdr* h, uint32_t seq) {
+  const int64_t n = h->n;
+  const double in = h->input_len, w_in = h->w_in, w_out = h->w_out;
+  const int kind = h->kind;
+  const double* src = reinterpret_cast<const double*>(h + 1);
+  double* dst = const_cast<double*>(src) + n;
+  for (int64_t k = threadIdx.x; k < n; k += blockDim.x) {
+    const double l = src[k];
+    double r;
+    if (kind == SS_COST_RESOURCE_BOUND)
+      r = __dadd_rn(__dmul_rn(__dmul_rn(l, l), 0.5), __dmul_rn(in, l));  // cost.py:98-99
+    else if (kind == SS_COST_OUTPUT_ONLY)
+      r = l;                                                               // cost.py:100-101
+    else
+      r = __dadd_rn(__dmul_rn(w_in, in), __dmul_rn(w_out, l));           // cost.py:102-103
+    dst[k] = r;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) percall_raise(h, seq);
+}
+
+int launch_gittins_percall(PerCallHdr* h_dev, int64_t n, uint32_t seq, cudaStream_t st) {
+  count_launch();
+  k_gittins_percall<<<1, 128, (size_t)2 * n * sizeof(double), st>>>(h_dev, seq);
+  SS_LAUNCH_CHECK();
+  return SS_OK;
+}
+
+int launch_cost_percall(PerCallHdr* h_dev, uint32_t seq, cudaStream_t st) {
+  count_launch();
+  k_cost_percall<<<1, 128, 0, st>>>(h_dev, seq);
+  SS_LAUNCH_CHECK();
+  return SS_OK;
 }
 
 int launch_gittins_dist(const double* support, const double* masses, const int64_t* npts,

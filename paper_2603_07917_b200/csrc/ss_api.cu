@@ -295,12 +295,79 @@ struct HostStaging {
 };
 static thread_local HostStaging g_stage;
 
+// Mapped per-call slot and a library stream, per thread (see PerCallHdr).
+struct PerCallSlot {
+  PerCallHdr* host = nullptr;  // mapped pinned
+  PerCallHdr* dev = nullptr;   // its device alias
+  cudaStream_t st = nullptr;
+  uint32_t seq = 0;
+  int device = -1;
+  ~PerCallSlot() { release(); }
+  void release() {
+    if (host) cudaFreeHost(host);
+    if (st) cudaStreamDestroy(st);
+    host = dev = nullptr;
+    st = nullptr;
+  }
+  int ready() {
+    int d = 0;
+    cudaGetDevice(&d);
+    if (host && d == device) return SS_OK;
+    release();
+    const size_t bytes = sizeof(PerCallHdr) + (size_t)2 * kPerCallMaxPts * sizeof(double);
+    void* p = nullptr;
+    SS_CUDA_TRY(cudaHostAlloc(&p, bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+    host = static_cast<PerCallHdr*>(p);
+    memset(host, 0, bytes);
+    void* dp = nullptr;
+    SS_CUDA_TRY(cudaHostGetDevicePointer(&dp, p, 0));
+    dev = static_cast<PerCallHdr*>(dp);
+    SS_CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    device = d;
+    return SS_OK;
+  }
+  // spin until the kernel raised the flag for `s` (or the stream failed)
+  int wait(uint32_t s) {
+    volatile uint32_t* f = &host->flag;
+    for (uint32_t spins = 1; *f != s; ++spins) {
+      if ((spins & 4095) == 0) {
+        cudaError_t e = cudaStreamQuery(st);
+        if (e != cudaSuccess && e != cudaErrorNotReady)
+          return set_error(SS_ERR_CUDA, "per-call kernel: %s", cudaGetErrorString(e));
+        if (e == cudaSuccess && *f != s)
+          return set_error(SS_ERR_CUDA, "per-call kernel finished without raising its flag");
+      }
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
+    return SS_OK;
+  }
+};
+static thread_local PerCallSlot g_call;
+
 extern "C" int ss_gittins_min_host(const double* support, const double* masses, int64_t n,
                                    double* out, void* stream) {
   if (n < 0 || !out || (n > 0 && (!support || !masses)))
     return set_error(SS_ERR_ARG, "gittins_min_host: bad args");
   if (n == 0) {
     *out = INFINITY;  // min over no support point
+    return SS_OK;
+  }
+  if (n <= kPerCallMaxPts) {
+    // mapped slot: inputs written here, pulled by the kernel; result and
+    // flag written back by the kernel (the stream argument orders nothing:
+    // inputs and output are host memory)
+    if (int rc = g_call.ready()) return rc;
+    PerCallHdr* h = g_call.host;
+    h->n = n;
+    double* data = reinterpret_cast<double*>(h + 1);
+    memcpy(data, support, (size_t)n * 8);
+    memcpy(data + n, masses, (size_t)n * 8);
+    const uint32_t seq = ++g_call.seq;
+    std::atomic_thread_fence(std::memory_order_release);
+    if (int rc = launch_gittins_percall(g_call.dev, n, seq, g_call.st)) return rc;
+    if (int rc = g_call.wait(seq)) return rc;
+    if (h->err == SS_ERR_ZERODIV) return set_error(SS_ERR_ZERODIV, "float division by zero");
+    *out = h->result;
     return SS_OK;
   }
   // staging: [npts i64][result f64][err i32 + pad][support n][masses n]
@@ -338,6 +405,23 @@ extern "C" int ss_cost_distribution_host(int32_t kind, double w_in, double w_out
   if (n < 0 || (n > 0 && (!len_support || !out_support)))
     return set_error(SS_ERR_ARG, "cost_distribution_host: bad args");
   if (n == 0) return SS_OK;
+  if (n <= kPerCallMaxPts) {  // mapped slot (see ss_gittins_min_host)
+    if (int rc = g_call.ready()) return rc;
+    PerCallHdr* h = g_call.host;
+    h->n = n;
+    h->input_len = input_len;
+    h->w_in = w_in;
+    h->w_out = w_out;
+    h->kind = kind;
+    double* data = reinterpret_cast<double*>(h + 1);
+    memcpy(data, len_support, (size_t)n * 8);
+    const uint32_t seq = ++g_call.seq;
+    std::atomic_thread_fence(std::memory_order_release);
+    if (int rc = launch_cost_percall(g_call.dev, seq, g_call.st)) return rc;
+    if (int rc = g_call.wait(seq)) return rc;
+    memcpy(out_support, data + n, (size_t)n * 8);
+    return SS_OK;
+  }
   // staging: [npts i64][I f64][support n][out n]
   const size_t hdr = 16, need = hdr + (size_t)n * 16;
   if (int rc = g_stage.reserve(need)) return rc;

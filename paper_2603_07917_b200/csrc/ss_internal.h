@@ -38,6 +38,23 @@ int pick_slices(int64_t qtiles, int64_t tiles, int sms);
 int launch_match_pmfs(const float* sims, int64_t nq, int64_t nw, const int64_t* lens,
                       double theta, int64_t max_len, double* sup, double* mas,
                       int64_t* sizes, int64_t out_stride, int* err, cudaStream_t st);
+// Per-call slot in mapped pinned memory (64-byte header, then the data):
+// the host writes n (and the cost parameters) and the inputs, launches, and
+// spins until the kernel sets flag to the call's sequence number.
+struct PerCallHdr {
+  uint32_t flag;
+  int32_t err;
+  double result;
+  int64_t n;
+  double input_len;
+  double w_in, w_out;
+  int32_t kind;
+  int32_t pad[3];
+};
+static_assert(sizeof(PerCallHdr) == 64, "per-call header is 64 bytes");
+constexpr int64_t kPerCallMaxPts = 2048;  // 2 x 2048 doubles of inputs = 32 KB of shared memory
+int launch_gittins_percall(PerCallHdr* h_dev, int64_t n, uint32_t seq, cudaStream_t st);
+int launch_cost_percall(PerCallHdr* h_dev, uint32_t seq, cudaStream_t st);
 int launch_gittins_dist(const double* support, const double* masses, const int64_t* npts,
                         const double* attained, const double* outlived, int64_t n,
                         int64_t stride, double* out, int* err, int ref_mode, cudaStream_t st);

@@ -93,6 +93,50 @@ def test_gittins_min_vs_reference(cuda, golden):
     assert K.gittins_min(np.zeros(0), np.zeros(0)) == np.inf
 
 
+def test_percall_paths_match_batch(cuda):
+    """The per-call drop-ins (mapped slot up to 2048 points, staged copies
+    above) give bit-identical values to the batched kernels, for every size
+    around the warp and slot boundaries, and from several threads at once
+    (the slot is per thread)."""
+    import threading
+
+    from paper_2603_07917_b200 import _kernels as K
+    from paper_2603_07917_b200 import cost as Cst
+    from paper_2603_07917_b200.distribution import DiscreteDistribution
+    rng = np.random.default_rng(11)
+    laws = []
+    for n in (1, 2, 31, 32, 33, 64, 511, 512, 2047, 2048, 2049, 5000):
+        sup = np.sort(rng.choice(np.arange(1, 10 * n + 10), n, replace=False)).astype(np.float64)
+        mas = rng.random(n) + 0.01
+        mas /= mas.sum()
+        laws.append((sup, mas))
+    for sup, mas in laws:
+        n = sup.size
+        ref = K.gittins_min_batch(_t(sup[None]), _t(mas[None]), _t(np.array([n], np.int64)))
+        assert K.gittins_min(sup, mas) == ref.item(), n
+        I = float(rng.integers(1, 4000))
+        got = Cst.cost_distribution(Cst.ResourceBound(), I, DiscreteDistribution(sup, mas))
+        want = Cst.cost_distribution_batch(Cst.ResourceBound(), _t(np.array([I])), _t(sup[None]),
+                                           _t(np.array([n], np.int64)))
+        np.testing.assert_array_equal(got.support, want[0, :n].cpu().numpy())
+    expect = [K.gittins_min(s_, m_) for s_, m_ in laws]
+    errs = []
+
+    def worker():
+        torch.cuda.set_device(0)
+        for _ in range(20):
+            for (s_, m_), e in zip(laws, expect):
+                if K.gittins_min(s_, m_) != e:
+                    errs.append(s_.size)
+
+    th = [threading.Thread(target=worker) for _ in range(4)]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join()
+    assert not errs
+
+
 def test_embed_vs_reference(cuda, golden):
     from paper_2603_07917_b200 import _kernels as K
     g = golden

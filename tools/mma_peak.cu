@@ -34,8 +34,14 @@ __host__ __device__ constexpr uint32_t idesc(int n) {
   return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
 }
 
+// MODE (compile time, so the peak loop carries no per-K-block tests -- any
+// extra instruction between MMAs lowers the issue rate): 0 = back to back;
+// bit 0: commit to bar_c (never completes) after every K-block; bit 1: wait on
+// bar_w (already complete) + tcgen05 fence before every K-block; bit 2: the
+// same with test_wait; bit 3: poll a shared flag; bit 4: acquire-load poll.
+template <int mode>
 __global__ void __launch_bounds__(384, 1) k_mma_peak(int tiles, int n, int a_tmem, int nacc, int drain_iters,
-                                                     unsigned* sink, int mode) {
+                                                     unsigned* sink) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;                  // NKB x 16 KB
@@ -118,28 +124,28 @@ __global__ void __launch_bounds__(384, 1) k_mma_peak(int tiles, int n, int a_tme
     for (int t = 0; t < tiles; ++t) {
       const uint32_t d = tmem + (t % nacc) * n;
       for (int kb = 0; kb < NKB; ++kb) {
-        if (mode & 4) {
+        if constexpr (mode & 4) {
           asm volatile(
               "{\n.reg .pred p;\nWT_%=:\nmbarrier.test_wait.parity.shared::cta.b64 p, [%0], 0;\n@!p bra WT_%=;\n}\n" ::"r"(
                   su32(&bar_w))
               : "memory");
           asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         }
-        if (mode & 8) {  // a plain shared-memory flag, polled
+        if constexpr (mode & 8) {  // a plain shared-memory flag, polled
           uint32_t f;
           do {
             asm volatile("ld.volatile.shared.u32 %0, [%1];\n" : "=r"(f) : "r"(su32(&flag)) : "memory");
           } while (f == 0);
           asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         }
-        if (mode & 16) {  // acquire-load poll of the flag
+        if constexpr (mode & 16) {  // acquire-load poll of the flag
           uint32_t f;
           do {
             asm volatile("ld.acquire.cta.shared.u32 %0, [%1];\n" : "=r"(f) : "r"(su32(&flag)) : "memory");
           } while (f == 0);
           asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         }
-        if (mode & 2) {
+        if constexpr (mode & 2) {
           asm volatile(
               "{\n.reg .pred p;\nWW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n@!p bra WW_%=;\n}\n" ::"r"(
                   su32(&bar_w))
@@ -165,7 +171,7 @@ __global__ void __launch_bounds__(384, 1) k_mma_peak(int tiles, int n, int a_tme
                 : "memory");
           }
         }
-        if (mode & 1)
+        if constexpr (mode & 1)
           asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
                            su32(&bar_c))
                        : "memory");
@@ -211,11 +217,15 @@ int mma_peak_run3(int n_cta, int tiles, int n, int a_in_tmem, int drain_warps, i
   const int nacc = (!a_in_tmem || 2 * n + DIM / 4 <= 512) ? 2 : 1;
   if (n < 8 || n > 256 || n % 16 || (a_in_tmem && nacc * n + DIM / 4 > 512)) return 1;
   const size_t smem = 1024 + (size_t)NKB * BM * BK + (size_t)NKB * n * BK;
-  if (cudaFuncSetAttribute(k_mma_peak, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+  auto kern = mode == 0 ? k_mma_peak<0> : mode == 1 ? k_mma_peak<1> : mode == 2 ? k_mma_peak<2> :
+              mode == 3 ? k_mma_peak<3> : mode == 4 ? k_mma_peak<4> : mode == 8 ? k_mma_peak<8> :
+              mode == 16 ? k_mma_peak<16> : nullptr;
+  if (!kern) return 5;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess)
     return 2;
-  k_mma_peak<<<n_cta, 128 + 32 * drain_warps, smem, (cudaStream_t)stream>>>(
-      tiles, n, a_in_tmem, nacc, drain_warps ? drain_iters : 0, sink, mode);
+  kern<<<n_cta, 128 + 32 * drain_warps, smem, (cudaStream_t)stream>>>(
+      tiles, n, a_in_tmem, nacc, drain_warps ? drain_iters : 0, sink);
   return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
 int mma_peak_dim(void) { return DIM; }
