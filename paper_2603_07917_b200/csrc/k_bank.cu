@@ -113,11 +113,37 @@ k_bank_write(int8_t* __restrict__ emb, float* __restrict__ inv, int32_t* __restr
   }
 }
 
+// The filter bounds of every 16-row group a write touched: (max inverse norm,
+// floored at 0; min inverse norm, capped at +inf) over the group's non-NaN
+// rows -- exactly the per-16-column bounds the TS kernel's epilogue used to
+// reduce from the tile's norms every tile, now computed once per write.  One
+// thread per written record recomputes its record's group (records sharing a
+// group write the same values).
+__global__ void __launch_bounds__(256)
+k_bank_bounds(const float* __restrict__ inv, float2* __restrict__ ibnd,
+              const int64_t* __restrict__ src_slot, int64_t n, int64_t first_seq, int64_t capacity,
+              int64_t skip) {
+  const int64_t r = skip + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const int64_t slot = src_slot ? src_slot[r] : (first_seq + r) % capacity;
+  if (slot < 0 || slot >= capacity) return;  // (k_bank_write flags it)
+  const int64_t g = slot >> 4;
+  const float4* p = reinterpret_cast<const float4*>(inv + g * 16);
+  float hi = 0.f, lo = INFINITY;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const float4 w = p[u];  // NaN (empty, zero or wide row) is ignored by fmaxf / fminf
+    hi = fmaxf(hi, fmaxf(fmaxf(w.x, w.y), fmaxf(w.z, w.w)));
+    lo = fminf(lo, fminf(fminf(w.x, w.y), fminf(w.z, w.w)));
+  }
+  ibnd[g] = make_float2(hi, lo);
+}
+
 int launch_bank_write(int8_t* emb, float* inv, int32_t* lens, int64_t* seq, int32_t* len_cnt,
                       int dim, const void* src_emb, int src_bytes, const float* src_inv,
                       const int32_t* src_lens, const int64_t* src_seq, const int64_t* src_slot,
                       int64_t n, int64_t first_seq, int64_t capacity, int64_t skip, int* err,
-                      cudaStream_t st, const int64_t* src_idx, const WidePlane* wp) {
+                      cudaStream_t st, const int64_t* src_idx, const WidePlane* wp, float2* ibnd) {
   int64_t m = n - skip;
   if (m <= 0) return SS_OK;
   const WidePlane w = wp ? *wp : WidePlane{};
@@ -134,6 +160,12 @@ int launch_bank_write(int8_t* emb, float* inv, int32_t* lens, int64_t* seq, int3
                                                src_lens, src_seq, src_slot, n, first_seq, capacity,
                                                skip, err, src_idx, w);
   SS_LAUNCH_CHECK();
+  if (ibnd) {
+    count_launch();
+    k_bank_bounds<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(inv, ibnd, src_slot, n, first_seq,
+                                                              capacity, skip);
+    SS_LAUNCH_CHECK();
+  }
   return SS_OK;
 }
 

@@ -308,7 +308,8 @@ constexpr int NACC = 2;  // accumulators: the MMA of tile t+1 runs while tile t 
 template <int BN, bool SHARE, bool RING>
 __global__ void __launch_bounds__(THREADS, 1)
 k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
-          const float* __restrict__ q_inv, int64_t nq, const float* __restrict__ inv, int64_t n_rows,
+          const float* __restrict__ q_inv, int64_t nq, const float* __restrict__ inv,
+          const float2* __restrict__ ibnd, int64_t n_rows,
           int dim, int stages, int k, float theta, int64_t hmod, int64_t gcap, int64_t slot_offset,
           int64_t tiles_per_slice, uint64_t* __restrict__ partials,
           uint32_t* __restrict__ gslots, int rshare) {
@@ -327,8 +328,7 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
   int* s_hcnt = reinterpret_cast<int*>(s_hroot + BM);                    // [128]
   int* s_hlock = s_hcnt + BM;                                            // [128]
   float* s_inv = reinterpret_cast<float*>(s_hlock + BM);                 // [ISLOTS][256]
-  float* s_ib = s_inv + IS * 256;                                        // [8 warps][16]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(s_ib + EPI_WARPS * 16);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(s_inv + IS * 256);
   // barriers: RING -- full[2] (a tile's parts landed + its accumulator
   // released), empty[2 * nkb] (one per K-block part); else full/empty[stages]
   const int nfull = RING ? NACC : stages, nempty = RING ? NACC * nkb : stages;
@@ -383,8 +383,9 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
         const int sl = t % IS;
         if constexpr (!RING) {
           bar_wait(&iempty[sl], ((t / IS) & 1) ^ 1);
-          bar_expect(&ifull[sl], BN * 4);
+          bar_expect(&ifull[sl], BN * 4 + BN / 2);
           bulk_g2s(s_inv + sl * 256, inv + row0, BN * 4, &ifull[sl]);
+          bulk_g2s(s_inv + sl * 256 + BN, ibnd + row0 / 16, BN / 2, &ifull[sl]);
         }
         if constexpr (RING) {
           // part kb of stage t & 1 is free once tile t - 2's K-block kb MMAs
@@ -402,8 +403,9 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
           // frees only when the epilogue is done with tile t - 2, which must
           // not hold back the bank loads
           bar_wait(&iempty[sl], ((t / IS) & 1) ^ 1);
-          bar_expect(&ifull[sl], BN * 4);
+          bar_expect(&ifull[sl], BN * 4 + BN / 2);
           bulk_g2s(s_inv + sl * 256, inv + row0, BN * 4, &ifull[sl]);
+          bulk_g2s(s_inv + sl * 256 + BN, ibnd + row0 / 16, BN / 2, &ifull[sl]);
         } else {
           for (int kb = 0; kb < nkb; ++kb, ++it) {
             const int s = it % stages;
@@ -491,7 +493,6 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
     }
     const float iq = (q < nq) ? q_inv[q] : __int_as_float(0x7fc00000);
     uint64_t* heap = s_heap + qrow;  // shared by the two column-half warps of this quarter
-    float* cib = s_ib + ew * 16;  // [max inv_w of half 0..7][min inv_w of half 0..7]
     float thr = (iq == iq) ? s_threshold(theta, iq) : INFINITY;
     for (int t = 0; t < ntiles; ++t) {
       const int64_t row0 = (tile0 + t) * BN + grp * CW;  // first bank row of my columns
@@ -510,25 +511,9 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
       }
       bar_wait_epi(&ifull[sl], (t / IS) & 1);
       TRACE(0, t);
-      {
-        // NaN (zero row / past the end) never passes the exact test: leave it
-        // out of the bounds
-        const float NaNf = __int_as_float(0x7fc00000);  // ignored by fmaxf / fminf
-        const float4 w4 = (lane * 4 < CW) ? reinterpret_cast<const float4*>(ciw)[lane]
-                                            : make_float4(NaNf, NaNf, NaNf, NaNf);
-        float hi = fmaxf(fmaxf(fmaxf(w4.x, w4.y), fmaxf(w4.z, w4.w)), 0.f);
-        float lo = fminf(fminf(fminf(w4.x, w4.y), fminf(w4.z, w4.w)), INFINITY);
-#pragma unroll
-        for (int o = 1; o < 4; o <<= 1) {  // 4 lanes x 4 floats = one 16-column half
-          hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-          lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-        }
-        if ((lane & 3) == 0 && lane * 4 < CW) {
-          cib[lane >> 2] = hi;
-          cib[8 + (lane >> 2)] = lo;
-        }
-      }
-      __syncwarp();
+      // this warp's four 16-column filter bounds (hi0, lo0, hi1, lo1 per
+      // 32-column chunk), precomputed per 16-row group by every bank write
+      const float4* cb = reinterpret_cast<const float4*>(s_inv + sl * 256 + BN) + grp * 2;
       TRACE(1, t);
       bar_wait_epi(&tfull[acc], (t / NACC) & 1);
       TRACE(2, t);
@@ -620,8 +605,9 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
         const int b4 = __vimax3_s32(v[28], v[29], v[30]);
         const int mdl = __vimax3_s32(__vimax3_s32(a0, a1, a2), __vimax3_s32(a3, a4, v[15]), a0);
         const int mdh = __vimax3_s32(__vimax3_s32(b0, b1, b2), __vimax3_s32(b3, b4, v[31]), b0);
-        const float bl = __fmul_rn(__int2float_rn(mdl), mdl >= 0 ? cib[2 * c] : cib[8 + 2 * c]);
-        const float bh = __fmul_rn(__int2float_rn(mdh), mdh >= 0 ? cib[2 * c + 1] : cib[8 + 2 * c + 1]);
+        const float4 bc = cb[c];
+        const float bl = __fmul_rn(__int2float_rn(mdl), mdl >= 0 ? bc.x : bc.y);
+        const float bh = __fmul_rn(__int2float_rn(mdh), mdh >= 0 ? bc.z : bc.w);
         if constexpr (SHARE) {
           // pure top-k: many chunks pass while the bounds rise -- one exact
           // pass (and one heap lock) per 32 columns is cheaper there
@@ -678,8 +664,9 @@ static PFN_cuTensorMapEncodeTiled_v12000 ts_encode() {
 }
 
 static size_t ts_fixed_smem(int k, int islots) {
-  return (size_t)k * ts::BM * 8 + ts::BM * 16 + (size_t)islots * 256 * 4 + ts::EPI_WARPS * 16 * 4 + 512 +
-         1024;
+  // heaps, per-query root / count / lock, the norms + bounds ring, barriers,
+  // 1 KB alignment slack
+  return (size_t)k * ts::BM * 8 + ts::BM * 16 + (size_t)islots * 256 * 4 + 512 + 1024;
 }
 
 // Shape of one launch: tile rows BN (the widest double buffer of accumulators
@@ -719,7 +706,7 @@ static TsShape ts_shape(int dim, int k, bool share) {
 bool topk_ts_supported(const TopkArgs& a) {
   if (a.dim % ts::BK || a.dim < ts::BK || a.k < 1 || a.k > ts::KMAX) return false;
   if (a.n_rows >= (1LL << 31) || a.nq >= (1LL << 31)) return false;
-  if (!a.inv_padded) return false;  // tiles of inverse norms are bulk-copied whole
+  if (!a.inv_padded || !a.ibnd) return false;  // tiles of norms and bounds are bulk-copied whole
   return ts_shape(a.dim, a.k, true).bn > 0 && ts_shape(a.dim, a.k, false).bn > 0;
 }
 
@@ -757,8 +744,8 @@ static int launch_ts_t(const TopkArgs& a, const TsShape& sh, int rshare, uint64_
   const int64_t tps = (tiles + n_slices - 1) / n_slices;
   dim3 grid((unsigned)((a.nq + ts::BM - 1) / ts::BM), (unsigned)n_slices);
   count_launch();
-  kern<<<grid, ts::THREADS, sh.smem, st>>>(mb, a.q, a.q_inv, a.nq, a.inv, a.n_rows, a.dim, sh.stages, a.k,
-                                           a.theta, a.head % a.gcap, a.gcap, a.slot_offset, tps,
+  kern<<<grid, ts::THREADS, sh.smem, st>>>(mb, a.q, a.q_inv, a.nq, a.inv, a.ibnd, a.n_rows, a.dim,
+                                           sh.stages, a.k, a.theta, a.head % a.gcap, a.gcap, a.slot_offset, tps,
                                            partials, a.gslots, rshare);
   SS_LAUNCH_CHECK();
   return SS_OK;

@@ -107,6 +107,7 @@ struct ss_bank {
   int64_t head;
   int8_t* emb = nullptr;
   float* inv = nullptr;
+  float2* ibnd = nullptr;  // per 16-row group filter bounds (k_bank_bounds), padded like inv
   int32_t* lens = nullptr;
   int64_t* seq = nullptr;
   int32_t* len_cnt = nullptr;  // exact-length histogram of the window [65536]
@@ -469,6 +470,8 @@ int ss_bank_create(ss_bank_t** out, int32_t device, int64_t capacity, int32_t di
   cudaError_t e;
   if ((e = cudaMalloc(&h->emb, (size_t)capacity * dim)) != cudaSuccess) fail(e);
   else if ((e = cudaMalloc(&h->inv, ((size_t)capacity + 256) * 4)) != cudaSuccess) fail(e);
+  else if ((e = cudaMalloc(&h->ibnd, (((size_t)capacity + 15) / 16 + 16) * sizeof(float2))) != cudaSuccess)
+    fail(e);
   else if ((e = cudaMalloc(&h->lens, (size_t)capacity * 4)) != cudaSuccess) fail(e);
   else if ((e = cudaMalloc(&h->seq, (size_t)capacity * 8)) != cudaSuccess) fail(e);
   else if ((e = cudaMalloc(&h->len_cnt, 65536 * 4)) != cudaSuccess) fail(e);
@@ -480,6 +483,17 @@ int ss_bank_create(ss_bank_t** out, int32_t device, int64_t capacity, int32_t di
   if (rc == SS_OK) {
     cudaMemset(h->emb, 0, (size_t)capacity * dim);
     cudaMemset(h->inv, 0xff, ((size_t)capacity + 256) * 4);  // NaN: never matches (+1 tile pad)
+    {  // every group empty: (0, +inf)
+      const size_t ng = ((size_t)capacity + 15) / 16 + 16;
+      float2* hb = static_cast<float2*>(malloc(ng * sizeof(float2)));
+      if (hb) {
+        for (size_t i = 0; i < ng; ++i) hb[i] = make_float2(0.f, INFINITY);
+        cudaMemcpy(h->ibnd, hb, ng * sizeof(float2), cudaMemcpyHostToDevice);
+        free(hb);
+      } else {
+        rc = set_error(SS_ERR_ARG, "bank_create: oom");
+      }
+    }
     cudaMemset(h->lens, 0, (size_t)capacity * 4);
     cudaMemset(h->seq, 0xff, (size_t)capacity * 8);  // -1: empty slot
     cudaMemset(h->len_cnt, 0, 65536 * 4);
@@ -500,6 +514,7 @@ int ss_bank_destroy(ss_bank_t* h) {
   DeviceGuard g(h->device);
   cudaFree(h->emb);
   cudaFree(h->inv);
+  cudaFree(h->ibnd);
   cudaFree(h->lens);
   cudaFree(h->seq);
   cudaFree(h->len_cnt);
@@ -531,7 +546,7 @@ int ss_bank_push(ss_bank_t* h, const int8_t* emb, const float* inv_norm, const i
   int64_t skip = n > h->cap ? n - h->cap : 0;
   int rc = launch_bank_write(h->emb, h->inv, h->lens, h->seq, h->len_cnt, h->dim, emb, 1, inv_norm,
                              lens, nullptr, nullptr, n, h->head, h->cap, skip, h->d_err,
-                             (cudaStream_t)stream, nullptr, h->wp.flag ? &h->wp : nullptr);
+                             (cudaStream_t)stream, nullptr, h->wp.flag ? &h->wp : nullptr, h->ibnd);
   if (rc) return rc;
   h->head += n;
   return SS_OK;
@@ -542,7 +557,7 @@ int ss_bank_write(ss_bank_t* h, const int8_t* emb, const float* inv_norm, const 
   if (!h || n < 0 || !seq || !local_slot) return set_error(SS_ERR_ARG, "bank_write: bad args");
   return launch_bank_write(h->emb, h->inv, h->lens, h->seq, h->len_cnt, h->dim, emb, 1, inv_norm,
                            lens, seq, local_slot, n, 0, h->cap, 0, h->d_err, (cudaStream_t)stream,
-                           nullptr, h->wp.flag ? &h->wp : nullptr);
+                           nullptr, h->wp.flag ? &h->wp : nullptr, h->ibnd);
 }
 
 static int ensure_wide(ss_bank* h) {
@@ -592,7 +607,7 @@ int ss_bank_push16(ss_bank_t* h, const int16_t* emb, const float* inv_norm, cons
   const int64_t skip = n > h->cap ? n - h->cap : 0;
   int rc = launch_bank_write(h->emb, h->inv, h->lens, h->seq, h->len_cnt, h->dim, emb, 2, inv_norm,
                              lens, nullptr, nullptr, n, h->head, h->cap, skip, h->d_err, st,
-                             nullptr, &h->wp);
+                             nullptr, &h->wp, h->ibnd);
   if (rc) return rc;
   h->head += n;
   return note_wide(h, st);
@@ -605,7 +620,8 @@ int ss_bank_write16(ss_bank_t* h, const int16_t* emb, const float* inv_norm, con
   if (int rc = ensure_wide(h)) return rc;
   cudaStream_t st = (cudaStream_t)stream;
   int rc = launch_bank_write(h->emb, h->inv, h->lens, h->seq, h->len_cnt, h->dim, emb, 2, inv_norm,
-                             lens, seq, local_slot, n, 0, h->cap, 0, h->d_err, st, nullptr, &h->wp);
+                             lens, seq, local_slot, n, 0, h->cap, 0, h->d_err, st, nullptr, &h->wp,
+                             h->ibnd);
   if (rc) return rc;
   return note_wide(h, st);
 }
@@ -691,6 +707,7 @@ static size_t topk_ws_need(ss_bank* h, int64_t nq, int32_t k, int32_t algo, cons
   TopkArgs a{nullptr, nullptr, nq, h->emb, h->inv, h->cap, h->dim, k, 0.f, h->head, h->gcap,
              h->slot_offset};
   a.inv_padded = true;  // the bank pads inv with one NaN tile
+  a.ibnd = h->ibnd;
   int slices = 1;
   if (topk_plan(h, a, algo, slices)) return 0;
   const bool wide = wide_on(h, wq);
@@ -746,6 +763,7 @@ static int topk_impl(ss_bank* h, const int8_t* q, const float* q_inv, int64_t nq
   TopkArgs a{q, q_inv, nq, h->emb, h->inv, h->cap, h->dim, k, theta, h->head, h->gcap,
              h->slot_offset};
   a.inv_padded = true;  // the bank pads inv with one NaN tile
+  a.ibnd = h->ibnd;
   a.qscratch = h->qscratch;
   int slices = 1;
   if (int rc = topk_plan(h, a, algo, slices)) return rc;
@@ -908,6 +926,7 @@ int ss_topk_partials(ss_bank_t* h, const int8_t* q, const float* q_inv, int64_t 
   TopkArgs a{q, q_inv, nq, h->emb, h->inv, h->cap, h->dim, k, theta, h->head, h->gcap,
              h->slot_offset};
   a.inv_padded = true;  // the bank pads inv with one NaN tile
+  a.ibnd = h->ibnd;
   a.gslots = gslots_reserve(h, nq, theta);
   a.qscratch = h->qscratch;
   int slices = 1;
@@ -1013,6 +1032,7 @@ static int round_impl(ss_bank* h, const int8_t* q, const float* q_inv, const int
   TopkArgs a{q, q_inv, nq, h->emb, h->inv, h->cap, h->dim, k, theta, h->head, h->gcap,
              h->slot_offset};
   a.inv_padded = true;  // the bank pads inv with one NaN tile
+  a.ibnd = h->ibnd;
   a.gslots = gslots_reserve(h, nq, theta);
   a.qscratch = h->qscratch;
   int slices = 1;
@@ -1213,7 +1233,7 @@ int bank_push_gather(ss_bank* h, const int8_t* src_emb, const float* src_inv,
   const int64_t skip = n > h->cap ? n - h->cap : 0;
   int rc = launch_bank_write(h->emb, h->inv, h->lens, h->seq, h->len_cnt, h->dim, src_emb, 1,
                              src_inv, src_lens, nullptr, nullptr, n, h->head, h->cap, skip,
-                             h->d_err, st, src_idx, h->wp.flag ? &h->wp : nullptr);
+                             h->d_err, st, src_idx, h->wp.flag ? &h->wp : nullptr, h->ibnd);
   if (rc) return rc;
   h->head += n;
   return SS_OK;

@@ -80,7 +80,7 @@ int launch_bank_write(int8_t* emb, float* inv, int32_t* lens, int64_t* seq, int3
                       const int32_t* src_lens, const int64_t* src_seq, const int64_t* src_slot,
                       int64_t n, int64_t first_seq, int64_t capacity, int64_t skip, int* err,
                       cudaStream_t st, const int64_t* src_idx = nullptr,
-                      const WidePlane* wp = nullptr);
+                      const WidePlane* wp = nullptr, float2* ibnd = nullptr);
 int launch_fallback_hist(const int32_t* len_cnt, int max_len, int nbins, int64_t* cnt,
                          int64_t* sv, int64_t* sv2, cudaStream_t st);
 
@@ -116,6 +116,10 @@ struct TopkArgs {
   // inv is followed by at least one tile (256 floats) of NaN padding, so a
   // whole tile's inverse norms may be bulk-copied (the bank allocates it so)
   bool inv_padded = false;
+  // per 16-row group of the bank: (max inverse norm or 0, min inverse norm or
+  // +inf) over its non-NaN rows, kept by every bank write (k_bank_bounds) and
+  // padded like inv; the TS kernel's per-16-column filter bounds
+  const float2* ibnd = nullptr;
   // optional [kMaxShareSlices][nq] scratch for the TS kernel's pure top-k
   // mode: every slice publishes the R-th best key it holds per query, and
   // every slice filters with the minimum over slices (a lower bound of the
