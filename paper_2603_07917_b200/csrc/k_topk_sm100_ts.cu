@@ -312,7 +312,8 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
           const float2* __restrict__ ibnd, int64_t n_rows,
           int dim, int stages, int k, float theta, int64_t hmod, int64_t gcap, int64_t slot_offset,
           int64_t tiles_per_slice, uint64_t* __restrict__ partials,
-          uint32_t* __restrict__ gslots, int rshare) {
+          uint32_t* __restrict__ gslots, int rshare, int* __restrict__ counts,
+          const int* __restrict__ resolved) {
   constexpr int A_COL = NACC * BN;
   constexpr int B_STAGE = BN * BK;
   constexpr int IS = ISLOTS;       // inverse-norm ring slots
@@ -349,6 +350,22 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
   const int64_t total_tiles = (n_rows + BN - 1) / BN;
   const int ntiles = (int)max((int64_t)0, min(total_tiles, tile0 + tiles_per_slice) - tile0);
 
+  // Pure top-k cascade, second pass: this query tile is done if every query
+  // already has >= k keys at or above the threshold pass's theta (their
+  // top-k lie above it, and the threshold pass's lists hold them); the CTA
+  // leaves before it allocates anything.
+  if (resolved) {
+    int need = 0;
+    for (int i = threadIdx.x; i < BM; i += blockDim.x) {
+      const int64_t qq = (int64_t)qt * BM + i;
+      if (qq < nq) {
+        int sum = 0;
+        for (int s2 = 0; s2 < (int)gridDim.y; ++s2) sum += resolved[(int64_t)s2 * nq + qq];
+        need |= sum < k;
+      }
+    }
+    if (!__syncthreads_or(need)) return;
+  }
   if (threadIdx.x == 0) {
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmB) : "memory");
     bar_init(a_full, 4);  // the 4 warps writing A into TMEM
@@ -629,6 +646,7 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
       uint64_t* out = partials + ((int64_t)slice * nq + q) * k;
       const int hc = s_hcnt[qrow];
       for (int i = 0; i < k; ++i) out[i] = (i < hc) ? heap[i * BM] : 0ull;
+      if (counts) counts[(int64_t)slice * nq + q] = hc;  // (pure top-k cascade, first pass)
     }
   }
   fence_before();
@@ -723,7 +741,7 @@ int topk_ts_lists(const TopkArgs& a, int device) {
 
 template <int BN>
 static int launch_ts_t(const TopkArgs& a, const TsShape& sh, int rshare, uint64_t* partials, int n_slices,
-                       cudaStream_t st) {
+                       cudaStream_t st, int* counts = nullptr, const int* resolved = nullptr) {
   auto enc = ts_encode();
   if (!enc) return set_error(SS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   CUtensorMap mb;
@@ -746,10 +764,23 @@ static int launch_ts_t(const TopkArgs& a, const TsShape& sh, int rshare, uint64_
   count_launch();
   kern<<<grid, ts::THREADS, sh.smem, st>>>(mb, a.q, a.q_inv, a.nq, a.inv, a.ibnd, a.n_rows, a.dim,
                                            sh.stages, a.k, a.theta, a.head % a.gcap, a.gcap, a.slot_offset, tps,
-                                           partials, a.gslots, rshare);
+                                           partials, a.gslots, rshare, counts, resolved);
   SS_LAUNCH_CHECK();
   return SS_OK;
 }
+
+// Pure top-k (theta <= 0) runs as a cascade when the bank's scratch is there:
+// (1) the threshold kernel at kCascadeTheta (the paper's similarity
+// threshold) writes every slice's list of keys >= it and their
+// counts; (2) the pure top-k kernel (bound sharing, SHARE) runs only for the
+// query tiles holding a query with fewer than k such keys in total -- the
+// other tiles exit at once.  Exact: a query with >= k keys at or above the
+// threshold has its whole top-k there, and each of those rows is in its
+// slice's top-k of keys >= the threshold, so the first pass's lists merge to
+// the same top-k.  When every query resolves (clustered prompts), pure top-k
+// costs the threshold pass plus an empty launch; when none does, the
+// threshold pass is overhead (~1/3 of the pure top-k kernel).
+constexpr float kCascadeTheta = 0.8f;
 
 int launch_topk_ts(const TopkArgs& a, uint64_t* partials, int n_lists, cudaStream_t st) {
   if (n_lists < 1) return set_error(SS_ERR_ARG, "ts: no slices");
@@ -760,8 +791,18 @@ int launch_topk_ts(const TopkArgs& a, uint64_t* partials, int n_lists, cudaStrea
     if (R <= 4) rshare = R;
   }
   const TsShape sh = ts_shape(a.dim, a.k, rshare > 0);
-  if (sh.bn == ts::BN) return launch_ts_t<ts::BN>(a, sh, rshare, partials, n_lists, st);
-  return set_error(SS_ERR_UNSUPPORTED, "ts: no shape fits shared memory");
+  if (sh.bn != ts::BN) return set_error(SS_ERR_UNSUPPORTED, "ts: no shape fits shared memory");
+  if (a.gslots && a.theta <= 0.f && n_lists <= kMaxShareSlices) {
+    // the bank's pure-top-k scratch: [kMaxShareSlices][nq] bounds, then
+    // [kMaxShareSlices][nq] per-slice counts
+    int* counts = reinterpret_cast<int*>(a.gslots + (size_t)kMaxShareSlices * a.nq);
+    TopkArgs a1 = a;
+    a1.theta = kCascadeTheta;
+    const TsShape sh1 = ts_shape(a.dim, a.k, false);
+    if (int rc = launch_ts_t<ts::BN>(a1, sh1, 0, partials, n_lists, st, counts, nullptr)) return rc;
+    return launch_ts_t<ts::BN>(a, sh, rshare, partials, n_lists, st, nullptr, counts);
+  }
+  return launch_ts_t<ts::BN>(a, sh, rshare, partials, n_lists, st);
 }
 
 }  // namespace ss

@@ -150,7 +150,7 @@ struct ss_bank {
 // simply disables the sharing.
 static uint32_t* gslots_reserve(ss_bank* h, int64_t nq, float theta) {
   if (!(theta <= 0.f)) return nullptr;
-  const int64_t need = nq * kMaxShareSlices;
+  const int64_t need = 2 * nq * kMaxShareSlices;  // bounds, then the cascade's per-slice counts
   if (need <= h->gslots_cap) return h->gslots;
   if (h->gslots) cudaFree(h->gslots);
   h->gslots = nullptr;

@@ -415,6 +415,46 @@ def test_topk_pure_large_bank_bit_exact(cuda, theta):
     _check_topk(w, comp, keys, seq, ref, 64)
 
 
+@pytest.mark.parametrize("theta", [-1.0, 0.0])
+def test_topk_pure_cascade_mixed_tiles(cuda, theta):
+    """Pure top-k runs as a cascade (a threshold pass, then the bound-sharing
+    pass only for query tiles with a query holding fewer than k keys >= the
+    threshold).  Queries from tight clusters (hundreds of rows >= 0.8) and
+    random queries (none) are interleaved so that every query tile mixes
+    resolved and unresolved queries, and one tile holds only cluster queries;
+    every top-k equals the oracle's."""
+    from paper_2603_07917_b200.history import HistoryWindow
+    rng = np.random.default_rng(5)
+    dim, ncl, per = 384, 8, 300
+    cent = rng.standard_normal((ncl, dim)).astype(np.float32)
+    cent /= np.linalg.norm(cent, axis=1, keepdims=True)
+
+    def quant(x):
+        x = x / np.linalg.norm(x, axis=1, keepdims=True)
+        return np.rint(127.0 * x / np.abs(x).max(axis=1, keepdims=True)).astype(np.int8)
+
+    def members(c, n):
+        z = rng.standard_normal((n, dim)).astype(np.float32)
+        z /= np.linalg.norm(z, axis=1, keepdims=True)
+        return quant(cent[c] + 0.2 * z)
+
+    bank = np.concatenate([members(c, per) for c in range(ncl)]
+                          + [quant(rng.standard_normal((30_000, dim)).astype(np.float32))])
+    bank = bank[rng.permutation(bank.shape[0])]
+    lens = rng.integers(1, 2000, bank.shape[0]).astype(np.int32)
+    w = HistoryWindow(bank.shape[0], dim)
+    w.push(bank, lens)
+    qc = np.concatenate([members(c % ncl, 1) for c in range(256)])          # resolved
+    qr = quant(rng.standard_normal((128, dim)).astype(np.float32))           # unresolved
+    mixed = np.empty((256, dim), np.int8)
+    mixed[0::2], mixed[1::2] = qc[:128], qr
+    q = np.concatenate([mixed, qc[128:]])  # tiles 0-1 mixed, tile 2 all resolved
+    qi = O.inv_norm(q)
+    keys, seq, ref = _oracle_topk(w, bank, q, qi, 64, theta)
+    comp, ln = w.topk(q, qi, 64, theta, "tcgen05")
+    _check_topk(w, comp, keys, seq, ref, 64)
+
+
 @pytest.mark.parametrize("algo", ["scan", "tcgen05"])
 def test_topk_edges(cuda, algo):
     """ragged nq (1 and 3: the streaming tcgen05 kernel; 129: the A-in-TMEM
