@@ -28,9 +28,13 @@ def main():
     I = np.random.default_rng(1).integers(1, 4097, 300).astype(np.int32)
     ok = True
     # nq = 300: k_topk_ts (theta 0.8: locked shared heaps; theta -1: the
-    # SHARE instantiation) + k_merge_finish_w + rank; nq = 64: k_topk_tc
-    for nq, theta in ((300, 0.8), (300, -1.0), (64, 0.8), (64, -1.0)):
-        q = emb[n:n + nq]
+    # pure top-k cascade -- threshold pass, then the SHARE instantiation for
+    # unresolved tiles, forced by random queries) + k_merge_finish_w + rank;
+    # nq = 64: k_topk_tc
+    rq = np.random.default_rng(2).integers(-60, 61, (300, 384)).astype(np.int8)
+    for nq, theta, rand in ((300, 0.8, False), (300, -1.0, False), (300, -1.0, True), (64, 0.8, False),
+                            (64, -1.0, False)):
+        q = rq[:nq] if rand else emb[n:n + nq]
         qi = O.inv_norm(q)
         cfg = RoundConfig(k=32, theta=theta, min_matches=20, nbins=64)
         perm, G, _ = SageScheduler(w, cfg).schedule_round(
@@ -41,7 +45,7 @@ def main():
         ref = O.predict_round(keys, np.arange(n), lens[:n], I[:nq], 32, theta, 20, 2048, 64,
                               window_lens=lens[:n])
         good = np.array_equal(G.cpu().numpy(), np.array([r["G"] for r in ref]))
-        print(f"nq={nq} theta={theta}: {'ok' if good else 'MISMATCH'}")
+        print(f"nq={nq} theta={theta}{' random queries' if rand else ''}: {'ok' if good else 'MISMATCH'}")
         ok &= good
     sys.exit(0 if ok else 1)
 
