@@ -44,7 +44,7 @@ k_topk_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUten
           const float* __restrict__ q_inv, int64_t nq, const float* __restrict__ inv,
           int64_t n_rows, int nkb, int stages, int k, float theta, int64_t hmod, int64_t gcap,
           int64_t slot_offset, int64_t tiles_per_slice, uint64_t* __restrict__ partials,
-          int spread) {
+          int spread, int* __restrict__ counts, const int* __restrict__ resolved) {
   constexpr int B_STAGE = tc::BN * tc::BK;     // bytes per K-block stage
   extern __shared__ uint8_t smem_raw[];
   // 1024-B alignment for the 128B-swizzle atoms; index the __shared__ array
@@ -68,6 +68,21 @@ k_topk_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUten
   const int64_t total_tiles = (n_rows + tc::BN - 1) / tc::BN;
   const int64_t tile1 = min(total_tiles, tile0 + tiles_per_slice);
   const int ntiles = (int)max((int64_t)0, tile1 - tile0);
+  // pure top-k cascade, second pass (see launch_topk_ts): leave at once when
+  // every query of this tile already holds >= k keys above the threshold
+  // pass's theta
+  if (resolved) {
+    int need = 0;
+    for (int i = threadIdx.x; i < tc::BM; i += blockDim.x) {
+      const int64_t qq = (int64_t)qt * tc::BM + i;
+      if (qq < nq) {
+        int sum = 0;
+        for (int s2 = 0; s2 < (int)gridDim.y; ++s2) sum += resolved[(int64_t)s2 * nq + qq];
+        need |= sum < k;
+      }
+    }
+    if (!__syncthreads_or(need)) return;
+  }
 
   if (threadIdx.x == 0) {
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmQ) : "memory");
@@ -262,6 +277,7 @@ k_topk_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUten
     if (q < nq) {
       uint64_t* out = partials + ((int64_t)slice * nq + q) * k;
       for (int i = 0; i < k; ++i) out[i] = (i < hcnt) ? heap[i * tc::BM] : 0ull;
+      if (counts) counts[(int64_t)slice * nq + q] = hcnt;  // (pure top-k cascade, first pass)
     }
   }
   tc_fence_before();
@@ -350,7 +366,8 @@ __global__ void k_spread_queries(const int8_t* __restrict__ q, int64_t nq, int d
   for (int j = threadIdx.x; j < dim / 16; j += blockDim.x) dst[j] = src[j];
 }
 
-static int launch_tc(const TopkArgs& a, uint64_t* partials, int n_slices, cudaStream_t st) {
+static int launch_tc(const TopkArgs& a, uint64_t* partials, int n_slices, cudaStream_t st,
+                     int* counts = nullptr, const int* resolved = nullptr) {
   const int stages = tc_stages(a.dim, a.k);
   if (stages < 2) return set_error(SS_ERR_UNSUPPORTED, "tcgen05: not enough shared memory");
   const size_t smem = tc_fixed_smem(a.dim, a.k) + (size_t)stages * tc::BN * tc::BK;
@@ -377,7 +394,7 @@ static int launch_tc(const TopkArgs& a, uint64_t* partials, int n_slices, cudaSt
   count_launch();
   k_topk_tc<<<dim3((unsigned)qtiles, (unsigned)n_slices), tc::THREADS, smem, st>>>(
       mq, mb, a.q_inv, a.nq, a.inv, a.n_rows, a.dim / tc::BK, stages, a.k, a.theta,
-      a.head % a.gcap, a.gcap, a.slot_offset, tps, partials, spread);
+      a.head % a.gcap, a.gcap, a.slot_offset, tps, partials, spread, counts, resolved);
   SS_LAUNCH_CHECK();
   return SS_OK;
 }
@@ -385,6 +402,15 @@ static int launch_tc(const TopkArgs& a, uint64_t* partials, int n_slices, cudaSt
 int launch_topk_tc(const TopkArgs& a, uint64_t* partials, int n_slices, cudaStream_t st) {
   if (!topk_tc_supported(a)) return set_error(SS_ERR_UNSUPPORTED, "tcgen05 path unsupported");
   if (use_ts(a)) return launch_topk_ts(a, partials, n_slices, st);
+  if (a.gslots && a.theta <= 0.f && n_slices <= kMaxShareSlices) {
+    // pure top-k as the threshold cascade (see launch_topk_ts); the counts
+    // live in the bank's pure-top-k scratch after the bound slots
+    int* counts = reinterpret_cast<int*>(a.gslots + (size_t)kMaxShareSlices * a.nq);
+    TopkArgs a1 = a;
+    a1.theta = kCascadeTheta;
+    if (int rc = launch_tc(a1, partials, n_slices, st, counts, nullptr)) return rc;
+    return launch_tc(a, partials, n_slices, st, nullptr, counts);
+  }
   return launch_tc(a, partials, n_slices, st);
 }
 

@@ -780,7 +780,6 @@ static int launch_ts_t(const TopkArgs& a, const TsShape& sh, int rshare, uint64_
 // the same top-k.  When every query resolves (clustered prompts), pure top-k
 // costs the threshold pass plus an empty launch; when none does, the
 // threshold pass is overhead (~1/3 of the pure top-k kernel).
-constexpr float kCascadeTheta = 0.8f;
 
 int launch_topk_ts(const TopkArgs& a, uint64_t* partials, int n_lists, cudaStream_t st) {
   if (n_lists < 1) return set_error(SS_ERR_ARG, "ts: no slices");

@@ -130,6 +130,9 @@ struct TopkArgs {
   int8_t* qscratch = nullptr;
 };
 constexpr int kMaxShareSlices = 160;
+// pure top-k cascade (launch_topk_ts / launch_topk_tc): the threshold pass's
+// theta -- the paper's similarity threshold
+constexpr float kCascadeTheta = 0.8f;
 int launch_topk_scan(const TopkArgs& a, uint64_t* partials, int n_slices, cudaStream_t st);
 int topk_scan_slices(const TopkArgs& a, int device);
 int launch_topk_tc(const TopkArgs& a, uint64_t* partials, int n_slices, cudaStream_t st);

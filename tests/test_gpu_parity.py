@@ -415,11 +415,12 @@ def test_topk_pure_large_bank_bit_exact(cuda, theta):
     _check_topk(w, comp, keys, seq, ref, 64)
 
 
+@pytest.mark.parametrize("layout", ["ts_mixed", "tc_mixed", "tc_resolved"])
 @pytest.mark.parametrize("theta", [-1.0, 0.0])
-def test_topk_pure_cascade_mixed_tiles(cuda, theta):
-    """Pure top-k runs as a cascade (a threshold pass, then the bound-sharing
+def test_topk_pure_cascade_mixed_tiles(cuda, theta, layout):
+    """Pure top-k runs as a cascade (a threshold pass, then the pure top-k
     pass only for query tiles with a query holding fewer than k keys >= the
-    threshold).  Queries from tight clusters (hundreds of rows >= 0.8) and
+    threshold), in both the A-in-TMEM kernel and the streaming kernel.  Queries from tight clusters (hundreds of rows >= 0.8) and
     random queries (none) are interleaved so that every query tile mixes
     resolved and unresolved queries, and one tile holds only cluster queries;
     every top-k equals the oracle's."""
@@ -448,7 +449,12 @@ def test_topk_pure_cascade_mixed_tiles(cuda, theta):
     qr = quant(rng.standard_normal((128, dim)).astype(np.float32))           # unresolved
     mixed = np.empty((256, dim), np.int8)
     mixed[0::2], mixed[1::2] = qc[:128], qr
-    q = np.concatenate([mixed, qc[128:]])  # tiles 0-1 mixed, tile 2 all resolved
+    if layout == "ts_mixed":    # 3 query tiles (A-in-TMEM kernel): 0-1 mixed, 2 all resolved
+        q = np.concatenate([mixed, qc[128:]])
+    elif layout == "tc_mixed":  # one tile (streaming kernel), mixed
+        q = mixed[:96]
+    else:                       # one tile, every query resolved by the threshold pass
+        q = qc[:64]
     qi = O.inv_norm(q)
     keys, seq, ref = _oracle_topk(w, bank, q, qi, 64, theta)
     comp, ln = w.topk(q, qi, 64, theta, "tcgen05")
