@@ -677,9 +677,16 @@ class CpuRound:
         self.n = C["n_bank"]
         emb, lens = make_bank_host(self.n, DIM, N_CLUSTERS, SEED)
         self.iw = O.inv_norm(emb)
-        # fp32 copy of the bank when it fits comfortably (c2: 1.6 GB); the 16M
-        # bank stays int8 (6.4 GB) and each chunk is widened inside the step
-        self.W = emb.astype(np.float32) if self.n <= (1 << 22) else emb
+        # fp32 copy of the bank when it fits in a third of the free host memory
+        # (c2: 1.6 GB; c4: 25.8 GB on a 196 GB box), else the int8 bank with
+        # each chunk widened inside the step (slower: the widening dominates)
+        try:
+            import psutil
+            avail = psutil.virtual_memory().available
+        except Exception:  # noqa: BLE001
+            avail = 0
+        fp32_bytes = emb.size * 4
+        self.W = emb.astype(np.float32) if (self.n <= (1 << 22) or fp32_bytes * 3 < avail) else emb
         self.lens = lens.astype(np.int64)
         self.fb = O.bin_hist(self.lens, MAX_LEN, NBINS)
         q, qi, I, ids = make_queries(C["nq"], DIM, N_CLUSTERS, SEED, qseed=1000)
