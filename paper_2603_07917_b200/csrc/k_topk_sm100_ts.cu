@@ -38,7 +38,10 @@ constexpr int BM = 128;          // queries (TMEM lanes)
 constexpr int BN = 192;          // bank rows per tile (UMMA N): 2 x 192 accumulator columns + A's dim / 4 <= 512
 constexpr int BK = 128;          // bytes per K-block (128B swizzle atom)
 constexpr int UK = 32;           // int8 K per MMA
-constexpr int EPW = 3;                // epilogue warps per TMEM lane quarter
+#ifndef SS_TS_EPW
+#define SS_TS_EPW 3
+#endif
+constexpr int EPW = SS_TS_EPW;        // epilogue warps per TMEM lane quarter (3: 64 columns each, 4: 48)
 constexpr int EPI_WARPS = 4 * EPW;    // 12
 constexpr int THREADS = 64 + EPI_WARPS * 32;
 constexpr int KMAX = 64;
@@ -165,6 +168,23 @@ __device__ __forceinline__ void wait_ld8(int (&v)[8]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;\n"
                : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]),
                  "+r"(v[7])
+               :
+               : "memory");
+}
+__device__ __forceinline__ void ld16_async(uint32_t taddr, int (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];\n"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void wait_ld16(int (&v)[16]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n"
+               : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]),
+                 "+r"(v[6]), "+r"(v[7]), "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]),
+                 "+r"(v[12]), "+r"(v[13]), "+r"(v[14]), "+r"(v[15])
                :
                : "memory");
 }
@@ -318,7 +338,8 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
   constexpr int B_STAGE = BN * BK;
   constexpr int IS = ISLOTS;       // inverse-norm ring slots
   constexpr int CW = BN / EPW;     // columns per epilogue warp per tile
-  static_assert(CW == 64, "tile shape: two 32-column chunks per epilogue warp");
+  static_assert(CW == 64 || CW == 48, "tile shape: 32 + 32 or 32 + 16 columns per epilogue warp");
+  constexpr int CW2 = CW - 32;     // the second chunk's columns
   constexpr uint32_t IDESC = idesc(BN);
   const int nkb = dim / BK;
   extern __shared__ uint8_t smem_raw[];
@@ -530,18 +551,20 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
       TRACE(0, t);
       // this warp's four 16-column filter bounds (hi0, lo0, hi1, lo1 per
       // 32-column chunk), precomputed per 16-row group by every bank write
-      const float4* cb = reinterpret_cast<const float4*>(s_inv + sl * 256 + BN) + grp * 2;
+      const float2* cb = reinterpret_cast<const float2*>(s_inv + sl * 256 + BN) + grp * (CW / 16);
       TRACE(1, t);
       bar_wait_epi(&tfull[acc], (t / NACC) & 1);
       TRACE(2, t);
       fence_after();
       const uint32_t tbase = tmem + lane_base + acc * BN + grp * CW;
       // pull my chunks into registers, then hand the accumulator back
-      int v0[32], v1[32];
+      int v0[32], v1[CW2];
       ld32_async(tbase, v0);
-      ld32_async(tbase + 32, v1);
+      if constexpr (CW2 == 32) ld32_async(tbase + 32, v1);
+      else ld16_async(tbase + 32, v1);
       wait_ld(v0);
-      wait_ld(v1);
+      if constexpr (CW2 == 32) wait_ld(v1);
+      else wait_ld16(v1);
       fence_before();
       __syncwarp();
       if (lane == 0) bar_arrive(RING ? &full[acc] : &tempty[acc]);  // accumulator free for tile t + 2
@@ -614,25 +637,31 @@ k_topk_ts(const __grid_constant__ CUtensorMap tmB, const int8_t* __restrict__ Q,
         }
       };
       auto chunk = [&](const auto& v, const int c) {
+        constexpr int W = sizeof(v) / sizeof(v[0]);  // 32, or 16 (the second chunk at CW = 48)
         const int a0 = __vimax3_s32(v[0], v[1], v[2]), a1 = __vimax3_s32(v[3], v[4], v[5]);
         const int a2 = __vimax3_s32(v[6], v[7], v[8]), a3 = __vimax3_s32(v[9], v[10], v[11]);
         const int a4 = __vimax3_s32(v[12], v[13], v[14]);
-        const int b0 = __vimax3_s32(v[16], v[17], v[18]), b1 = __vimax3_s32(v[19], v[20], v[21]);
-        const int b2 = __vimax3_s32(v[22], v[23], v[24]), b3 = __vimax3_s32(v[25], v[26], v[27]);
-        const int b4 = __vimax3_s32(v[28], v[29], v[30]);
         const int mdl = __vimax3_s32(__vimax3_s32(a0, a1, a2), __vimax3_s32(a3, a4, v[15]), a0);
-        const int mdh = __vimax3_s32(__vimax3_s32(b0, b1, b2), __vimax3_s32(b3, b4, v[31]), b0);
-        const float4 bc = cb[c];
-        const float bl = __fmul_rn(__int2float_rn(mdl), mdl >= 0 ? bc.x : bc.y);
-        const float bh = __fmul_rn(__int2float_rn(mdh), mdh >= 0 ? bc.z : bc.w);
-        if constexpr (SHARE) {
-          // pure top-k: many chunks pass while the bounds rise -- one exact
-          // pass (and one heap lock) per 32 columns is cheaper there
-          if (fmaxf(bl, bh) >= thr)
-            exact(v, c, std::integral_constant<int, 0>(), std::integral_constant<int, 32>());
+        const float2 b0 = cb[2 * c];
+        const float bl = __fmul_rn(__int2float_rn(mdl), mdl >= 0 ? b0.x : b0.y);
+        if constexpr (W == 32) {
+          const int b0_ = __vimax3_s32(v[16], v[17], v[18]), b1 = __vimax3_s32(v[19], v[20], v[21]);
+          const int b2 = __vimax3_s32(v[22], v[23], v[24]), b3 = __vimax3_s32(v[25], v[26], v[27]);
+          const int b4 = __vimax3_s32(v[28], v[29], v[30]);
+          const int mdh = __vimax3_s32(__vimax3_s32(b0_, b1, b2), __vimax3_s32(b3, b4, v[31]), b0_);
+          const float2 b1h = cb[2 * c + 1];
+          const float bh = __fmul_rn(__int2float_rn(mdh), mdh >= 0 ? b1h.x : b1h.y);
+          if constexpr (SHARE) {
+            // pure top-k: many chunks pass while the bounds rise -- one exact
+            // pass (and one heap lock) per 32 columns is cheaper there
+            if (fmaxf(bl, bh) >= thr)
+              exact(v, c, std::integral_constant<int, 0>(), std::integral_constant<int, 32>());
+          } else {
+            if (bl >= thr) exact(v, c, std::integral_constant<int, 0>(), std::integral_constant<int, 16>());
+            if (bh >= thr) exact(v, c, std::integral_constant<int, 16>(), std::integral_constant<int, 16>());
+          }
         } else {
           if (bl >= thr) exact(v, c, std::integral_constant<int, 0>(), std::integral_constant<int, 16>());
-          if (bh >= thr) exact(v, c, std::integral_constant<int, 16>(), std::integral_constant<int, 16>());
         }
       };
       chunk(v0, 0);
