@@ -331,6 +331,14 @@ def run_single(args):
                  "kernel": topk_kernel_name(SCAN_NQ), "nq": SCAN_NQ, "n_slices": scan_slices,
                  "kernel_ms": round(scan_ms, 4),
                  "traffic": ncu_traffic(args.config + "_scan8", topk_kernel_name(SCAN_NQ))}
+    # the north star's target shape (BASELINE configs[3]) on this one GPU
+    # (after the peak probes: its long run heats the part): the per-GPU
+    # similarity work of the 8-GPU configuration is 1/8 of it
+    c4 = None
+    if args.config == "c2" and not args.no_c4:
+        del graph, sched, win
+        torch.cuda.empty_cache()
+        c4 = c4_one_gpu(args)
     line = {
         "metric": METRIC, "value": round(nq * args.steps / (ms / 1e3), 1), "unit": "requests/s",
         "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
@@ -348,12 +356,56 @@ def run_single(args):
         "roofline": roof,
         "roofline_scan": roof_scan,
         "pure_topk": pure,
+        "c4_one_gpu": c4,
         "gpu_launches": int(per_round * args.steps),
         "clocks": clocks,
     }
     if not args.no_cpu_baseline and args.config == "c2":
         line["cpu_baseline"] = cpu_baseline(args.config, budget_s=args.cpu_budget)
     print(json.dumps(line), flush=True)
+
+
+def c4_one_gpu(args):
+    """The c4 round (16M x 384 bank, 8192 requests) on this GPU: graph-replayed
+    rounds and the similarity kernel alone, a few steps (a sub-record of the
+    default c2 line; `--config c4` gives the full line)."""
+    import torch
+
+    from paper_2603_07917_b200.history import HistoryWindow
+    from paper_2603_07917_b200.scheduler import RoundConfig, SageScheduler
+    from paper_2603_07917_b200.synthetic import make_bank_device, make_queries
+
+    C = CONFIGS["c4"]
+    n_bank, nq = C["n_bank"], C["nq"]
+    emb, lens, _ = make_bank_device(n_bank, DIM, N_CLUSTERS, SEED)
+    win = HistoryWindow(n_bank, DIM)
+    win.push(emb, lens)
+    del emb, lens
+    torch.cuda.empty_cache()
+    q, qi, I, ids = make_queries(nq, DIM, N_CLUSTERS, SEED, qseed=1000)
+    dq, dqi, dI, dids = (torch.as_tensor(x, device="cuda") for x in (q, qi, I, ids))
+    cfg = RoundConfig(k=K, theta=THETA, min_matches=MIN_MATCHES, max_len=MAX_LEN, nbins=NBINS)
+    sched = SageScheduler(win, cfg)
+    graph, _ = sched.capture_round(dq, dqi, dI, dids)
+    for _ in range(3):
+        graph.replay()
+    torch.cuda.synchronize()
+    steps = 5
+    sampler = ClockSampler(0)
+    with sampler:
+        t0 = time.time()
+        ms = time_ms(graph.replay, steps)
+        t1 = time.time()
+        clocks = sampler.summary(t0, t1)
+    kern_ms, n_slices = time_topk(win, dq, dqi, nq, THETA, 3)
+    out = {"workload": C["workload"], "value": round(nq / (ms / 1e3), 1), "unit": "requests/s",
+           "ms_per_step": round(ms, 3), "steps": steps, "kernel": topk_kernel_name(nq),
+           "kernel_ms": round(kern_ms, 3), "n_slices": n_slices,
+           "kernel_tops": round(2.0 * nq * n_bank * DIM / (kern_ms / 1e3) / 1e12, 1),
+           "clocks": clocks}
+    del graph, sched, win, dq, dqi, dI, dids
+    torch.cuda.empty_cache()
+    return out
 
 
 def time_e2e(sched, q, qi, I, ids, args):
@@ -803,6 +855,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-pure", action="store_true", help="skip the theta = -1 sub-record")
+    ap.add_argument("--no-c4", action="store_true", help="skip the c4-on-one-GPU sub-record")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--config", default=None, choices=["c2", "c3", "c4", "c5"],
                     help="c2 = headline at N = 1 (BASELINE configs[1]); c4 = 16M x 8192 "
