@@ -1060,11 +1060,12 @@ def test_topk_scatter_shards_equal_single_bank(cuda, world, algo):
                   0.5, 0, world, 0, tc, tl, _lib.stream_ptr())
 
 
-@pytest.mark.parametrize("mode", ["owner", "per-rank"])
+@pytest.mark.parametrize("mode", ["owner", "per-rank", "owner-coll"])
 def test_sharded_p2p_two_ranks_one_gpu(cuda, mode):
-    """World-2 round with the fused P2P merge + exchange, both ranks on cuda:0
-    (tests/_p2p_worker.py): the queue owner's result equals the single-GPU
-    round (single owner: rank 1 holds the whole queue)."""
+    """World-2 round, two processes on cuda:0 (tests/_p2p_worker.py), with the
+    fused P2P merge + exchange or (owner-coll) the collective exchange: the
+    queue owner's result equals the single-GPU round (single owner: rank 1
+    holds the whole queue)."""
     import pathlib
     import socket
     import subprocess
