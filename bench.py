@@ -230,6 +230,9 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # (ranks beyond the visible GPUs share them: the --backend gloo check of
+    # the multi-rank path on a one-GPU box)
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     sharded = world > 1 or args.sharded
     if sharded:
@@ -238,7 +241,10 @@ def run_ours(args):
                 s.bind(("127.0.0.1", 0))
                 os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(s.getsockname()[1]),
                                   RANK="0", WORLD_SIZE="1")
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        else:
+            dist.init_process_group("gloo")
     if rank == 0 and (_build.is_stale() or not os.path.exists(_build.LIB_PATH)):
         _build.build()
     if sharded:
@@ -459,6 +465,8 @@ def run_sharded(args, world, rank, local):
     per_round = _lib.launch_count() - c0
     graph = None
     try:
+        if args.backend == "gloo":  # gloo collectives cannot be captured into a CUDA graph
+            raise RuntimeError("gloo backend")
         graph, _ = sched.capture_round(*args_round, nq=nq)
     except Exception as e:  # noqa: BLE001
         print(f"sharded round not captured ({type(e).__name__}: {e}); timing eager rounds",
@@ -862,6 +870,9 @@ def main():
                          "(default at N > 1); c3 = refresh storm; c5 = rolling replay")
     ap.add_argument("--sharded", action="store_true",
                     help="run the multi-GPU single-owner round even at N = 1")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="torch.distributed backend of the sharded round (gloo: a functional check "
+                         "of the multi-rank path with several ranks sharing one GPU; not a measurement)")
     ap.add_argument("--exchange", default="nccl", choices=["nccl", "p2p"],
                     help="candidate exchange of the sharded round")
     args = ap.parse_args()

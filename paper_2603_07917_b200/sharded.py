@@ -422,11 +422,17 @@ class ShardedScheduler:
             for d, x in zip(dev, t):
                 d.copy_(x)
             args = self._round_args(dev, has_ids, nq)
-            try:
-                g, res = self.capture_round(*args[0], **args[1])
-            except Exception:  # noqa: BLE001 -- NCCL without graph support: eager rounds
-                torch.cuda.synchronize()
-                g, res = None, None
+            g, res = None, None
+            # only NCCL collectives can be captured (a gloo group -- the
+            # several-ranks-on-one-GPU checks -- runs the round eagerly: a
+            # capture attempt would run some of its collectives on one rank
+            # and not the other)
+            if dist.get_backend(self.group) == "nccl":
+                try:
+                    g, res = self.capture_round(*args[0], **args[1])
+                except Exception:  # noqa: BLE001 -- NCCL without graph support: eager rounds
+                    torch.cuda.synchronize()
+                    g, res = None, None
             st = self._host[key] = (dev, g, res)
         dev, g, res = st
         for d, x in zip(dev, t):
