@@ -394,6 +394,37 @@ def test_topk_multi_tile_ring_wrap(cuda, algo, theta):
         assert np.array_equal(ln[i, :m], lens[seqs[sel]]), i
 
 
+@pytest.mark.parametrize("theta", [0.8, -1.0])
+def test_topk_after_small_pushes(cuda, theta):
+    """The bank's per-16-row filter bounds (rewritten after every write) stay
+    exact when pushes of odd sizes rewrite parts of 16-row groups and the
+    ring wraps several times: TS-kernel top-k equals the oracle's."""
+    from paper_2603_07917_b200.history import HistoryWindow
+    cap, dim, nq, k = 20_000, 384, 200, 32
+    n = 3 * cap + 777
+    emb, lens, _, _ = O.make_bank(n + nq, dim, 60, 8)
+    w = HistoryWindow(cap, dim)
+    rng = np.random.default_rng(4)
+    pos = 0
+    while pos < n:
+        m = int(min(n - pos, rng.integers(1, 700)))
+        w.push(emb[pos:pos + m], lens[pos:pos + m])
+        pos += m
+    q = emb[n:]
+    qi = O.inv_norm(q)
+    seqs = np.arange(n - cap, n)
+    bank_e = emb[n - cap:n]
+    keys = O.scores(q, qi, bank_e, O.inv_norm(bank_e))
+    ref = [O.select_topk(keys[i], seqs, k, theta) for i in range(nq)]
+    comp, ln = w.topk(q, qi, k, theta, "tcgen05")
+    key, gseq, _ = w.decode(comp)
+    key, gseq = key.cpu().numpy(), gseq.cpu().numpy()
+    for i, sel in enumerate(ref):
+        m = sel.size
+        assert np.array_equal(gseq[i, :m], seqs[sel]), i
+        assert np.array_equal(key[i, :m], keys[i, sel]), i
+
+
 @pytest.mark.parametrize("theta", [0.8, 0.3, 0.0, -1.0])
 def test_topk_large_batch_tcgen05(cuda, theta):
     """nq = 1024 (the A-in-TMEM kernel with its integer pre-filter for
