@@ -340,11 +340,12 @@ def run_single(args):
     # the north star's target shape (BASELINE configs[3]) on this one GPU
     # (after the peak probes: its long run heats the part): the per-GPU
     # similarity work of the 8-GPU configuration is 1/8 of it
-    c4 = None
+    c4 = sweep = None
     if args.config == "c2" and not args.no_c4:
         del graph, sched, win
         torch.cuda.empty_cache()
         c4 = c4_one_gpu(args)
+        sweep = vs_bank_size(args)
     line = {
         "metric": METRIC, "value": round(nq * args.steps / (ms / 1e3), 1), "unit": "requests/s",
         "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
@@ -363,6 +364,7 @@ def run_single(args):
         "roofline_scan": roof_scan,
         "pure_topk": pure,
         "c4_one_gpu": c4,
+        "vs_bank_size": sweep,
         "gpu_launches": int(per_round * args.steps),
         "clocks": clocks,
     }
@@ -412,6 +414,39 @@ def c4_one_gpu(args):
     del graph, sched, win, dq, dqi, dI, dids
     torch.cuda.empty_cache()
     return out
+
+
+def vs_bank_size(args, sizes=(1 << 16, 1 << 18, 1 << 20, 1 << 22, 1 << 24)):
+    """BASELINE's metric is requests scheduled/s per round *vs bank size*: the
+    c2 round (1024 prompts, k 64, 128 bins, theta 0.8) over banks of 64k ..
+    16M rows, graph-replayed, five rounds each."""
+    import torch
+
+    from paper_2603_07917_b200.history import HistoryWindow
+    from paper_2603_07917_b200.scheduler import RoundConfig, SageScheduler
+    from paper_2603_07917_b200.synthetic import make_bank_device, make_queries
+
+    nq = CONFIGS["c2"]["nq"]
+    emb, lens, _ = make_bank_device(max(sizes), DIM, N_CLUSTERS, SEED)
+    q, qi, I, ids = make_queries(nq, DIM, N_CLUSTERS, SEED, qseed=1000)
+    dq, dqi, dI, dids = (torch.as_tensor(x, device="cuda") for x in (q, qi, I, ids))
+    cfg = RoundConfig(k=K, theta=THETA, min_matches=MIN_MATCHES, max_len=MAX_LEN, nbins=NBINS)
+    out = []
+    for n in sizes:
+        win = HistoryWindow(n, DIM)
+        win.push(emb[:n], lens[:n])
+        sched = SageScheduler(win, cfg)
+        graph, _ = sched.capture_round(dq, dqi, dI, dids)
+        for _ in range(3):
+            graph.replay()
+        ms = time_ms(graph.replay, 5)
+        out.append({"bank_rows": n, "ms_per_step": round(ms, 4), "value": round(nq / (ms / 1e3), 1),
+                    "unit": "requests/s"})
+        del graph, sched, win
+        torch.cuda.empty_cache()
+    del emb, lens
+    torch.cuda.empty_cache()
+    return {"nq": nq, "k": K, "nbins": NBINS, "theta": THETA, "points": out}
 
 
 def time_e2e(sched, q, qi, I, ids, args):
