@@ -376,4 +376,41 @@ int launch_cost_dist(int kind, double w_in, double w_out, const double* I, const
   return SS_OK;
 }
 
+
+// ---------------------------------------------------------------------------
+// host-buffer round inputs read straight from mapped pinned host memory: one
+// kernel for up to kGatherSegs (src, dst, bytes) segments instead of one
+// copy-engine node each (a small H2D copy node costs ~4 us of the plugin
+// call; scripts/probe_e2e.py).  16-byte loads when both ends allow.
+// ---------------------------------------------------------------------------
+__global__ void k_h2d_gather(GatherSegs g) {
+  for (int s = 0; s < g.n; ++s) {
+    const unsigned char* src = static_cast<const unsigned char*>(g.src[s]);
+    unsigned char* dst = static_cast<unsigned char*>(g.dst[s]);
+    const int64_t nb = g.bytes[s];
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nt = (int64_t)gridDim.x * blockDim.x;
+    if ((((uintptr_t)src | (uintptr_t)dst) & 15) == 0) {
+      const int64_t n16 = nb >> 4;
+      for (int64_t i = tid; i < n16; i += nt)
+        reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(src)[i];
+      for (int64_t i = (n16 << 4) + tid; i < nb; i += nt) dst[i] = src[i];
+    } else {
+      for (int64_t i = tid; i < nb; i += nt) dst[i] = src[i];
+    }
+  }
+}
+
+int launch_h2d_gather(const GatherSegs& g, cudaStream_t st) {
+  int64_t total = 0;
+  for (int s = 0; s < g.n; ++s) total += g.bytes[s];
+  if (total <= 0) return SS_OK;
+  int blocks = (int)((total / 16 + 255) / 256);
+  blocks = blocks < 1 ? 1 : (blocks > 148 ? 148 : blocks);
+  count_launch();
+  k_h2d_gather<<<blocks, 256, 0, st>>>(g);
+  SS_LAUNCH_CHECK();
+  return SS_OK;
+}
+
 }  // namespace ss

@@ -55,6 +55,14 @@ static_assert(sizeof(PerCallHdr) == 64, "per-call header is 64 bytes");
 constexpr int64_t kPerCallMaxPts = 2048;  // 2 x 2048 doubles of inputs = 32 KB of shared memory
 int launch_gittins_percall(PerCallHdr* h_dev, int64_t n, uint32_t seq, cudaStream_t st);
 int launch_cost_percall(PerCallHdr* h_dev, uint32_t seq, cudaStream_t st);
+constexpr int kGatherSegs = 4;
+struct GatherSegs {  // (src, dst, bytes) triples, by value as a kernel parameter
+  const void* src[kGatherSegs];
+  void* dst[kGatherSegs];
+  int64_t bytes[kGatherSegs];
+  int n;
+};
+int launch_h2d_gather(const GatherSegs& g, cudaStream_t st);
 int launch_gittins_dist(const double* support, const double* masses, const int64_t* npts,
                         const double* attained, const double* outlived, int64_t n,
                         int64_t stride, double* out, int* err, int ref_mode, cudaStream_t st);

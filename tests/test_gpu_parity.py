@@ -712,6 +712,47 @@ def test_round_host_graph_replay(cuda):
         assert np.array_equal(G, Gc) and np.array_equal(perm, pc), it
 
 
+def test_round_host_input_paths(cuda):
+    """The host-buffer call reads pinned inputs with one gather kernel and
+    pageable ones with copies: both, with and without ids, and pinned views
+    that are not 16-byte aligned (ragged nq), give the same G and order."""
+    from paper_2603_07917_b200.history import HistoryWindow
+    from paper_2603_07917_b200.scheduler import RoundConfig, SageScheduler
+    n, nq = 8_000, 301
+    emb, lens, _, _ = O.make_bank(n + nq, 384, 100, 21)
+    w = HistoryWindow(n, 384)
+    w.push(emb[:n], lens[:n])
+    q = emb[n:]
+    qi = O.inv_norm(q)
+    I = np.random.default_rng(5).integers(1, 4097, nq).astype(np.int32)
+    ids = np.arange(nq, dtype=np.int64)[::-1].copy()
+    s = SageScheduler(w, RoundConfig(k=32, theta=0.8, min_matches=20, max_len=2048, nbins=64))
+
+    def pinned(a, off=0):
+        # a pinned copy of a starting `off` bytes into a pinned block
+        b = torch.empty(a.nbytes + 64, dtype=torch.uint8).pin_memory().numpy()
+        v = b[off:off + a.nbytes].view(a.dtype).reshape(a.shape)
+        v[:] = a
+        return v
+
+    ref_p, ref_G = s.schedule_round_host(q, qi, I, ids)  # pageable: copy-engine path
+    ref_G, ref_p = ref_G.copy(), ref_p.copy()
+    for off in (0, 4):
+        for with_ids in (True, False):
+            args = [pinned(q, off), pinned(qi, off), pinned(I, off), pinned(ids, 8 if off else 0)]
+            if not with_ids:
+                args[3] = None
+            G = pinned(np.zeros(nq)); perm = pinned(np.zeros(nq, dtype=np.int64))
+            for _ in range(3):  # eager, eager, captured replay
+                G[:] = 0
+                s.schedule_round_host(*args, G, perm)
+                assert np.array_equal(G, ref_G), (off, with_ids)
+                if with_ids:
+                    assert np.array_equal(perm, ref_p), (off, with_ids)
+                else:
+                    assert np.array_equal(np.sort(perm), np.arange(nq))
+
+
 def test_round_fallback_and_cold_start(cuda):
     from paper_2603_07917_b200 import _lib
     from paper_2603_07917_b200.history import HistoryWindow
