@@ -57,36 +57,57 @@ __device__ __forceinline__ int block_excl_scan_i32(int v, int* s_warp, int* tota
   return pre;
 }
 
-// 1. progress of the last batch; completions compacted in batch order
+// 1. progress of the last batch; completions compacted in batch order.  The
+// batch carries each request's table row from the pack (the table has not
+// moved since); a row whose id does not match falls back to a binary search
+// of the id-sorted table.  EG_ITEMS consecutive batch entries per thread
+// with their loads in flight, one block scan per EG_THREADS * EG_ITEMS.
+constexpr int EG_ITEMS = 8;
 __global__ void __launch_bounds__(EG_THREADS)
-k_progress(const int64_t* __restrict__ run_ids, const int32_t* __restrict__ run_count,
-           const int64_t* __restrict__ ids, int64_t n, int32_t* __restrict__ g, int tok,
-           const int32_t* __restrict__ true_len, int64_t* __restrict__ done_ids,
-           uint8_t* __restrict__ drop, int32_t* __restrict__ n_done) {
+k_progress(const int64_t* __restrict__ run_ids, const int64_t* __restrict__ run_rows,
+           const int32_t* __restrict__ run_count, const int64_t* __restrict__ ids, int64_t n,
+           int32_t* __restrict__ g, int tok, const int32_t* __restrict__ true_len,
+           int64_t* __restrict__ done_ids, uint8_t* __restrict__ drop, int32_t* __restrict__ n_done) {
   __shared__ int s_warp[32];
   const int cnt = max(*run_count, 0);
   int carry = 0;
-  for (int base = 0; base < cnt; base += EG_THREADS) {
-    const int i = base + threadIdx.x;
-    bool done = false;
-    int64_t id = -1;
-    if (i < cnt && n > 0) {
-      id = run_ids[i];
-      int64_t lo = 0, hi = n;  // lower_bound in the id-sorted table
-      while (lo < hi) {
-        const int64_t mid = (lo + hi) >> 1;
-        if (ids[mid] < id) lo = mid + 1; else hi = mid;
+  for (int base = 0; base < cnt; base += EG_THREADS * EG_ITEMS) {
+    const int i0 = base + threadIdx.x * EG_ITEMS;
+    int64_t id[EG_ITEMS], row[EG_ITEMS];
+#pragma unroll
+    for (int j = 0; j < EG_ITEMS; ++j) {
+      const bool v = i0 + j < cnt && n > 0;
+      id[j] = v ? run_ids[i0 + j] : -1;
+      row[j] = v ? run_rows[i0 + j] : -1;
+    }
+    int nd = 0;
+    bool done[EG_ITEMS];
+#pragma unroll
+    for (int j = 0; j < EG_ITEMS; ++j) {
+      done[j] = false;
+      if (id[j] < 0) continue;
+      int64_t r = row[j];
+      if (r < 0 || r >= n || ids[r] != id[j]) {  // lower_bound in the id-sorted table
+        int64_t lo = 0, hi = n;
+        while (lo < hi) {
+          const int64_t mid = (lo + hi) >> 1;
+          if (ids[mid] < id[j]) lo = mid + 1; else hi = mid;
+        }
+        r = (lo < n && ids[lo] == id[j]) ? lo : -1;
       }
-      if (lo < n && ids[lo] == id) {
-        const int gn = g[lo] + tok;
-        g[lo] = gn;
-        done = gn >= true_len[id];
-        if (done) drop[lo] = 1;
+      if (r >= 0) {
+        const int gn = g[r] + tok;
+        g[r] = gn;
+        done[j] = gn >= true_len[id[j]];
+        if (done[j]) drop[r] = 1;
       }
+      nd += done[j];
     }
     int tot;
-    const int pos = block_excl_scan_i32(done ? 1 : 0, s_warp, &tot);
-    if (done) done_ids[carry + pos] = id;
+    int pos = carry + block_excl_scan_i32(nd, s_warp, &tot);
+#pragma unroll
+    for (int j = 0; j < EG_ITEMS; ++j)
+      if (done[j]) done_ids[pos++] = id[j];
     carry += tot;
   }
   if (threadIdx.x == 0) *n_done = carry;
@@ -97,14 +118,24 @@ __global__ void __launch_bounds__(EG_THREADS)
 k_keep_scan(uint8_t* __restrict__ drop, int64_t n, int64_t* __restrict__ pos) {
   __shared__ int s_warp[32];
   int64_t carry = 0;
-  for (int64_t base = 0; base < n; base += EG_THREADS) {
-    const int64_t i = base + threadIdx.x;
-    const bool keep = i < n && !drop[i];
+  for (int64_t base = 0; base < n; base += EG_THREADS * EG_ITEMS) {
+    const int64_t i0 = base + threadIdx.x * EG_ITEMS;  // EG_ITEMS consecutive rows per thread
+    bool keep[EG_ITEMS];
+    int nk = 0;
+#pragma unroll
+    for (int j = 0; j < EG_ITEMS; ++j) {
+      keep[j] = i0 + j < n && !drop[i0 + j];
+      nk += keep[j];
+    }
     int tot;
-    const int p = block_excl_scan_i32(keep ? 1 : 0, s_warp, &tot);
-    if (i < n) {
-      pos[i] = keep ? carry + p : -1;
-      drop[i] = 0;
+    int64_t p = carry + block_excl_scan_i32(nk, s_warp, &tot);
+#pragma unroll
+    for (int j = 0; j < EG_ITEMS; ++j) {
+      if (i0 + j < n) {
+        pos[i0 + j] = keep[j] ? p : -1;
+        drop[i0 + j] = 0;
+      }
+      p += keep[j];
     }
     carry += tot;
   }
@@ -288,7 +319,7 @@ int ss_engine_round(ss_table_t* t, ss_bank_t* h, const int8_t* tr_emb, const flo
   int64_t n = t->n_act;
   // 1. progress of the last batch
   count_launch();
-  k_progress<<<1, EG_THREADS, 0, st>>>(t->run_ids, t->count, t->buf[t->cur].ids, n,
+  k_progress<<<1, EG_THREADS, 0, st>>>(t->run_ids, t->batch, t->count, t->buf[t->cur].ids, n,
                                        t->buf[t->cur].g, tokens_per_round, tr_true_len,
                                        t->done_ids, t->drop, t->d_ndone);
   SS_LAUNCH_CHECK();

@@ -27,6 +27,7 @@
 namespace ss {
 
 constexpr int PK_THREADS = 1024;
+constexpr int PK_ITEMS = 8;
 
 // exclusive prefix of v over the block; *total = block sum.  All threads call.
 __device__ __forceinline__ long long block_excl_scan(long long v, long long* s_warp,
@@ -63,6 +64,7 @@ k_pack_batch(const int64_t* __restrict__ perm, const int32_t* __restrict__ I,
              int64_t* __restrict__ out_tokens) {
   __shared__ long long s_warp[32];
   __shared__ long long s_bad;
+  __shared__ long long s_used;
   __shared__ int s_first;
   const int tid = threadIdx.x;
   if (tid == 0) s_bad = LLONG_MAX;
@@ -79,6 +81,50 @@ k_pack_batch(const int64_t* __restrict__ perm, const int32_t* __restrict__ I,
   }
   long long R = K;  // remaining KV budget (block-uniform)
   int cnt = 0;      // admitted so far (block-uniform)
+  if (mode == 0) {
+    // cut form: PK_ITEMS consecutive ranked requests per thread, all their
+    // loads in flight, one block scan per PK_THREADS * PK_ITEMS requests;
+    // projected tokens are >= 1, so the admitted set is a prefix
+    for (int64_t base = 0; base < n && cnt < B; base += (int64_t)PK_THREADS * PK_ITEMS) {
+      const int64_t i0 = base + (int64_t)tid * PK_ITEMS;
+      int64_t rv[PK_ITEMS];
+      long long tv[PK_ITEMS];
+#pragma unroll
+      for (int j = 0; j < PK_ITEMS; ++j) rv[j] = (i0 + j < n) ? perm[i0 + j] : -1;
+      long long loc = 0;
+#pragma unroll
+      for (int j = 0; j < PK_ITEMS; ++j) {
+        tv[j] = rv[j] >= 0 ? (long long)I[rv[j]] + (long long)g[rv[j]] + 1 : 0;
+        loc += tv[j];
+      }
+      long long tot;
+      if (tid == 0) s_used = 0;  // published by the block scans' barriers
+      long long run = block_excl_scan(loc, s_warp, &tot);
+      int myok = 0;
+      long long last = 0;
+#pragma unroll
+      for (int j = 0; j < PK_ITEMS; ++j) {
+        run += tv[j];
+        const bool ok = rv[j] >= 0 && run <= R && (i0 + j - base) < (int64_t)(B - cnt);
+        if (ok) {
+          out_batch[cnt + (i0 + j - base)] = rv[j];
+          ++myok;
+          last = run;
+        }
+      }
+      long long nok;
+      block_excl_scan(myok, s_warp, &nok);
+      // tokens admitted = the prefix at the last admitted request (the
+      // largest admitted prefix: prefixes increase)
+      if (myok) atomicMax(&s_used, last);
+      __syncthreads();
+      const long long used = s_used;
+      __syncthreads();
+      R -= used;
+      cnt += (int)nok;
+      if (nok < min((int64_t)PK_THREADS * PK_ITEMS, n - base)) break;
+    }
+  } else
   for (int64_t base = 0; base < n && cnt < B; base += PK_THREADS) {
     const int64_t i = base + tid;
     const bool live = i < n;

@@ -960,7 +960,7 @@ def test_c3_refresh_storm_full_size(cuda):
         assert Gh[i] == O.gittins_points(c, D, int(I[i]), int(g[i])), i
 
 
-@pytest.mark.parametrize("n", [1, 7, 1024, 4096, 4097, 8192, 8193, 20_000, 200_000, 1_000_003])
+@pytest.mark.parametrize("n", [1, 7, 1024, 4096, 4097, 5120, 5121, 6000, 8192, 8193, 20_000, 200_000, 1_000_003])
 def test_rank_bit_exact(cuda, n):
     from paper_2603_07917_b200.scheduler import rank
     rng = np.random.default_rng(n)
@@ -976,7 +976,7 @@ def test_rank_bit_exact(cuda, n):
     assert np.array_equal(perm, O.rank(G, sids))
 
 
-@pytest.mark.parametrize("n", [3001, 50_000])
+@pytest.mark.parametrize("n", [3001, 7001, 50_000])
 def test_rank_special_values(cuda, n):
     """inf (no law yet), zero, wide exponent range, negative and > 2^32 ids
     (counting rank and onesweep)."""
@@ -1192,7 +1192,8 @@ def test_ipc_buffer_cross_process(cuda, tmp_path):
 @pytest.mark.parametrize("mode", ["cut", "skip"])
 @pytest.mark.parametrize("n,K,B", [(0, 8192, 64), (1, 8192, 64), (7, 20, 3), (1024, 8192, 64),
                                    (3000, 60_000, 2000), (5000, 8192, 4096),
-                                   (200_000, 8192, 64), (200_000, 1 << 40, 5000)])
+                                   (200_000, 8192, 64), (200_000, 1 << 40, 5000),
+                                   (20_000, 1 << 40, 20_000), (9000, 5_000_000, 9000)])
 def test_pack_batch_bit_exact(cuda, mode, n, K, B):
     from paper_2603_07917_b200.scheduler import pack_batch
     rng = np.random.default_rng(n + B)
