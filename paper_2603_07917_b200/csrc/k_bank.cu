@@ -213,9 +213,7 @@ k_fallback_hist(const int32_t* __restrict__ len_cnt, int max_len, int nbins,
 int launch_fallback_hist(const int32_t* len_cnt, int max_len, int nbins, int64_t* cnt, int64_t* sv,
                          int64_t* sv2, cudaStream_t st) {
   size_t smem = (size_t)3 * nbins * sizeof(unsigned long long);
-  if (smem > 48 * 1024)
-    SS_CUDA_TRY(cudaFuncSetAttribute(k_fallback_hist, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem));
+  SS_CUDA_TRY(ensure_dyn_smem(k_fallback_hist, smem));
   count_launch();
   k_fallback_hist<<<1, FB_THREADS, smem, st>>>(len_cnt, max_len, nbins, cnt, sv, sv2);
   SS_LAUNCH_CHECK();

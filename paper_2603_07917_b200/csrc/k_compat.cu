@@ -76,8 +76,7 @@ int launch_match_pmfs(const float* sims, int64_t nq, int64_t nw, const int64_t* 
                       int64_t* sizes, int64_t out_stride, int* err, cudaStream_t st) {
   size_t smem = (size_t)(max_len + 1) * sizeof(int);
   if (smem > 200 * 1024) return set_error(SS_ERR_UNSUPPORTED, "max_len %lld too large", (long long)max_len);
-  if (smem > 48 * 1024)
-    SS_CUDA_TRY(cudaFuncSetAttribute(k_match_pmfs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  SS_CUDA_TRY(ensure_dyn_smem(k_match_pmfs, smem));
   count_launch();
   k_match_pmfs<<<(unsigned)nq, 256, smem, st>>>(sims, nw, lens, theta, (int)max_len, sup, mas,
                                                  sizes, out_stride, err);
@@ -322,12 +321,10 @@ int launch_embed(const int64_t* tokens, const int64_t* offsets, int64_t n, uint6
   unsigned grid = (unsigned)((n + 3) / 4);
   count_launch();
   if (out_i16) {
-    if (smem > 48 * 1024)
-      SS_CUDA_TRY(cudaFuncSetAttribute(k_embed<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    SS_CUDA_TRY(ensure_dyn_smem(k_embed<true>, smem));
     k_embed<true><<<grid, 128, smem, st>>>(tokens, offsets, n, salt, dim, nullptr, out_i16, out_inv, err);
   } else {
-    if (smem > 48 * 1024)
-      SS_CUDA_TRY(cudaFuncSetAttribute(k_embed<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    SS_CUDA_TRY(ensure_dyn_smem(k_embed<false>, smem));
     k_embed<false><<<grid, 128, smem, st>>>(tokens, offsets, n, salt, dim, out_f64, nullptr, nullptr, err);
   }
   SS_LAUNCH_CHECK();

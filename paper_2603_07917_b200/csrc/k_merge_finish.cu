@@ -85,10 +85,193 @@ static size_t merge_smem(int nlists, int k, int kpad) {
   return (size_t)nlists * k * 12 + (size_t)kpad * 12;
 }
 
+// ---------------------------------------------------------------------------
+// warp-per-query merge (the shard / slice merge for nlists * k <= MW_MAX_M):
+// the same result as k_merge -- the top-k composites sorted descending,
+// 0-padded, each with its payload (carried length, or the bank length looked
+// up for the winners) -- without block barriers.  A block per query spends
+// most of its time in __syncthreads at the c4 owner's 8 x 64 candidates per
+// query; a warp per query keeps 8192 queries in one short wave.
+//   1. candidates + payloads -> per-warp smem; tau = max over full lists of
+//      their minimum (the k-th best is >= it, any list order); survivors
+//      (>= tau) compacted in place with ballots
+//   2. k-th largest: MSB-first 8-bit radix select on the high 32 bits (the
+//      key), bitwise on the low 32 bits only if the key is tied at the boundary
+//   3. winners ranked by counting (composites are unique) -> output slots
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int warp_sum_i32(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+constexpr int MW_WARPS = 4;
+constexpr int MW_MAX_M = 2048;  // 24 KB of candidates per warp
+
+__global__ void __launch_bounds__(MW_WARPS * 32)
+k_merge_w(const uint64_t* __restrict__ comp, const int32_t* __restrict__ len, int nlists,
+          int64_t nq, int k, uint64_t* __restrict__ out_comp, int32_t* __restrict__ out_len,
+          const int32_t* __restrict__ bank_lens, int64_t head, int64_t gcap, int64_t slot_offset,
+          PeerOut po, size_t warp_bytes) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t q = (int64_t)blockIdx.x * MW_WARPS + warp;
+  pdl_wait();  // the producing kernel's lists
+  if (q >= nq) return;  // warp-uniform; no block barriers below
+  const int M = nlists * k;
+  uint64_t* cand = reinterpret_cast<uint64_t*>(smem + warp * warp_bytes);  // [M]
+  int32_t* cpay = reinterpret_cast<int32_t*>(cand + M);                    // [M]
+  __shared__ int whist_all[MW_WARPS][256];
+  int* whist = whist_all[warp];
+  const unsigned lt = (1u << lane) - 1u;
+
+  // 1. load (lists are [nlists][nq][k]); per list its minimum and whether it
+  // is full (k non-zero entries) -> tau
+  uint64_t tau = 1ull;
+  for (int l = 0; l < nlists; ++l) {
+    const int64_t src = ((int64_t)l * nq + q) * k;
+    uint64_t mn = ~0ull;
+    for (int j = lane; j < k; j += 32) {
+      const uint64_t c = __ldcs(comp + src + j);
+      cand[l * k + j] = c;
+      if (len) cpay[l * k + j] = __ldcs(len + src + j);
+      mn = min(mn, c);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    if (mn != 0ull) tau = max(tau, mn);  // no zero entry: the list is full
+  }
+  __syncwarp();
+  int m1 = 0;
+  for (int i0 = 0; i0 < M; i0 += 32) {
+    const int i = i0 + lane;
+    const uint64_t c = (i < M) ? cand[i] : 0ull;
+    const int32_t p = (i < M && len) ? cpay[i] : 0;
+    const bool keep = c != 0ull && c >= tau;
+    const unsigned b = __ballot_sync(0xffffffffu, keep);
+    __syncwarp();
+    if (keep) {
+      cand[m1 + __popc(b & lt)] = c;
+      cpay[m1 + __popc(b & lt)] = p;
+    }
+    m1 += __popc(b);
+    __syncwarp();
+  }
+  // 2. k-th largest: T with |{c >= T}| = min(k, m1)
+  uint64_t T = 1ull;
+  if (m1 > k) {
+    uint32_t th = 0, hmask = 0;
+    int need_hi = k;
+    for (int shift = 24; shift >= 0; shift -= 8) {
+      for (int d = lane; d < 256; d += 32) whist[d] = 0;
+      __syncwarp();
+      for (int i = lane; i < m1; i += 32) {
+        const uint32_t h = (uint32_t)(cand[i] >> 32);
+        if ((h & hmask) == th) atomicAdd(&whist[(h >> shift) & 255u], 1);
+      }
+      __syncwarp();
+      int local = 0;  // lane owns digits 255-8*lane .. 248-8*lane (descending)
+#pragma unroll
+      for (int t = 0; t < 8; ++t) local += whist[255 - 8 * lane - t];
+      const int incl = warp_incl_scan_i32(local, lane);
+      const int excl = incl - local;
+      int dsel = -1, nsel = 0;
+      if (excl < need_hi && incl >= need_hi) {
+        int cum = excl;
+        for (int t = 0; t < 8; ++t) {
+          const int d = 255 - 8 * lane - t;
+          if (cum + whist[d] >= need_hi) { dsel = d; nsel = need_hi - cum; break; }
+          cum += whist[d];
+        }
+      }
+      const unsigned who = __ballot_sync(0xffffffffu, dsel >= 0);
+      const int src = __ffs(who) - 1;
+      dsel = __shfl_sync(0xffffffffu, dsel, src);
+      need_hi = __shfl_sync(0xffffffffu, nsel, src);
+      th |= (uint32_t)dsel << shift;
+      hmask |= 255u << shift;
+      __syncwarp();
+    }
+    int gt = 0, eq = 0;
+    for (int i = lane; i < m1; i += 32) {
+      const uint32_t h = (uint32_t)(cand[i] >> 32);
+      gt += (h > th);
+      eq += (h == th);
+    }
+    gt = warp_sum_i32(gt);
+    eq = warp_sum_i32(eq);
+    const int need = k - gt;
+    uint32_t tl = 0;
+    if (eq > need) {  // key tie at the boundary: resolve on rel (insertion order)
+      for (int bit = 31; bit >= 0; --bit) {
+        const uint32_t t = tl | (1u << bit);
+        int cnt = 0;
+        for (int i = lane; i < m1; i += 32)
+          cnt += ((uint32_t)(cand[i] >> 32) == th) && ((uint32_t)cand[i] >= t);
+        if (warp_sum_i32(cnt) >= need) tl = t;
+      }
+    }
+    T = ((uint64_t)th << 32) | tl;
+  }
+  // winners to the front (unordered), then each one's rank by counting
+  int m = 0;
+  for (int i0 = 0; i0 < m1; i0 += 32) {
+    const int i = i0 + lane;
+    const uint64_t c = (i < m1) ? cand[i] : 0ull;
+    const int32_t p = (i < m1) ? cpay[i] : 0;
+    const bool w = c >= T;
+    const unsigned b = __ballot_sync(0xffffffffu, w && i < m1);
+    __syncwarp();
+    if (w && i < m1) {
+      cand[m + __popc(b & lt)] = c;
+      cpay[m + __popc(b & lt)] = p;
+    }
+    m += __popc(b);
+    __syncwarp();
+  }
+  int64_t row = q;
+  if (po.world > 0) {  // fused exchange (see k_merge)
+    const int owner = (int)(q / po.nq_local);
+    row = (int64_t)po.rank * po.nq_local + (q - (int64_t)owner * po.nq_local);
+    out_comp = po.comp[owner];
+    out_len = po.len[owner];
+  }
+  // 3. rank r of each winner = #winners above it; slot r of the output row
+  for (int i = lane; i < m; i += 32) {
+    const uint64_t c = cand[i];
+    int r = 0;
+    for (int j = 0; j < m; ++j) r += (cand[j] > c);
+    int32_t L = cpay[i];
+    if (!len) {
+      int64_t g = (int64_t)comp_rel(c) + head % gcap;
+      if (g >= gcap) g -= gcap;
+      L = bank_lens[g - slot_offset];
+    }
+    out_comp[row * k + r] = c;
+    out_len[row * k + r] = L;
+  }
+  for (int i = m + lane; i < k; i += 32) {
+    out_comp[row * k + i] = 0ull;
+    out_len[row * k + i] = 0;
+  }
+  if (po.world > 0) __threadfence_system();  // peer stores visible before the barrier
+}
+
 int launch_merge(const uint64_t* comp, const int32_t* len, int nlists, int64_t nq, int k,
                  uint64_t* out_comp, int32_t* out_len, const int32_t* bank_lens, int64_t head,
                  int64_t gcap, int64_t slot_offset, cudaStream_t st, const PeerOut* po) {
   if (nq <= 0) return SS_OK;
+  if ((int64_t)nlists * k <= MW_MAX_M) {
+    const size_t wb = ((size_t)nlists * k * 12 + 15) & ~(size_t)15;
+    const size_t smem = wb * MW_WARPS;
+    SS_CUDA_TRY(ensure_dyn_smem(k_merge_w, smem));
+    count_launch();
+    SS_CUDA_TRY(pdl_launch(k_merge_w, dim3((unsigned)((nq + MW_WARPS - 1) / MW_WARPS)),
+                           dim3(MW_WARPS * 32), smem, st, comp, len, nlists, nq, k, out_comp,
+                           out_len, bank_lens, head, gcap, slot_offset, po ? *po : PeerOut{}, wb));
+    SS_LAUNCH_CHECK();
+    return SS_OK;
+  }
   int kpad = 1;
   while (kpad < k) kpad <<= 1;
   size_t smem = merge_smem(nlists, k, kpad);
@@ -433,11 +616,6 @@ __device__ __forceinline__ void warp_finish_tail(
 
 
 
-__device__ __forceinline__ int warp_sum_i32(int v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
 
 __global__ void __launch_bounds__(MFW_WARPS * 32)
 k_merge_finish_w(const uint64_t* __restrict__ partials, int nlists, int64_t nq, int k,
@@ -663,9 +841,7 @@ int launch_finish(const uint64_t* comp, const int32_t* len, int64_t nq, int k, i
     const size_t wb = (((size_t)k * 4 + 15) & ~(size_t)15) + ((finish_smem(nbins) + 15) & ~(size_t)15);
     const size_t smem = wb * MFW_WARPS;
     if (smem <= 200 * 1024) {
-      if (smem > 48 * 1024)
-        SS_CUDA_TRY(cudaFuncSetAttribute(k_finish_w, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem));
+      SS_CUDA_TRY(ensure_dyn_smem(k_finish_w, smem));
       count_launch();
       SS_CUDA_TRY(pdl_launch(k_finish_w, dim3((unsigned)((nq + MFW_WARPS - 1) / MFW_WARPS)),
                              dim3(MFW_WARPS * 32), smem, st, comp, len, nq, k, min_matches, max_len,
@@ -676,8 +852,7 @@ int launch_finish(const uint64_t* comp, const int32_t* len, int64_t nq, int k, i
   }
   size_t smem = finish_smem(nbins);
   if (smem > 200 * 1024) return set_error(SS_ERR_UNSUPPORTED, "nbins %d too large", nbins);
-  if (smem > 48 * 1024)
-    SS_CUDA_TRY(cudaFuncSetAttribute(k_finish, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  SS_CUDA_TRY(ensure_dyn_smem(k_finish, smem));
   count_launch();
   k_finish<<<(unsigned)nq, MF_THREADS, smem, st>>>(comp, len, nq, k, min_matches, max_len, nbins, I,
                                                   fb_cnt, fb_sv, fb_sv2, P, npts, pbin, pcnt, pD,
@@ -699,9 +874,7 @@ int launch_merge_finish(const uint64_t* partials, int nlists, int64_t nq, int k,
                        ~(size_t)15) + ((finish_smem(nbins) + 15) & ~(size_t)15);
     const size_t smem = wb * MFW_WARPS;
     if (smem <= 200 * 1024) {
-      if (smem > 48 * 1024)
-        SS_CUDA_TRY(cudaFuncSetAttribute(k_merge_finish_w,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      SS_CUDA_TRY(ensure_dyn_smem(k_merge_finish_w, smem));
       count_launch();
       SS_CUDA_TRY(pdl_launch(k_merge_finish_w, dim3((unsigned)((nq + MFW_WARPS - 1) / MFW_WARPS)),
                              dim3(MFW_WARPS * 32), smem, st, partials, nlists, nq, k, bank_lens, head,

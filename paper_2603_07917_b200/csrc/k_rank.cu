@@ -461,9 +461,7 @@ int launch_rank(const double* G, const int64_t* ids, int64_t n, int64_t* perm, v
     SS_CUDA_TRY(pdl_launch(k_rank_chunk, dim3(nch), dim3(CH_N), 0, st, G, ids, (int)n, sk, sid, six));
     SS_LAUNCH_CHECK();
     const size_t smem = (size_t)n * (8 + 8 + 4);
-    if (smem > 48 * 1024)
-      SS_CUDA_TRY(cudaFuncSetAttribute(k_rank_merge, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem));
+    SS_CUDA_TRY(ensure_dyn_smem(k_rank_merge, smem));
     count_launch();
     SS_CUDA_TRY(pdl_launch(k_rank_merge, dim3(nch), dim3(CH_N), smem, st, (const uint64_t*)sk,
                            (const int64_t*)sid, (const int32_t*)six, (int)n, perm));

@@ -10,6 +10,18 @@ namespace ss {
 
 void count_launch();
 
+// opt `kern` in to `dyn` bytes of dynamic shared memory when its static
+// shared memory plus `dyn` exceeds the 48 KB default (the default limit
+// covers both)
+template <typename... KArgs>
+inline cudaError_t ensure_dyn_smem(void (*kern)(KArgs...), size_t dyn) {
+  if (dyn == 0) return cudaSuccess;
+  cudaFuncAttributes fa{};
+  if (cudaError_t e = cudaFuncGetAttributes(&fa, kern)) return e;
+  if (fa.sharedSizeBytes + dyn <= 48 * 1024) return cudaSuccess;
+  return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+}
+
 // launch `kern` with the programmatic-stream-serialization attribute (PDL):
 // its launch overlaps the tail of the previous kernel on the stream; the
 // kernel calls pdl_wait() before reading that kernel's outputs

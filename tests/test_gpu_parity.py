@@ -1088,6 +1088,51 @@ def test_topk_gather_shards_equal_single_bank(cuda, world):
     assert torch.equal(out_c, c0) and torch.equal(out_l, l0)
 
 
+@pytest.mark.parametrize("nlists,k,fill", [(8, 64, "full"), (8, 64, "ragged"), (3, 20, "ragged"),
+                                            (18, 64, "ragged"), (8, 256, "full"), (1, 64, "ragged"),
+                                            (40, 64, "full"), (5, 7, "empty")])
+def test_merge_topk_vs_sorted_union(cuda, nlists, k, fill):
+    """ss_merge_topk (the owner's merge of the shards' lists; the warp-per-query
+    kernel up to nlists * k = 2048 candidates, the block kernel above) against
+    the sorted union of the lists: top-k composites descending, 0-padded, each
+    with its carried length.  Keys tie across lists (same high word, different
+    insertion rank) so the low-word resolution is exercised; lists are in
+    arbitrary order and partly empty."""
+    from paper_2603_07917_b200 import _lib
+    rng = np.random.default_rng(nlists * 1000 + k)
+    nq = 300
+    pool = nlists * k
+    comp = np.zeros((nlists, nq, k), np.uint64)
+    ln = np.zeros((nlists, nq, k), np.int32)
+    for q in range(nq):
+        keys = rng.integers(0x3F000000, 0x3F000000 + max(4, pool // 3), pool).astype(np.uint64)
+        rel = rng.permutation(1 << 20)[:pool].astype(np.uint64)  # unique insertion ranks
+        c = (keys << np.uint64(32)) | rel
+        for l in range(nlists):
+            n = {"full": k, "ragged": int(rng.integers(0, k + 1)), "empty": 0}[fill]
+            part = c[l * k:l * k + n]
+            comp[l, q, :n] = rng.permutation(part)
+            ln[l, q, :n] = (part % np.uint64(2047)).astype(np.int32) + 1
+    out_c = torch.full((nq, k), -5, dtype=torch.int64, device="cuda")
+    out_l = torch.full((nq, k), -5, dtype=torch.int32, device="cuda")
+    dc, dl = _t(comp.view(np.int64)), _t(ln)
+    _lib.call("ss_merge_topk", _lib.ptr(dc), _lib.ptr(dl), nlists, nq, k, _lib.ptr(out_c),
+              _lib.ptr(out_l), _lib.stream_ptr())
+    got_c = out_c.cpu().numpy().view(np.uint64)
+    got_l = out_l.cpu().numpy()
+    for q in range(nq):
+        allc = comp[:, q, :].ravel()
+        alll = ln[:, q, :].ravel()
+        nz = allc != 0
+        order = np.argsort(allc[nz])[::-1][:k]
+        want_c = np.zeros(k, np.uint64)
+        want_l = np.zeros(k, np.int32)
+        want_c[:order.size] = allc[nz][order]
+        want_l[:order.size] = alll[nz][order]
+        assert np.array_equal(got_c[q], want_c), q
+        assert np.array_equal(got_l[q], want_l), q
+
+
 @pytest.mark.parametrize("world,algo", [(2, "auto"), (3, "auto"), (2, "scan")])
 def test_topk_scatter_shards_equal_single_bank(cuda, world, algo):
     """ss_topk_scatter addressing, all ranks simulated in one process: shard r
