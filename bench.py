@@ -385,12 +385,13 @@ def run_single(args):
     # the north star's target shape (BASELINE configs[3]) on this one GPU
     # (after the peak probes: its long run heats the part): the per-GPU
     # similarity work of the 8-GPU configuration is 1/8 of it
-    c4 = sweep = None
+    c4 = sweep = proj = None
     if args.config == "c2" and not args.no_c4:
         del graph, sched, win
         torch.cuda.empty_cache()
         c4 = c4_one_gpu(args)
         sweep = vs_bank_size(args)
+        proj = c4_projection()
     line = {
         "metric": METRIC, "value": round(nq * args.steps / (ms / 1e3), 1), "unit": "requests/s",
         "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
@@ -410,6 +411,7 @@ def run_single(args):
         "pure_topk": pure,
         "c4_one_gpu": c4,
         "vs_bank_size": sweep,
+        "c4_n_gpus_projection": proj,
         "gpu_launches": int(per_round * args.steps),
         "clocks": clocks,
     }
@@ -462,6 +464,110 @@ def c4_one_gpu(args):
         out["kernel_frac_of_sustained"] = round(out["kernel_tops"] / s_peak, 4)
         out["sustained_probe_clocks"] = s_clk
     del graph, sched, win, dq, dqi, dI, dids
+    torch.cuda.empty_cache()
+    return out
+
+
+NVLINK_GBS, COLL_LAT_US = 770.0, 15.0  # B200_PROFILING.md peer copy per direction; per-collective latency
+
+
+def c4_projection(rows=1 << 24, nq=8192, worlds=(2, 4, 8), reps=5):
+    """c4 single-owner round at N GPUs PROJECTED from components measured on
+    this one GPU (not a multi-GPU measurement): the bank cut into N shards by
+    ShardPlan exactly as the sharded round places them; every shard's local
+    stage (HistoryWindow.topk: TS kernel + slice merge) timed with CUDA
+    events; the owner's stages (ss_merge_topk of the N lists, ss_finish,
+    ss_rank) timed on the stacked shard outputs; the merged lists, window
+    histogram, G and order checked bit-identical to the unsharded round.  The
+    broadcast and all-gather are charged at NVLINK_GBS + COLL_LAT_US each.
+    round(N) = max over shards of the local stage + collectives + owner."""
+    import torch
+
+    from paper_2603_07917_b200 import _lib
+    from paper_2603_07917_b200.history import HistoryWindow
+    from paper_2603_07917_b200.scheduler import rank
+    from paper_2603_07917_b200.sharded import ShardPlan
+    from paper_2603_07917_b200.synthetic import make_bank_device, make_queries
+
+    _lib.load()
+    P = _lib.ptr
+    emb, lens, _ = make_bank_device(rows, DIM, N_CLUSTERS, SEED)
+    q, qi, I, ids = make_queries(nq, DIM, N_CLUSTERS, SEED, qseed=1000)
+    dq, dqi, dI, dids = (torch.as_tensor(x, device="cuda") for x in (q, qi, I, ids))
+
+    def owner(comp_x, len_x, nlists, fb):
+        comp = torch.empty((nq, K), dtype=torch.int64, device="cuda")
+        ln = torch.empty((nq, K), dtype=torch.int32, device="cuda")
+        o = {n: torch.zeros(sh, dtype=dt, device="cuda") for n, sh, dt in (
+            ("npts", nq, torch.int32), ("pbin", (nq, NBINS), torch.int32),
+            ("pcnt", (nq, NBINS), torch.int32), ("pD", (nq, NBINS), torch.int64),
+            ("used_fb", nq, torch.uint8), ("G", nq, torch.float64), ("perm", nq, torch.int64))}
+        ws = torch.empty(int(_lib.lib().ss_rank_workspace_bytes(nq)), dtype=torch.uint8, device="cuda")
+        c, l_ = (comp, ln) if nlists > 1 else (comp_x, len_x)
+
+        def go():
+            if nlists > 1:
+                _lib.call("ss_merge_topk", P(comp_x), P(len_x), nlists, nq, K, P(comp), P(ln),
+                          _lib.stream_ptr())
+            _lib.call("ss_finish", P(c), P(l_), nq, K, MIN_MATCHES, MAX_LEN, NBINS, P(dI), P(fb[0]),
+                      P(fb[1]), P(fb[2]), NBINS, P(o["npts"]), P(o["pbin"]), P(o["pcnt"]),
+                      P(o["pD"]), None, P(o["used_fb"]), P(o["G"]), _lib.stream_ptr())
+            rank(o["G"], dids, o["perm"], ws)
+        t = time_ms(go, reps)
+        go()
+        torch.cuda.synchronize()
+        return t, c, l_, o
+
+    full = HistoryWindow(rows, DIM)
+    full.push(emb, lens)
+    fb1 = full.fallback_hist(MAX_LEN, NBINS)
+    full.topk(dq, dqi, K, THETA)
+    t_loc1 = time_ms(lambda: full.topk(dq, dqi, K, THETA), reps)
+    c1, l1 = full.topk(dq, dqi, K, THETA)
+    t_own1, _, _, o1 = owner(c1, l1, 1, fb1)
+    del full
+    torch.cuda.empty_cache()
+    out = {"what": "c4 single-owner round on N GPUs PROJECTED from components measured on this "
+                   "one GPU (not a multi-GPU measurement)",
+           "rows": rows, "nq": nq, "k": K, "theta": THETA,
+           "one_gpu_round_ms": round(t_loc1 + t_own1, 3),
+           "collective_model": f"{NVLINK_GBS} GB/s per direction (B200_PROFILING.md peer copy) + "
+                               f"{COLL_LAT_US} us per collective (broadcast, all-gather)",
+           "points": []}
+    for world in worlds:
+        comps, lns, times = [], [], []
+        fb = torch.zeros((3, NBINS), dtype=torch.int64, device="cuda")
+        for r in range(world):
+            plan = ShardPlan(rows, world, r)  # the sharded round's own placement
+            w = HistoryWindow(plan.local_capacity, DIM, global_capacity=rows,
+                              slot_offset=plan.slot_offset)
+            idx, seq, slot = (torch.as_tensor(x, device="cuda") for x in plan.route(0, rows))
+            w.write(emb[idx], lens[idx], seq, slot)
+            w.set_head(rows)
+            del idx, seq, slot
+            fb += w.fallback_hist(MAX_LEN, NBINS)
+            w.topk(dq, dqi, K, THETA)
+            times.append(time_ms(lambda: w.topk(dq, dqi, K, THETA), reps))
+            c, l_ = w.topk(dq, dqi, K, THETA)
+            comps.append(c)
+            lns.append(l_)
+            del w
+            torch.cuda.empty_cache()
+        t_own, c, l_, o = owner(torch.stack(comps).contiguous(), torch.stack(lns).contiguous(),
+                                world, fb)
+        exact = bool(torch.equal(c, c1) and torch.equal(l_, l1) and torch.equal(fb, fb1)
+                     and torch.equal(o["G"], o1["G"]) and torch.equal(o["perm"], o1["perm"]))
+        coll_b = nq * (DIM + 4) + (world - 1) * nq * K * 12  # queue broadcast + owner's gather
+        t_coll = coll_b / (NVLINK_GBS * 1e9) * 1e3 + 2 * COLL_LAT_US / 1e3
+        t_round = max(times) + t_coll + t_own
+        out["points"].append({
+            "n_gpus": world, "shard_rows": rows // world,
+            "local_stage_ms_max": round(max(times), 3), "local_stage_ms_min": round(min(times), 3),
+            "owner_merge_finish_rank_ms": round(t_own, 3), "collectives_ms_modelled": round(t_coll, 3),
+            "projected_round_ms": round(t_round, 3),
+            "projected_value": round(nq / (t_round / 1e3), 1), "unit": "requests/s",
+            "bit_identical_to_one_gpu_round": exact})
+    del emb, lens
     torch.cuda.empty_cache()
     return out
 
