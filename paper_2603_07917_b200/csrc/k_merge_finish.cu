@@ -916,11 +916,57 @@ int launch_merge_finish(const uint64_t* partials, int nlists, int64_t nq, int k,
 // is warp-converged.
 // ---------------------------------------------------------------------------
 constexpr int RF_GL = 8;
-// chunks of RF_GL points kept in registers between the two passes (64
-// points: a c3 law has ~52); 6 blocks per SM (64 regs) measured best:
-// 72 us for c3 vs 90-117 us at other (lanes, chunks, occupancy) choices
-constexpr int RF_R = 8;
-constexpr int RF_MINB = 6;
+// chunks of RF_GL points kept between the two passes (64 points: a c3 law
+// has ~52), 6 blocks per SM (40 registers).  SS_RF_ALL runs the scan pass
+// over every kept chunk (straight-line code: fewer divergence guards and
+// spills than a loop bounded by the warp's longest law).  c3 k_refresh on
+// B200 (profiles/ROUND2.md, r2v): 71.5 us with a per-point divide, 69.3 us
+// with the cross-multiplied minimum (SS_RF_XMUL), 66.7 us with both; fewer
+// blocks per SM or fewer kept chunks measured slower (73-84 us)
+#ifndef SS_RF_R
+#define SS_RF_R 8
+#endif
+#ifndef SS_RF_ALL
+#define SS_RF_ALL 1
+#endif
+#ifndef SS_RF_MINB
+#define SS_RF_MINB 6
+#endif
+constexpr int RF_R = SS_RF_R;
+constexpr int RF_MINB = SS_RF_MINB;
+
+#ifndef SS_RF_XMUL
+#define SS_RF_XMUL 1
+#endif
+// exact n1/d1 < n2/d2 for n >= 0, d >= 0 (d = 0: +inf) by products with
+// their FMA rounding errors, (p, e) compared lexicographically: p1 < p2
+// implies n1 d2 <= n2 d1 exactly, and ties in the exact values pick either
+// side with the same quotient.  Division rounds monotonically, so the
+// correctly rounded quotient of the pair this minimum keeps equals the
+// minimum of the correctly rounded per-point quotients (the reference's
+// min over r_k): one divide per law instead of one per point.
+__device__ __forceinline__ bool ratio_less(double n1, double d1, double n2, double d2) {
+  const double p1 = __dmul_rn(n1, d2), e1 = __fma_rn(n1, d2, -p1);
+  const double p2 = __dmul_rn(n2, d1), e2 = __fma_rn(n2, d1, -p2);
+  return p1 < p2 || (p1 == p2 && e1 < e2);
+}
+struct RatioMin {
+  double n = 1.0, d = 0.0;  // +inf
+  __device__ __forceinline__ void add(long long P, long long C, long long T, long long ck,
+                                      long long dk) {
+    const double num = __dadd_rn(__dmul_rn((double)P, (double)ck), __dmul_rn((double)dk, (double)(T - C)));
+    const double den = __dmul_rn(2.0 * (double)ck, (double)C);
+    if (ratio_less(num, den, n, d)) { n = num; d = den; }
+  }
+  __device__ __forceinline__ void group_reduce() {
+#pragma unroll
+    for (int o = RF_GL / 2; o > 0; o >>= 1) {
+      const double on = __shfl_xor_sync(0xffffffffu, n, o), od = __shfl_xor_sync(0xffffffffu, d, o);
+      if (ratio_less(on, od, n, d)) { n = on; d = od; }
+    }
+  }
+  __device__ __forceinline__ double value() const { return d == 0.0 ? INFINITY : __ddiv_rn(n, d); }
+};
 
 __device__ __forceinline__ long long grp_incl_scan_i64(long long v, int gl) {
 #pragma unroll
@@ -993,14 +1039,20 @@ k_refresh(int64_t n, const int32_t* __restrict__ I, const int32_t* __restrict__ 
   // pass 2: prefix sums and the ratio at every surviving point
   long long Cc = 0, Pc = 0;
   double best = INFINITY;
+  RatioMin rm;
 #pragma unroll
   for (int j = 0; j < RF_R; ++j) {
-    if (j * RF_GL >= npmax) break;  // warp-uniform
-    const long long C = grp_incl_scan_i32(cr[j], gl) + Cc;
-    const long long Pp = grp_incl_scan_i64(dr[j], gl) + Pc;
-    if (cr[j] > 0) best = fmin(best, gittins_ratio(Pp, C, T, cr[j], dr[j]));
-    Cc = __shfl_sync(0xffffffffu, C, RF_GL - 1, RF_GL);
-    Pc = __shfl_sync(0xffffffffu, Pp, RF_GL - 1, RF_GL);
+    if (SS_RF_ALL || j * RF_GL < npmax) {  // warp-uniform
+      const long long C = grp_incl_scan_i32(cr[j], gl) + Cc;
+      const long long Pp = grp_incl_scan_i64(dr[j], gl) + Pc;
+      if (SS_RF_XMUL) {
+        if (cr[j] > 0) rm.add(Pp, C, T, cr[j], dr[j]);
+      } else if (cr[j] > 0) {
+        best = fmin(best, gittins_ratio(Pp, C, T, cr[j], dr[j]));
+      }
+      Cc = __shfl_sync(0xffffffffu, C, RF_GL - 1, RF_GL);
+      Pc = __shfl_sync(0xffffffffu, Pp, RF_GL - 1, RF_GL);
+    }
   }
   for (int b = RF_R * RF_GL; b < npmax; b += RF_GL) {
     const int k = b + gl;
@@ -1013,12 +1065,21 @@ k_refresh(int64_t n, const int32_t* __restrict__ I, const int32_t* __restrict__ 
     }
     const long long C = grp_incl_scan_i32(ck, gl) + Cc;
     const long long Pp = grp_incl_scan_i64(dk, gl) + Pc;
-    if (ck > 0) best = fmin(best, gittins_ratio(Pp, C, T, ck, dk));
+    if (SS_RF_XMUL) {
+      if (ck > 0) rm.add(Pp, C, T, ck, dk);
+    } else if (ck > 0) {
+      best = fmin(best, gittins_ratio(Pp, C, T, ck, dk));
+    }
     Cc = __shfl_sync(0xffffffffu, C, RF_GL - 1, RF_GL);
     Pc = __shfl_sync(0xffffffffu, Pp, RF_GL - 1, RF_GL);
   }
+  if (SS_RF_XMUL) {
+    rm.group_reduce();
+    best = rm.value();
+  } else {
 #pragma unroll
-  for (int o = RF_GL / 2; o > 0; o >>= 1) best = fmin(best, __shfl_xor_sync(0xffffffffu, best, o));
+    for (int o = RF_GL / 2; o > 0; o >>= 1) best = fmin(best, __shfl_xor_sync(0xffffffffu, best, o));
+  }
   if (gl == 0 && live) {
     if (due) {
       double v = best;
