@@ -330,6 +330,37 @@ __device__ __forceinline__ double gittins_ratio(long long P, long long C, long l
   return __ddiv_rn(num, __dmul_rn(2.0 * (double)ck, (double)C));
 }
 
+// exact n1/d1 < n2/d2 for n >= 0, d >= 0 (d = 0: +inf) by products with
+// their FMA rounding errors, (p, e) compared lexicographically: p1 < p2
+// implies n1 d2 <= n2 d1 exactly, and ties in the exact values pick either
+// side with the same quotient.  Division rounds monotonically, so the
+// correctly rounded quotient of the pair this minimum keeps equals the
+// minimum of the correctly rounded per-point quotients (the reference's
+// min over r_k): one divide per law instead of one per point.
+__device__ __forceinline__ bool ratio_less(double n1, double d1, double n2, double d2) {
+  const double p1 = __dmul_rn(n1, d2), e1 = __fma_rn(n1, d2, -p1);
+  const double p2 = __dmul_rn(n2, d1), e2 = __fma_rn(n2, d1, -p2);
+  return p1 < p2 || (p1 == p2 && e1 < e2);
+}
+struct RatioMin {
+  double n = 1.0, d = 0.0;  // +inf
+  __device__ __forceinline__ void add(long long P, long long C, long long T, long long ck,
+                                      long long dk) {
+    const double num = __dadd_rn(__dmul_rn((double)P, (double)ck), __dmul_rn((double)dk, (double)(T - C)));
+    const double den = __dmul_rn(2.0 * (double)ck, (double)C);
+    if (ratio_less(num, den, n, d)) { n = num; d = den; }
+  }
+  template <int W>  // lanes per group (a power of two <= 32)
+  __device__ __forceinline__ void group_reduce() {
+#pragma unroll
+    for (int o = W / 2; o > 0; o >>= 1) {
+      const double on = __shfl_xor_sync(0xffffffffu, n, o), od = __shfl_xor_sync(0xffffffffu, d, o);
+      if (ratio_less(on, od, n, d)) { n = on; d = od; }
+    }
+  }
+  __device__ __forceinline__ double value() const { return d == 0.0 ? INFINITY : __ddiv_rn(n, d); }
+};
+
 __device__ double warp_gittins_exact(const int32_t* c, const int64_t* D, int np, long long A2,
                                      int I, int g, int bucket, int lane) {
   int first = np;
@@ -348,7 +379,7 @@ __device__ double warp_gittins_exact(const int32_t* c, const int64_t* D, int np,
   for (int k = first + lane; k < np; k += 32) T += c[k];
   for (int o = 16; o > 0; o >>= 1) T += __shfl_xor_sync(0xffffffffu, T, o);
   long long Cc = 0, Pc = 0;
-  double best = INFINITY;
+  RatioMin rm;  // min over points of the exact ratio, one divide at the end
   for (int b = first; b < np; b += 32) {
     int k = b + lane;
     long long ck = 0, dk = 0;
@@ -358,11 +389,12 @@ __device__ double warp_gittins_exact(const int32_t* c, const int64_t* D, int np,
     }
     long long C = warp_incl_scan_i64(ck, lane) + Cc;
     long long P = warp_incl_scan_i64(dk, lane) + Pc;
-    if (k < np) best = fmin(best, gittins_ratio(P, C, T, ck, dk));
+    if (k < np) rm.add(P, C, T, ck, dk);
     Cc = __shfl_sync(0xffffffffu, C, 31);
     Pc = __shfl_sync(0xffffffffu, P, 31);
   }
-  return warp_min_f64(best);
+  rm.group_reduce<32>();
+  return rm.value();
 }
 
 // ---------------------------------------------------------------------------
@@ -906,8 +938,8 @@ int launch_merge_finish(const uint64_t* partials, int nlists, int64_t nq, int k,
 // refresh (SPEC.md:345-353 cadence): RF_GL = 8 lanes per request, four
 // requests per warp, so the prefix scans are 3 shuffle steps and a ~50-point
 // law fills the lanes; one read of the law (its first 64 points stay in
-// registers for the second pass), one divide per point.  Same arithmetic, in
-// the same order, as warp_gittins_exact / oracle gittins_points:
+// registers for the second pass), one divide per law (RatioMin).  Same
+// arithmetic, in the same order, as warp_gittins_exact / oracle gittins_points:
 //   survivors  D_k > A2 c_k (a suffix: bin means increase with the bin)
 //   T = sum of surviving c;  C_k, P_k inclusive prefix sums over survivors
 //   r_k = (P_k c_k + d_k (T - C_k)) / (2 c_k C_k),  d_k = D_k - A2 c_k,  G = min r_k
@@ -926,6 +958,9 @@ constexpr int RF_GL = 8;
 #ifndef SS_RF_R
 #define SS_RF_R 8
 #endif
+#ifndef SS_RF_XMUL
+#define SS_RF_XMUL 1
+#endif
 #ifndef SS_RF_ALL
 #define SS_RF_ALL 1
 #endif
@@ -934,39 +969,6 @@ constexpr int RF_GL = 8;
 #endif
 constexpr int RF_R = SS_RF_R;
 constexpr int RF_MINB = SS_RF_MINB;
-
-#ifndef SS_RF_XMUL
-#define SS_RF_XMUL 1
-#endif
-// exact n1/d1 < n2/d2 for n >= 0, d >= 0 (d = 0: +inf) by products with
-// their FMA rounding errors, (p, e) compared lexicographically: p1 < p2
-// implies n1 d2 <= n2 d1 exactly, and ties in the exact values pick either
-// side with the same quotient.  Division rounds monotonically, so the
-// correctly rounded quotient of the pair this minimum keeps equals the
-// minimum of the correctly rounded per-point quotients (the reference's
-// min over r_k): one divide per law instead of one per point.
-__device__ __forceinline__ bool ratio_less(double n1, double d1, double n2, double d2) {
-  const double p1 = __dmul_rn(n1, d2), e1 = __fma_rn(n1, d2, -p1);
-  const double p2 = __dmul_rn(n2, d1), e2 = __fma_rn(n2, d1, -p2);
-  return p1 < p2 || (p1 == p2 && e1 < e2);
-}
-struct RatioMin {
-  double n = 1.0, d = 0.0;  // +inf
-  __device__ __forceinline__ void add(long long P, long long C, long long T, long long ck,
-                                      long long dk) {
-    const double num = __dadd_rn(__dmul_rn((double)P, (double)ck), __dmul_rn((double)dk, (double)(T - C)));
-    const double den = __dmul_rn(2.0 * (double)ck, (double)C);
-    if (ratio_less(num, den, n, d)) { n = num; d = den; }
-  }
-  __device__ __forceinline__ void group_reduce() {
-#pragma unroll
-    for (int o = RF_GL / 2; o > 0; o >>= 1) {
-      const double on = __shfl_xor_sync(0xffffffffu, n, o), od = __shfl_xor_sync(0xffffffffu, d, o);
-      if (ratio_less(on, od, n, d)) { n = on; d = od; }
-    }
-  }
-  __device__ __forceinline__ double value() const { return d == 0.0 ? INFINITY : __ddiv_rn(n, d); }
-};
 
 __device__ __forceinline__ long long grp_incl_scan_i64(long long v, int gl) {
 #pragma unroll
@@ -1074,7 +1076,7 @@ k_refresh(int64_t n, const int32_t* __restrict__ I, const int32_t* __restrict__ 
     Pc = __shfl_sync(0xffffffffu, Pp, RF_GL - 1, RF_GL);
   }
   if (SS_RF_XMUL) {
-    rm.group_reduce();
+    rm.group_reduce<RF_GL>();
     best = rm.value();
   } else {
 #pragma unroll
