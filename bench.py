@@ -704,6 +704,7 @@ def run_sharded(args, world, rank, local):
         i8_peak, i8_detail = int8_peak()
         ops = 2.0 * nq * (n_bank // world) * DIM
         achieved = ops / (kern_ms / 1e3) / 1e12
+        B = "NCCL" if args.backend == "nccl" else "gloo (functional check: ranks share GPUs)"
         line = {
             "metric": METRIC, "value": round(nq * args.steps / (ms / 1e3), 1), "unit": "requests/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -713,11 +714,11 @@ def run_sharded(args, world, rank, local):
             "config": {"workload": C["workload"] + f"; bank row-sharded over {world} GPU(s), "
                        "one queue owned by rank 0", "bank_rows": n_bank, "dim": DIM, "nq": nq,
                        "k": K, "nbins": NBINS, "theta": THETA, "min_matches": MIN_MATCHES,
-                       "parallelism": f"bank shard x{world}; NCCL broadcast of the queue, "
+                       "parallelism": f"bank shard x{world}; {B} broadcast of the queue, "
                                       + ("fused P2P gather of k candidates/query (ss_topk_gather)"
                                          if args.exchange == "p2p" else
-                                         "NCCL all-gather of k candidates/query")
-                                      + ", NCCL all-reduce of the window histogram; stages 2-4 "
+                                         f"{B} all-gather of k candidates/query")
+                                      + f", {B} all-reduce of the window histogram; stages 2-4 "
                                         "on the owner",
                        "graph": graph is not None,
                        "l2": "bank shard streamed from HBM each round"},
