@@ -1439,3 +1439,15 @@ def test_c2_round_time_guard(cuda):
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / 20
     assert ms < 0.6, ms
+
+
+def test_sharded_owner_stages_bit_identical_small(cuda):
+    """The measured-component projection of the single-owner round
+    (bench.c4_projection) at a small shape: the bank cut by ShardPlan into 2
+    and 4 shards, each shard's local top-k, the owner's ss_merge_topk +
+    ss_finish + ss_rank -- lists, window histogram, G and order bit-identical
+    to the one-window round."""
+    import bench
+    out = bench.c4_projection(rows=1 << 16, nq=512, worlds=(2, 4), reps=1)
+    assert [p["n_gpus"] for p in out["points"]] == [2, 4]
+    assert all(p["bit_identical_to_one_gpu_round"] for p in out["points"])
