@@ -318,17 +318,12 @@ int launch_decode(const uint64_t* comp, int64_t n, int64_t head, int64_t capacit
 //   D_k = sum v^2 + 2 I sum v over bin k  (so c_k s_k = D_k / 2 exactly)
 //   attained 2a = A2 = g^2 + 2 I g; survivors D_k > A2 c_k (a suffix)
 //   ratio_k = (0.5 P'_k + s'_k (T' - C'_k)) / C'_k,  s'_k = d_k / (2 c_k),
-//           = (P'_k c_k + d_k (T' - C'_k)) / (2 c_k C'_k)   (one divide)
+//           = (P'_k c_k + d_k (T' - C'_k)) / (2 c_k C'_k)   (RatioMin::add)
 //   d_k = D_k - A2 c_k, P'_k = sum_{j<=k surv} d_j, C'_k = sum c_j, T' = C'_last
 // -- the algebra of _kernels.py:110-115 (cum_xp + s (1 - cum_p)) / cum_p with
 // masses c/T'.  Integer sums are exact; the fp64 ops are explicit _rn (no FMA
 // contraction) in the order of oracle.gittins_points -> bit-identical.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ double gittins_ratio(long long P, long long C, long long T, long long ck,
-                                                long long dk) {
-  const double num = __dadd_rn(__dmul_rn((double)P, (double)ck), __dmul_rn((double)dk, (double)(T - C)));
-  return __ddiv_rn(num, __dmul_rn(2.0 * (double)ck, (double)C));
-}
 
 // exact n1/d1 < n2/d2 for n >= 0, d >= 0 (d = 0: +inf) by products with
 // their FMA rounding errors, (p, e) compared lexicographically: p1 < p2
@@ -949,23 +944,18 @@ int launch_merge_finish(const uint64_t* partials, int nlists, int64_t nq, int k,
 // ---------------------------------------------------------------------------
 constexpr int RF_GL = 8;
 // chunks of RF_GL points kept between the two passes (64 points: a c3 law
-// has ~52), 6 blocks per SM (40 registers).  SS_RF_ALL runs the scan pass
-// over every kept chunk (straight-line code: fewer divergence guards and
-// spills than a loop bounded by the warp's longest law).  c3 k_refresh on
-// B200 (profiles/ROUND2.md, r2v): 71.5 us with a per-point divide, 69.3 us
-// with the cross-multiplied minimum (SS_RF_XMUL), 66.7 us with both; fewer
-// blocks per SM or fewer kept chunks measured slower (73-84 us)
+// has ~52), 5 blocks per SM (48 registers).  c3 k_refresh on B200
+// (profiles/ROUND2.md, r2v-r2zf): 71.5 us with a per-point divide and a
+// shuffle-reduced chunk bound; 66.7 us with the cross-multiplied minimum;
+// 63.7 us with the bound from redux.sync (a value the compiler knows is
+// warp-uniform: the chunk guards become uniform branches, no divergence
+// fallbacks around the shuffles, fewer spills) at 5 blocks per SM (6: 64.3,
+// 4: 65.6 us); fewer kept chunks measured slower (70-84 us)
 #ifndef SS_RF_R
 #define SS_RF_R 8
 #endif
-#ifndef SS_RF_XMUL
-#define SS_RF_XMUL 1
-#endif
-#ifndef SS_RF_ALL
-#define SS_RF_ALL 1
-#endif
 #ifndef SS_RF_MINB
-#define SS_RF_MINB 6
+#define SS_RF_MINB 5
 #endif
 constexpr int RF_R = SS_RF_R;
 constexpr int RF_MINB = SS_RF_MINB;
@@ -1004,9 +994,9 @@ k_refresh(int64_t n, const int32_t* __restrict__ I, const int32_t* __restrict__ 
   const int nb = g / bucket_size;
   const bool due = live && (force || nb > bucket_io[i]);
   const int np = due ? npts[i] : 0;
-  int npmax = np;
-#pragma unroll
-  for (int o = 16; o >= RF_GL; o >>= 1) npmax = max(npmax, __shfl_xor_sync(0xffffffffu, npmax, o));
+  // warp-wide maximum by redux.sync: a value the compiler knows is uniform,
+  // so the chunk guards below are uniform branches
+  const int npmax = (int)__reduce_max_sync(0xffffffffu, (unsigned)np);
   const long long Ii = live ? I[i] : 0;
   const long long A2 = (long long)g * g + 2 * Ii * g;
   const int32_t* c = pcnt + (live ? i : 0) * (int64_t)P;
@@ -1040,18 +1030,13 @@ k_refresh(int64_t n, const int32_t* __restrict__ I, const int32_t* __restrict__ 
   T = grp_sum_i64(T);
   // pass 2: prefix sums and the ratio at every surviving point
   long long Cc = 0, Pc = 0;
-  double best = INFINITY;
   RatioMin rm;
 #pragma unroll
   for (int j = 0; j < RF_R; ++j) {
-    if (SS_RF_ALL || j * RF_GL < npmax) {  // warp-uniform
+    if (j * RF_GL < npmax) {  // warp-uniform
       const long long C = grp_incl_scan_i32(cr[j], gl) + Cc;
       const long long Pp = grp_incl_scan_i64(dr[j], gl) + Pc;
-      if (SS_RF_XMUL) {
-        if (cr[j] > 0) rm.add(Pp, C, T, cr[j], dr[j]);
-      } else if (cr[j] > 0) {
-        best = fmin(best, gittins_ratio(Pp, C, T, cr[j], dr[j]));
-      }
+      if (cr[j] > 0) rm.add(Pp, C, T, cr[j], dr[j]);
       Cc = __shfl_sync(0xffffffffu, C, RF_GL - 1, RF_GL);
       Pc = __shfl_sync(0xffffffffu, Pp, RF_GL - 1, RF_GL);
     }
@@ -1067,21 +1052,12 @@ k_refresh(int64_t n, const int32_t* __restrict__ I, const int32_t* __restrict__ 
     }
     const long long C = grp_incl_scan_i32(ck, gl) + Cc;
     const long long Pp = grp_incl_scan_i64(dk, gl) + Pc;
-    if (SS_RF_XMUL) {
-      if (ck > 0) rm.add(Pp, C, T, ck, dk);
-    } else if (ck > 0) {
-      best = fmin(best, gittins_ratio(Pp, C, T, ck, dk));
-    }
+    if (ck > 0) rm.add(Pp, C, T, ck, dk);
     Cc = __shfl_sync(0xffffffffu, C, RF_GL - 1, RF_GL);
     Pc = __shfl_sync(0xffffffffu, Pp, RF_GL - 1, RF_GL);
   }
-  if (SS_RF_XMUL) {
-    rm.group_reduce<RF_GL>();
-    best = rm.value();
-  } else {
-#pragma unroll
-    for (int o = RF_GL / 2; o > 0; o >>= 1) best = fmin(best, __shfl_xor_sync(0xffffffffu, best, o));
-  }
+  rm.group_reduce<RF_GL>();
+  const double best = rm.value();
   if (gl == 0 && live) {
     if (due) {
       double v = best;
