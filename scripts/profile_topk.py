@@ -16,7 +16,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 from paper_2603_07917_b200 import _lib  # noqa: E402
 from paper_2603_07917_b200.history import HistoryWindow  # noqa: E402
-from paper_2603_07917_b200.synthetic import make_bank_device, make_queries  # noqa: E402
+from paper_2603_07917_b200.synthetic import inv_norm_np, make_bank_device, make_queries  # noqa: E402
 
 
 def main():
@@ -29,6 +29,9 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--time", action="store_true")
     ap.add_argument("--lib", default=None, help="an experiment build of libsagesched.so")
+    ap.add_argument("--random", action="store_true",
+                    help="uniform random int8 queries (few neighbours above 0.8: the pure top-k "
+                         "cascade's worst case)")
     a = ap.parse_args()
     _lib.load(a.lib)
     emb, lens, _ = make_bank_device(a.rows, 384, 4096, 0)
@@ -36,6 +39,9 @@ def main():
     w.push(emb, lens)
     del emb
     q, qi, _, _ = make_queries(a.nq, 384, 4096, 0, 1000)
+    if a.random:
+        q = np.random.default_rng(7).integers(-60, 61, (a.nq, 384)).astype(np.int8)
+        qi = inv_norm_np(q)
     dq, dqi = torch.as_tensor(q, device="cuda"), torch.as_tensor(qi, device="cuda")
     part = torch.empty(1024 * a.nq * a.k, dtype=torch.int64, device="cuda")
     ns = C.c_int32()
